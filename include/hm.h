@@ -1,0 +1,216 @@
+/*
+ * hm.h -- C-ABI of libhm: B200-native (sm_100a, FP64) accumulated-update
+ * H-matrix arithmetic after S. Boerm, "Hierarchical matrix arithmetic with
+ * accumulated updates", arXiv 1703.09085 (cited as P:L<line> of PAPER.md).
+ *
+ * Plain C99.  No C++ or torch types cross this boundary: only opaque
+ * handles, plain host/device pointers, sizes and status codes.  No
+ * exception crosses the ABI; every call returns hm_status.
+ *
+ * Data conventions (all calls)
+ *   - FP64 everywhere; dense panels and factors column-major with leading
+ *     dimension = number of rows.
+ *   - Vectors/panels exchanged with hm_matvec_thin are in TREE order
+ *     (cluster index sets are contiguous); hm_build returns the permutation
+ *     tree position -> original point index.
+ *   - Device pointers passed in are BORROWED (caller-owned, e.g. a torch
+ *     tensor's data_ptr()) and must stay valid until the stream passes the
+ *     call.  Every hm_mat and all internal pools are OWNED by the context
+ *     and released by hm_free / hm_ctx_destroy.
+ *   - Calls are stream-ordered on the context's stream.  Calls that return
+ *     host data (hm_build, hm_import, hm_export, hm_stats, hm_addmul's rank
+ *     bookkeeping) synchronize the stream.
+ *   - Errors: argument / shape errors return HM_EINVAL before any work;
+ *     X or Y aliasing Z returns HM_ESTRUCT (use hm_clone for X = Y = Z);
+ *     CUDA faults return HM_ECUDA; a message is kept in hm_last_error().
+ *   - There is no CPU fallback: every arithmetic step of hm_addmul,
+ *     hm_matvec_thin and hm_build runs in this library's sm_100a kernels.
+ */
+#ifndef HM_H_
+#define HM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hm_ctx_s* hm_ctx;
+typedef struct hm_mat_s* hm_mat;
+
+typedef enum {
+  HM_OK = 0,
+  HM_EINVAL = -1,        /* bad argument / shape */
+  HM_ENOMEM = -2,        /* device or host allocation failed */
+  HM_ECUDA = -3,         /* CUDA runtime error (incl. asynchronous faults) */
+  HM_EPIVOT = -4,        /* numerical breakdown of a leaf factorization */
+  HM_ESTRUCT = -5,       /* incompatible trees or aliasing of X/Y with Z */
+  HM_EUNSUPPORTED = -6   /* operation not available in this build */
+} hm_status;
+
+enum { HM_KERNEL_SLP = 0, HM_KERNEL_SLP_SYM = 1 };   /* G, (G + G^T)/2 */
+enum { HM_OP_G = 0, HM_OP_GT = 1 };
+
+/* Block kinds (Def 2.2 / Def 2.4). */
+enum { HM_BLOCK_SUB = 0, HM_BLOCK_ADM = 1, HM_BLOCK_DENSE = 2 };
+
+/*
+ * Flat host description of an H-matrix (cluster tree, block tree, leaf
+ * payloads).  Trees are breadth-first numbered: the sons of a node are
+ * consecutive (son0 .. son0+nsons-1), block sons row-major over
+ * sons(t) x sons(s) (Def 2.2).  Payloads:
+ *   admissible leaf b (rank k, m = #t, n = #s): A_b = factors[off .. off+m*k)
+ *     (m x k), B_b = factors[off+m*k .. off+(m+n)*k) (n x k); G|_b = A_b B_b^T
+ *   dense leaf b: N_b = dense[off .. off+m*n) (m x n)
+ * Ownership: for hm_import the arrays are caller-owned and read during the
+ * call only; for hm_export they are owned by the hm_mat and valid until the
+ * next hm_export on it or hm_free.
+ */
+typedef struct {
+  int64_t n;
+  int32_t nclusters;
+  const int32_t* cl_start;
+  const int32_t* cl_size;
+  const int32_t* cl_son0;     /* -1 for leaves */
+  const int32_t* cl_nsons;
+  const int32_t* cl_level;
+  const double* cl_bbox;      /* nclusters x 6: lo[3], hi[3] */
+  int32_t nblocks;
+  const int32_t* bl_row;      /* row cluster id t */
+  const int32_t* bl_col;      /* column cluster id s */
+  const int32_t* bl_kind;     /* HM_BLOCK_* */
+  const int32_t* bl_son0;
+  const int32_t* bl_nsons;
+  const int32_t* bl_rank;     /* admissible leaves: k; else 0 */
+  const int64_t* bl_off;      /* payload offset (doubles) or -1 */
+  const double* factors;
+  int64_t nfactors;
+  const double* dense;
+  int64_t ndense;
+  const int64_t* perm;        /* tree position -> original index (may be NULL) */
+} hm_host_desc;
+
+/* Statistics of a matrix and of the last operation of the context. */
+typedef struct {
+  int64_t n;
+  int32_t nclusters, nblocks, nadm, ndense, depth;
+  int32_t max_rank;
+  double mean_rank;
+  int64_t factor_doubles, dense_doubles;
+  /* last hm_addmul */
+  int64_t addproduct_calls;   /* = product-tree nodes */
+  int64_t evaluated_terms;
+  int64_t truncations;        /* T1 + T2 + T3 + merge truncations */
+  int64_t trunc_cols;         /* sum of stacked widths l */
+  int64_t merges;
+  int64_t dense_adds;
+  int64_t levels;
+  double flops_trunc;         /* SURVEY §8(d) convention flops */
+  double flops_eval;
+  double flops_dense;
+  double bytes_trunc;         /* SURVEY §8(d) convention bytes */
+  double bytes_eval;
+  double bytes_dense;
+} hm_stats_t;
+
+/* Per-kernel-class device timing (CUDA events on the context stream,
+ * summed over launches since hm_profile_reset). */
+#define HM_NPROF 16
+typedef struct {
+  char name[HM_NPROF][24];
+  double ms[HM_NPROF];
+  int64_t launches[HM_NPROF];
+  double flops[HM_NPROF];     /* convention flops attributed to the class */
+  double bytes[HM_NPROF];     /* convention bytes attributed to the class */
+  int32_t count;
+} hm_prof_t;
+
+/* Device memory hook; NULL -> cudaMallocAsync/cudaFreeAsync on the stream. */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* stream, void* user);
+  void (*free)(void* ptr, size_t bytes, void* stream, void* user);
+  void* user;
+} hm_allocator;
+
+/* Context: binds a device and a CUDA stream (cudaStream_t passed as void*;
+ * NULL = the legacy default stream).  One context per host thread. */
+hm_status hm_ctx_create(int device, void* cuda_stream, const hm_allocator* alloc, hm_ctx* out);
+hm_status hm_ctx_destroy(hm_ctx ctx);
+const char* hm_last_error(hm_ctx ctx);
+hm_status hm_sync(hm_ctx ctx);
+const char* hm_version(void);
+
+/*
+ * hm_build: H-matrix approximation of the BEM-like kernel matrix of
+ * BASELINE.json (G_ij = area_j/(4 pi |x_i - x_j|), G_ii = sqrt(area_i/pi)/2;
+ * HM_KERNEL_SLP_SYM: (G+G^T)/2).  Trees: bounding-box bisection (longest
+ * axis, midpoint) with leaf size `leaf_size`; admissibility
+ * max(diam_t, diam_s) <= eta dist(t,s) (squared form).  Dense leaves hold
+ * exact entries; admissible leaves TRUNC_eps(G|_b) (relative Frobenius
+ * rule), computed on the device from generated entries by a certified
+ * randomized range finder (residual <= 1e-12 ||G|_b||_F) followed by the
+ * batched TRUNC kernels.
+ *   pts_host: n x 3 row-major, area_host: n (host, read during the call)
+ *   perm_host: optional, n entries written (tree position -> original)
+ */
+hm_status hm_build(hm_ctx ctx, const double* pts_host, const double* area_host, int64_t n,
+                   int kernel, int leaf_size, double eta, double eps,
+                   hm_mat* out, int64_t* perm_host);
+
+/* hm_import: upload a flat host description (trees + payloads). */
+hm_status hm_import(hm_ctx ctx, const hm_host_desc* d, hm_mat* out);
+/* hm_export: download; pointers in *d owned by the matrix (see above). */
+hm_status hm_export(hm_ctx ctx, hm_mat m, hm_host_desc* d);
+hm_status hm_clone(hm_ctx ctx, hm_mat src, hm_mat* out);
+hm_status hm_free(hm_ctx ctx, hm_mat m);
+
+/*
+ * hm_addmul: Z <- blocktrunc(Z + alpha X Y) with accumulated updates
+ * (addproduct Fig. 5, split Fig. 6, flush Fig. 7).  X, Y, Z must
+ * share one block tree (e.g. clones); Z must not alias X or Y.  The
+ * schedule is the level-batched S2 reading: exact terms are
+ * truncated once per accumulator at split (T1) or flush (T2/T3), plus the
+ * rkmerge truncations (Fig. 4).  eps: relative Frobenius truncation
+ * tolerance per block.  Every level of the block tree is one batch of
+ * device work; the host reads back only the per-level rank arrays.
+ */
+hm_status hm_addmul(hm_ctx ctx, double alpha, hm_mat X, hm_mat Y, hm_mat Z, double eps);
+
+/* H-LR (unit lower L, upper R, in place) and H-Cholesky (lower L, in place,
+ * G + shift*I factored) with accumulated updates. */
+hm_status hm_lr(hm_ctx ctx, hm_mat G, double eps);
+hm_status hm_chol(hm_ctx ctx, hm_mat G, double eps, double shift);
+
+/*
+ * hm_matvec_thin: Y <- alpha op(G) X + beta Y (Fig. 1 addeval/addevaltrans,
+ * P:L300-334) for n x ncols device panels in tree order.
+ */
+hm_status hm_matvec_thin(hm_ctx ctx, hm_mat G, int op, double alpha, const double* x_dev,
+                         int64_t ldx, double beta, double* y_dev, int64_t ldy, int ncols);
+
+hm_status hm_stats(hm_ctx ctx, hm_mat m, hm_stats_t* out);
+
+/* Kernel-class timing with CUDA events (off by default). */
+hm_status hm_profile_enable(hm_ctx ctx, int on);
+hm_status hm_profile_reset(hm_ctx ctx);
+hm_status hm_profile_get(hm_ctx ctx, hm_prof_t* out);
+
+/*
+ * Test-only export: batched TRUNC_eps of independent stacks (kernel-level
+ * parity).  For job i: A_i (m_i x l_i, ld m_i) at a_dev + a_off[i],
+ * B_i (n_i x l_i) at b_dev + b_off[i] (device, CONSUMED: overwritten);
+ * results U_k (m_i x k) at ua_dev + o_off[i] (ld m_i) and V_k S_k
+ * (n_i x k) at ub_dev + p_off[i] (ld n_i) with capacity min(m,n,l)
+ * columns; ranks_host[i] = k.  Offsets are host arrays in doubles.
+ */
+hm_status hm_test_trunc_batched(hm_ctx ctx, int njobs, const int32_t* m, const int32_t* n,
+                                const int32_t* l, double* a_dev, const int64_t* a_off,
+                                double* b_dev, const int64_t* b_off, double* ua_dev,
+                                const int64_t* o_off, double* ub_dev, const int64_t* p_off,
+                                double eps, int32_t* ranks_host, double* sigma_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HM_H_ */

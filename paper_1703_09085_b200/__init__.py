@@ -1,0 +1,278 @@
+"""paper_1703_09085_b200 -- B200-native accumulated-update H-matrix arithmetic.
+
+Thin Python binding over the C-ABI library libhm (include/hm.h): argument
+marshalling only.  Every arithmetic step runs in libhm's sm_100a kernels;
+PyTorch supplies device memory (for user panels) and the CUDA stream.  There
+is no CPU fallback: importing this package without the built library, or
+using it without a CUDA device, raises.
+
+    ctx = Context()                       # device 0, torch's current stream
+    G = ctx.build(points, areas, leaf_size=32, eta=2.0, eps=1e-4)
+    X, Y, Z = G.clone(), G.clone(), G.clone()
+    addmul(1.0, X, Y, Z, eps=1e-4)         # Z <- blocktrunc(Z + X Y)
+    d = Z.export()                        # host description (numpy arrays)
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        _LIB = _lib.load()
+    return _LIB
+
+
+class HMError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_lib.STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+class Context:
+    """hm_ctx bound to a device and a CUDA stream."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1703_09085_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+        self.device = device
+        with torch.cuda.device(device):
+            s = stream if stream is not None else torch.cuda.current_stream(device)
+        self.stream = s
+        h = C.c_void_p()
+        st = lib().hm_ctx_create(device, C.c_void_p(s.cuda_stream), None, C.byref(h))
+        if st != 0:
+            raise HMError(st, "hm_ctx_create failed")
+        self.h = h
+
+    def check(self, st):
+        if st != 0:
+            raise HMError(st, lib().hm_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hm_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        self.check(lib().hm_sync(self.h))
+
+    # ---- construction
+    def build(self, points, areas, leaf_size, eta, eps, kernel=0):
+        pts = np.ascontiguousarray(points, dtype=np.float64)
+        ar = np.ascontiguousarray(areas, dtype=np.float64)
+        n = len(ar)
+        perm = np.empty(n, np.int64)
+        h = C.c_void_p()
+        self.check(lib().hm_build(self.h, _ptr(pts, C.c_double), _ptr(ar, C.c_double), n, int(kernel),
+                                  int(leaf_size), float(eta), float(eps), C.byref(h), _ptr(perm, C.c_int64)))
+        m = HMatrix(self, h)
+        m.perm = perm
+        return m
+
+    def import_desc(self, d):
+        keep = {}
+
+        def arr(key, dt):
+            a = np.ascontiguousarray(d[key], dtype=dt)
+            keep[key] = a
+            return a
+
+        hd = _lib.HostDesc()
+        hd.n = int(d["n"])
+        cs = arr("cl_start", np.int32)
+        hd.nclusters = len(cs)
+        hd.cl_start = _ptr(cs, C.c_int32)
+        for k in ("cl_size", "cl_son0", "cl_nsons", "cl_level"):
+            setattr(hd, k, _ptr(arr(k, np.int32), C.c_int32))
+        hd.cl_bbox = _ptr(arr("cl_bbox", np.float64), C.c_double)
+        br = arr("bl_row", np.int32)
+        hd.nblocks = len(br)
+        hd.bl_row = _ptr(br, C.c_int32)
+        for k in ("bl_col", "bl_kind", "bl_son0", "bl_nsons", "bl_rank"):
+            setattr(hd, k, _ptr(arr(k, np.int32), C.c_int32))
+        hd.bl_off = _ptr(arr("bl_off", np.int64), C.c_int64)
+        f = arr("factors", np.float64)
+        hd.factors = _ptr(f, C.c_double)
+        hd.nfactors = len(f)
+        dn = arr("dense", np.float64)
+        hd.dense = _ptr(dn, C.c_double)
+        hd.ndense = len(dn)
+        if d.get("perm") is not None:
+            hd.perm = _ptr(arr("perm", np.int64), C.c_int64)
+        h = C.c_void_p()
+        self.check(lib().hm_import(self.h, C.byref(hd), C.byref(h)))
+        m = HMatrix(self, h)
+        m.perm = keep.get("perm")
+        return m
+
+    # ---- profiling
+    def profile(self, on=True):
+        self.check(lib().hm_profile_enable(self.h, 1 if on else 0))
+
+    def profile_reset(self):
+        self.check(lib().hm_profile_reset(self.h))
+
+    def profile_get(self):
+        p = _lib.Prof()
+        self.check(lib().hm_profile_get(self.h, C.byref(p)))
+        out = {}
+        for i in range(p.count):
+            name = bytes(p.name[i]).split(b"\0", 1)[0].decode()
+            out[name] = dict(ms=p.ms[i], launches=p.launches[i], flops=p.flops[i], bytes=p.bytes[i])
+        return out
+
+    def last_stats(self):
+        s = _lib.Stats()
+        self.check(lib().hm_stats(self.h, None, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in _lib.Stats._fields_}
+
+
+class HMatrix:
+    """Opaque hm_mat owned by its context."""
+
+    def __init__(self, ctx: Context, h):
+        self.ctx = ctx
+        self.h = h
+        self.perm = None
+
+    def free(self):
+        if self.h is not None and self.ctx.h is not None:
+            self.ctx.check(lib().hm_free(self.ctx.h, self.h))
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def clone(self):
+        h = C.c_void_p()
+        self.ctx.check(lib().hm_clone(self.ctx.h, self.h, C.byref(h)))
+        m = HMatrix(self.ctx, h)
+        m.perm = self.perm
+        return m
+
+    def stats(self):
+        s = _lib.Stats()
+        self.ctx.check(lib().hm_stats(self.ctx.h, self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in _lib.Stats._fields_}
+
+    def export(self):
+        hd = _lib.HostDesc()
+        self.ctx.check(lib().hm_export(self.ctx.h, self.h, C.byref(hd)))
+        nc, nb = hd.nclusters, hd.nblocks
+
+        def cp(p, cnt, dt):
+            if not p or cnt == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(p, shape=(cnt,)).astype(dt, copy=True)
+
+        d = dict(n=np.int64(hd.n))
+        for k in ("cl_start", "cl_size", "cl_son0", "cl_nsons", "cl_level"):
+            d[k] = cp(getattr(hd, k), nc, np.int32)
+        d["cl_bbox"] = cp(hd.cl_bbox, 6 * nc, np.float64).reshape(nc, 6) if hd.cl_bbox else np.zeros((0, 6))
+        for k in ("bl_row", "bl_col", "bl_kind", "bl_son0", "bl_nsons", "bl_rank"):
+            d[k] = cp(getattr(hd, k), nb, np.int32)
+        d["bl_off"] = cp(hd.bl_off, nb, np.int64)
+        d["factors"] = cp(hd.factors, hd.nfactors, np.float64)
+        d["dense"] = cp(hd.dense, hd.ndense, np.float64)
+        d["perm"] = cp(hd.perm, hd.n, np.int64) if hd.perm else None
+        return d
+
+
+def addmul(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps):
+    """Z <- blocktrunc(Z + alpha X Y) (hm_addmul)."""
+    Z.ctx.check(lib().hm_addmul(Z.ctx.h, float(alpha), X.h, Y.h, Z.h, float(eps)))
+
+
+def matvec(G: HMatrix, x, y, alpha=1.0, beta=0.0, op=0):
+    """y <- alpha op(G) x + beta y for torch CUDA float64 tensors (n x c, column-major
+    = x.T contiguous, or 1-D)."""
+    import torch
+    assert x.is_cuda and y.is_cuda and x.dtype == torch.float64 and y.dtype == torch.float64
+    n = x.shape[0]
+    ncols = 1 if x.dim() == 1 else x.shape[1]
+    if x.dim() == 2:
+        assert x.stride(0) == 1 and y.stride(0) == 1, "panels must be column-major (stride(0) == 1)"
+        ldx, ldy = x.stride(1), y.stride(1)
+    else:
+        ldx = ldy = n
+    G.ctx.check(lib().hm_matvec_thin(G.ctx.h, G.h, int(op), float(alpha), C.c_void_p(x.data_ptr()), ldx,
+                                     float(beta), C.c_void_p(y.data_ptr()), ldy, ncols))
+
+
+def test_trunc_batched(ctx: Context, stacks, eps):
+    """Kernel-level parity export: list of (A (m x l), B (n x l)) numpy arrays ->
+    list of (U_k, V_k S_k) numpy arrays, ranks, sigmas (hm_test_trunc_batched)."""
+    import torch
+    nj = len(stacks)
+    m = np.array([a.shape[0] for a, b in stacks], np.int32)
+    n = np.array([b.shape[0] for a, b in stacks], np.int32)
+    l = np.array([a.shape[1] for a, b in stacks], np.int32)
+    kcap = np.array([max(min(min(mm, ll), min(nn, ll)), 1) for mm, nn, ll in zip(m, n, l)], np.int64)
+    a_off = np.zeros(nj, np.int64)
+    b_off = np.zeros(nj, np.int64)
+    o_off = np.zeros(nj, np.int64)
+    p_off = np.zeros(nj, np.int64)
+    ta = tb = to = tp = 0
+    for i in range(nj):
+        a_off[i], b_off[i], o_off[i], p_off[i] = ta, tb, to, tp
+        ta += int(m[i]) * int(l[i]) + 1
+        tb += int(n[i]) * int(l[i]) + 1
+        to += int(m[i]) * int(kcap[i]) + 1
+        tp += int(n[i]) * int(kcap[i]) + 1
+    dev = torch.device("cuda", ctx.device)
+    A = torch.zeros(ta, dtype=torch.float64, device=dev)
+    B = torch.zeros(tb, dtype=torch.float64, device=dev)
+    UA = torch.zeros(to, dtype=torch.float64, device=dev)
+    UB = torch.zeros(tp, dtype=torch.float64, device=dev)
+    ha = np.zeros(ta)
+    hb = np.zeros(tb)
+    for i, (a, b) in enumerate(stacks):
+        ha[a_off[i]:a_off[i] + a.size] = np.asarray(a, np.float64).ravel(order="F")
+        hb[b_off[i]:b_off[i] + b.size] = np.asarray(b, np.float64).ravel(order="F")
+    A.copy_(torch.from_numpy(ha))
+    B.copy_(torch.from_numpy(hb))
+    torch.cuda.synchronize(dev)
+    ranks = np.zeros(nj, np.int32)
+    qs = [int(min(mm, nn, ll)) for mm, nn, ll in zip(m, n, l)]
+    sig = np.zeros(max(sum(qs), 1))
+    ctx.check(lib().hm_test_trunc_batched(
+        ctx.h, nj, _ptr(m, C.c_int32), _ptr(n, C.c_int32), _ptr(l, C.c_int32),
+        C.c_void_p(A.data_ptr()), _ptr(a_off, C.c_int64), C.c_void_p(B.data_ptr()), _ptr(b_off, C.c_int64),
+        C.c_void_p(UA.data_ptr()), _ptr(o_off, C.c_int64), C.c_void_p(UB.data_ptr()), _ptr(p_off, C.c_int64),
+        float(eps), _ptr(ranks, C.c_int32), _ptr(sig, C.c_double)))
+    ua = UA.cpu().numpy()
+    ub = UB.cpu().numpy()
+    out, sigmas, o = [], [], 0
+    for i in range(nj):
+        k = int(ranks[i])
+        U = ua[o_off[i]:o_off[i] + int(m[i]) * k].reshape((int(m[i]), k), order="F")
+        V = ub[p_off[i]:p_off[i] + int(n[i]) * k].reshape((int(n[i]), k), order="F")
+        out.append((U, V))
+        sigmas.append(sig[o:o + qs[i]].copy())
+        o += qs[i]
+    return out, ranks, sigmas
+
+
+__all__ = ["Context", "HMatrix", "HMError", "addmul", "matvec", "lib", "test_trunc_batched"]

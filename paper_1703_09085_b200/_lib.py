@@ -1,0 +1,107 @@
+"""ctypes declarations of libhm (include/hm.h).  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhm.so")
+
+HM_OK, HM_EINVAL, HM_ENOMEM, HM_ECUDA, HM_EPIVOT, HM_ESTRUCT, HM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+STATUS = {0: "HM_OK", -1: "HM_EINVAL", -2: "HM_ENOMEM", -3: "HM_ECUDA", -4: "HM_EPIVOT",
+          -5: "HM_ESTRUCT", -6: "HM_EUNSUPPORTED"}
+
+P_i32 = C.POINTER(C.c_int32)
+P_i64 = C.POINTER(C.c_int64)
+P_f64 = C.POINTER(C.c_double)
+
+
+class HostDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("nclusters", C.c_int32),
+        ("cl_start", P_i32), ("cl_size", P_i32), ("cl_son0", P_i32), ("cl_nsons", P_i32),
+        ("cl_level", P_i32), ("cl_bbox", P_f64),
+        ("nblocks", C.c_int32),
+        ("bl_row", P_i32), ("bl_col", P_i32), ("bl_kind", P_i32), ("bl_son0", P_i32),
+        ("bl_nsons", P_i32), ("bl_rank", P_i32), ("bl_off", P_i64),
+        ("factors", P_f64), ("nfactors", C.c_int64),
+        ("dense", P_f64), ("ndense", C.c_int64),
+        ("perm", P_i64),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("nclusters", C.c_int32), ("nblocks", C.c_int32), ("nadm", C.c_int32),
+        ("ndense", C.c_int32), ("depth", C.c_int32),
+        ("max_rank", C.c_int32),
+        ("mean_rank", C.c_double),
+        ("factor_doubles", C.c_int64), ("dense_doubles", C.c_int64),
+        ("addproduct_calls", C.c_int64), ("evaluated_terms", C.c_int64),
+        ("truncations", C.c_int64), ("trunc_cols", C.c_int64), ("merges", C.c_int64),
+        ("dense_adds", C.c_int64), ("levels", C.c_int64),
+        ("flops_trunc", C.c_double), ("flops_eval", C.c_double), ("flops_dense", C.c_double),
+        ("bytes_trunc", C.c_double), ("bytes_eval", C.c_double), ("bytes_dense", C.c_double),
+    ]
+
+
+HM_NPROF = 16
+
+
+class Prof(C.Structure):
+    _fields_ = [
+        ("name", (C.c_char * 24) * HM_NPROF),
+        ("ms", C.c_double * HM_NPROF),
+        ("launches", C.c_int64 * HM_NPROF),
+        ("flops", C.c_double * HM_NPROF),
+        ("bytes", C.c_double * HM_NPROF),
+        ("count", C.c_int32),
+    ]
+
+
+EXPORTS = [
+    "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_build",
+    "hm_import", "hm_export", "hm_clone", "hm_free", "hm_addmul", "hm_lr", "hm_chol",
+    "hm_matvec_thin", "hm_stats", "hm_profile_enable", "hm_profile_reset", "hm_profile_get",
+    "hm_test_trunc_batched",
+]
+
+
+def load(path: str = LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError(
+            f"libhm not built: {path} is missing.  Run `make -C paper_1703_09085_b200` or "
+            "__graft_entry__.build().  There is no CPU fallback.")
+    lib = C.CDLL(path)
+    vp = C.c_void_p
+    sig = {
+        "hm_version": (C.c_char_p, []),
+        "hm_ctx_create": (C.c_int, [C.c_int, vp, vp, C.POINTER(vp)]),
+        "hm_ctx_destroy": (C.c_int, [vp]),
+        "hm_last_error": (C.c_char_p, [vp]),
+        "hm_sync": (C.c_int, [vp]),
+        "hm_build": (C.c_int, [vp, P_f64, P_f64, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,
+                               C.POINTER(vp), P_i64]),
+        "hm_import": (C.c_int, [vp, C.POINTER(HostDesc), C.POINTER(vp)]),
+        "hm_export": (C.c_int, [vp, vp, C.POINTER(HostDesc)]),
+        "hm_clone": (C.c_int, [vp, vp, C.POINTER(vp)]),
+        "hm_free": (C.c_int, [vp, vp]),
+        "hm_addmul": (C.c_int, [vp, C.c_double, vp, vp, vp, C.c_double]),
+        "hm_lr": (C.c_int, [vp, vp, C.c_double]),
+        "hm_chol": (C.c_int, [vp, vp, C.c_double, C.c_double]),
+        "hm_matvec_thin": (C.c_int, [vp, vp, C.c_int, C.c_double, vp, C.c_int64, C.c_double, vp,
+                                     C.c_int64, C.c_int]),
+        "hm_stats": (C.c_int, [vp, vp, C.POINTER(Stats)]),
+        "hm_profile_enable": (C.c_int, [vp, C.c_int]),
+        "hm_profile_reset": (C.c_int, [vp]),
+        "hm_profile_get": (C.c_int, [vp, C.POINTER(Prof)]),
+        "hm_test_trunc_batched": (C.c_int, [vp, C.c_int, P_i32, P_i32, P_i32, vp, P_i64, vp, P_i64,
+                                            vp, P_i64, vp, P_i64, C.c_double, P_i32, P_f64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib

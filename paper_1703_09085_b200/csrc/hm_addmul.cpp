@@ -1,0 +1,609 @@
+// hm_addmul: Z <- blocktrunc(Z + alpha X Y) with accumulated updates
+// (§4: addproduct Fig. 5, split Fig. 6 P:L1028-1050,
+// flush Fig. 7), executed level-synchronously.
+//
+// Accumulators of one block-tree level are processed together: the host
+// expands the pending products of level l into the accumulators of level
+// l+1 (integer work only) and emits ONE batch of device work per level:
+//   gather (copies of base / Z views, explicit factors, identities),
+//   eval   (addeval / addevaltrans over DFS leaf ranges, Fig. 1),
+//   TRUNC  (T1 reduce at split, T2 flush into admissible Z leaves, T3 flush
+//           into temporary Z~ blocks),
+//   dense  (exact N_b += A B^T for inadmissible Z leaves).
+// Then the rkmerge truncations (Fig. 4, T4) run bottom-up, one batch per
+// level.  The schedule is the S2 reading: each accumulator truncates its
+// exact stack once (DESIGN.md §3 R2), so the truncated matrices are the
+// oracle's (oracle/product.py S2).
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "hm_internal.h"
+
+namespace hm {
+namespace {
+
+enum { ZS = 0, ZA = 1, ZD = 2, ZV = 3 };
+
+struct FP {            // device factor pair; rows relative to clusters starting at t0 / r0
+  double* A;
+  double* B;
+  int lda, ldb;
+  int t0, r0;
+  int k;
+};
+
+struct Term { int bx, by, br, w; };
+struct Pend { int bx, by; };
+
+struct Node {
+  int t, r;
+  int zt, zb;
+  int base = -1;
+  std::vector<Term> terms;
+  std::vector<Pend> pend;
+  int red = -1;
+  int result = -1;
+  int child0 = -1;
+};
+
+struct Planner {
+  Ctx* c;
+  Arena persist;        // FP outputs (freed at the end of hm_addmul)
+  const Tree& T;
+  Mat *X, *Y, *Z;
+  double alpha, eps;
+  std::vector<FP> fps;
+  std::vector<std::vector<Node>> levels;
+  std::vector<int> zresult;   // real adm leaf id -> FP id
+  std::vector<LeafDesc> lx, ly;
+  LeafDesc *dlx = nullptr, *dly = nullptr;
+  // stats
+  int64_t n_addproduct = 0, n_eval = 0, n_trunc = 0, n_cols = 0, n_merge = 0, n_dense = 0;
+  double fl_trunc = 0, by_trunc = 0, fl_eval = 0, by_eval = 0, fl_dense = 0, by_dense = 0;
+
+  Planner(Ctx* c_, const Tree& T_, Mat* X_, Mat* Y_, Mat* Z_, double a, double e)
+      : c(c_), persist(c_), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {}
+
+  int csize(int cl) const { return T.cl_size[cl]; }
+  int cstart(int cl) const { return T.cl_start[cl]; }
+
+  // Fig. 5 classification in printed branch order.
+  bool classify(int bx, int by, Term& out) const {
+    const int kx = T.bl_kind[bx], ky = T.bl_kind[by];
+    const int t = T.bl_row[bx], s = T.bl_col[bx], r = T.bl_col[by];
+    out.bx = bx;
+    out.by = by;
+    if (kx == HM_BLOCK_DENSE) {
+      if (csize(t) <= csize(s)) { out.br = 0; out.w = csize(t); }
+      else { out.br = 1; out.w = csize(s); }
+    } else if (ky == HM_BLOCK_DENSE) {
+      if (csize(r) <= csize(s)) { out.br = 2; out.w = csize(r); }
+      else { out.br = 3; out.w = csize(s); }
+    } else if (kx == HM_BLOCK_ADM) {
+      out.br = 4; out.w = X->rank[bx];
+    } else if (ky == HM_BLOCK_ADM) {
+      out.br = 5; out.w = Y->rank[by];
+    } else {
+      return false;
+    }
+    return true;
+  }
+
+  void addproduct(Node& nd, int bx, int by) {
+    n_addproduct++;
+    Term tm;
+    if (classify(bx, by, tm)) { nd.terms.push_back(tm); n_eval++; }
+    else nd.pend.push_back(Pend{bx, by});
+  }
+
+  FP zview(int zb) const {
+    FP f;
+    f.A = Z->pA[zb];
+    f.B = Z->pB[zb];
+    f.lda = csize(T.bl_row[zb]);
+    f.ldb = csize(T.bl_col[zb]);
+    f.t0 = cstart(T.bl_row[zb]);
+    f.r0 = cstart(T.bl_col[zb]);
+    f.k = Z->rank[zb];
+    return f;
+  }
+
+  int new_fp(int m, int n, int kcap, int t0, int r0) {
+    FP f;
+    f.A = persist.alloc((size_t)m * std::max(kcap, 1));
+    f.B = persist.alloc((size_t)n * std::max(kcap, 1));
+    f.lda = m;
+    f.ldb = n;
+    f.t0 = t0;
+    f.r0 = r0;
+    f.k = -1;
+    fps.push_back(f);
+    return (int)fps.size() - 1;
+  }
+
+  // ------------------------------------------------------------ level batch
+  struct Stack {
+    int node;
+    int kind;      // 1 T1, 2 T2/T3, 3 dense
+    int m, n, l;
+    double *A, *B;
+    int out = -1;  // FP id
+  };
+
+  void add_copy(std::vector<CopyJob>& cj, int64_t& tiles, double* dst, int ldd, const double* src,
+                int lds, int rows, int cols, int trans, int identity, double coef) {
+    if (rows <= 0 || cols <= 0) return;
+    CopyJob j{};
+    j.dst = dst; j.src = src; j.ldd = ldd; j.lds = lds; j.rows = rows; j.cols = cols;
+    j.trans = trans; j.identity = identity; j.accumulate = 0; j.coef = coef; j.tile0 = tiles;
+    tiles += (int64_t)((rows + 31) / 32) * ((cols + 31) / 32);
+    cj.push_back(j);
+  }
+
+  void add_eval(std::vector<EvalJob>& ej, bool yside, int blk, double coef, double* out, int ldo,
+                int w, const double* V, int ldv, int vtrans, int videntity) {
+    if (w <= 0) return;
+    EvalJob e{};
+    e.leaves = yside ? dly : dlx;
+    e.leaf_begin = T.bl_lbeg[blk];
+    e.leaf_end = T.bl_lend[blk];
+    e.trans = yside ? 1 : 0;
+    e.t0 = cstart(T.bl_row[blk]);
+    e.s0 = cstart(T.bl_col[blk]);
+    e.coef = coef;
+    e.out = out;
+    e.ldo = ldo;
+    e.w = w;
+    e.V = V;
+    e.ldv = ldv;
+    e.vtrans = vtrans;
+    e.videntity = videntity;
+    const std::vector<LeafDesc>& lt = yside ? ly : lx;
+    double fl = 0, by = 0;
+    for (int i = e.leaf_begin; i < e.leaf_end; i++) {
+      const LeafDesc& L = lt[i];
+      if (L.kind == HM_BLOCK_DENSE) {
+        fl += 2.0 * L.m * L.n * w;
+        by += 8.0 * ((double)L.m * L.n + (double)(L.m + L.n) * w);
+      } else {
+        fl += 2.0 * L.k * (double)(L.m + L.n) * w;
+        by += 8.0 * ((double)L.k * (L.m + L.n) + (double)(L.m + L.n) * w);
+      }
+    }
+    if (videntity) fl = 0;   // expansion: a copy, not arithmetic
+    fl_eval += fl;
+    by_eval += by;
+    e.cost = (int64_t)(by + fl);
+    ej.push_back(e);
+  }
+
+  // Emit the A2 realisation of one evaluated term into stack columns [col, col+w).
+  void emit_term(const Term& tm, double* SA, int m, double* SB, int n, int col,
+                 std::vector<CopyJob>& cj, int64_t& ctiles, std::vector<EvalJob>& ej) {
+    const int bx = tm.bx, by = tm.by, w = tm.w;
+    const int t = T.bl_row[bx], s = T.bl_col[bx], r = T.bl_col[by];
+    const int nt = csize(t), ns = csize(s), nr = csize(r);
+    double* a = SA + (size_t)col * m;
+    double* b = SB + (size_t)col * n;
+    switch (tm.br) {
+      case 0:  // A = alpha I_t ; B = Y|sr^T N_X^T
+        add_copy(cj, ctiles, a, m, nullptr, 0, nt, nt, 0, 1, alpha);
+        add_eval(ej, true, by, 1.0, b, n, w, X->pA[bx], nt, 1, 0);
+        break;
+      case 1:  // A = alpha N_X ; B = Y|sr^T I
+        add_copy(cj, ctiles, a, m, X->pA[bx], nt, nt, ns, 0, 0, alpha);
+        add_eval(ej, true, by, 1.0, b, n, w, nullptr, 0, 0, 1);
+        break;
+      case 2:  // B = I_r ; A = alpha X|ts N_Y
+        add_copy(cj, ctiles, b, n, nullptr, 0, nr, nr, 0, 1, 1.0);
+        add_eval(ej, false, bx, alpha, a, m, w, Y->pA[by], ns, 0, 0);
+        break;
+      case 3:  // B = N_Y^T ; A = alpha X|ts I
+        add_copy(cj, ctiles, b, n, Y->pA[by], ns, nr, ns, 1, 0, 1.0);
+        add_eval(ej, false, bx, alpha, a, m, w, nullptr, 0, 0, 1);
+        break;
+      case 4:  // A = alpha A_X ; B = Y|sr^T B_X
+        add_copy(cj, ctiles, a, m, X->pA[bx], nt, nt, w, 0, 0, alpha);
+        add_eval(ej, true, by, 1.0, b, n, w, X->pB[bx], ns, 0, 0);
+        break;
+      case 5:  // B = B_Y ; A = alpha X|ts A_Y
+        add_copy(cj, ctiles, b, n, Y->pB[by], nr, nr, w, 0, 0, 1.0);
+        add_eval(ej, false, bx, alpha, a, m, w, Y->pA[by], ns, 0, 0);
+        break;
+    }
+  }
+
+  void copy_view(const FP& f, int t, int r, double* SA, int m, double* SB, int n, int col,
+                 std::vector<CopyJob>& cj, int64_t& ctiles) {
+    if (f.k <= 0) return;
+    add_copy(cj, ctiles, SA + (size_t)col * m, m, f.A + (cstart(t) - f.t0), f.lda, m, f.k, 0, 0, 1.0);
+    add_copy(cj, ctiles, SB + (size_t)col * n, n, f.B + (cstart(r) - f.r0), f.ldb, n, f.k, 0, 0, 1.0);
+  }
+
+  void sync_ranks(int* d_ranks, const std::vector<int>& fp_ids) {
+    if (fp_ids.empty()) return;
+    std::vector<int> h(fp_ids.size());
+    HM_CUDA(cudaStreamSynchronize(c->stream));
+    HM_CUDA(cudaMemcpy(h.data(), d_ranks, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < fp_ids.size(); i++) fps[fp_ids[i]].k = h[i];
+  }
+
+  void run_level(std::vector<Node>& nodes) {
+    Arena scratch(c);
+    std::vector<Stack> stacks;
+    for (int i = 0; i < (int)nodes.size(); i++) {
+      Node& nd = nodes[i];
+      const int m = csize(nd.t), n = csize(nd.r);
+      int kind = 0, l = 0;
+      const int kb = nd.base >= 0 ? fps[nd.base].k : 0;
+      int wt = 0;
+      for (auto& tm : nd.terms) wt += tm.w;
+      if (!nd.pend.empty()) {
+        if (nd.zt == ZD)
+          throw Error(HM_ESTRUCT, "flush: pending products into an inadmissible leaf");
+        if (!nd.terms.empty()) { kind = 1; l = kb + wt; }
+        else nd.red = nd.base;
+      } else if (nd.zt == ZA || nd.zt == ZV) {
+        kind = 2;
+        l = zview(nd.zb).k + kb + wt;
+      } else if (nd.zt == ZD) {
+        if (kb + wt > 0) { kind = 3; l = kb + wt; }
+      } else {
+        throw Error(HM_EUNSUPPORTED, "flush branch (iii) into a subdivided block with P = 0");
+      }
+      if (kind) stacks.push_back(Stack{i, kind, m, n, l, nullptr, nullptr, -1});
+    }
+    if (stacks.empty()) return;
+    size_t total = 0;
+    for (auto& s : stacks) total += (size_t)(s.m + s.n) * s.l;
+    double* buf = scratch.alloc(total + 1);
+    {
+      ProfScope ps(c, PC_MEMSET, 0, 8.0 * total);
+      HM_CUDA(cudaMemsetAsync(buf, 0, total * sizeof(double), c->stream));
+    }
+    size_t off = 0;
+    for (auto& s : stacks) {
+      s.A = buf + off;
+      off += (size_t)s.m * s.l;
+      s.B = buf + off;
+      off += (size_t)s.n * s.l;
+    }
+    std::vector<CopyJob> cj;
+    std::vector<EvalJob> ej;
+    int64_t ctiles = 0;
+    for (auto& s : stacks) {
+      Node& nd = nodes[s.node];
+      int col = 0;
+      if (s.kind == 2) {
+        FP zf = zview(nd.zb);
+        copy_view(zf, nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
+        col += zf.k;
+      }
+      if (nd.base >= 0) {
+        copy_view(fps[nd.base], nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
+        col += fps[nd.base].k;
+      }
+      for (auto& tm : nd.terms) {
+        emit_term(tm, s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
+        col += tm.w;
+      }
+    }
+    {
+      double cb = 0;
+      for (auto& j : cj) cb += 16.0 * j.rows * (j.identity ? 1 : j.cols);
+      ProfScope ps(c, PC_COPY, 0, cb);
+      launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
+      HM_CHECK_LAUNCH();
+    }
+    if (!ej.empty()) {
+      std::stable_sort(ej.begin(), ej.end(),
+                       [](const EvalJob& a, const EvalJob& b) { return a.cost > b.cost; });
+      double fl = 0, by = 0;
+      ProfScope ps(c, PC_EVAL, fl, by);
+      launch_eval(scratch.upload(ej), (int)ej.size(), c->stream);
+      HM_CHECK_LAUNCH();
+    }
+    // truncations and dense adds
+    std::vector<TruncReq> tr;
+    std::vector<int> tr_fp;
+    std::vector<GemmJob> gj;
+    int64_t gtiles = 0;
+    int* d_ranks = static_cast<int*>(scratch.alloc_bytes(sizeof(int) * (stacks.size() + 1)));
+    for (auto& s : stacks) {
+      Node& nd = nodes[s.node];
+      if (s.kind == 3) {
+        GemmJob g{};
+        g.A = s.A; g.lda = s.m; g.transA = 0;
+        g.B = s.B; g.ldb = s.n; g.transB = 1;
+        g.C = Z->pA[nd.zb]; g.ldc = s.m;
+        g.m = s.m; g.n = s.n; g.k = s.l;
+        g.alpha = 1.0; g.beta = 1.0;
+        g.tile0 = gtiles;
+        gtiles += (int64_t)((s.m + 63) / 64) * ((s.n + 63) / 64);
+        gj.push_back(g);
+        n_dense++;
+        fl_dense += 2.0 * s.m * s.n * s.l;
+        by_dense += 8.0 * ((double)(s.m + s.n) * s.l + 2.0 * s.m * s.n);
+        continue;
+      }
+      const int kcap = trunc_kcap(s.m, s.n, s.l);
+      const int out = new_fp(s.m, s.n, kcap, cstart(nd.t), cstart(nd.r));
+      s.out = out;
+      TruncReq q{s.m, s.n, s.l, s.A, s.B, fps[out].A, fps[out].B, d_ranks + tr.size(), nullptr};
+      tr.push_back(q);
+      tr_fp.push_back(out);
+      if (s.kind == 1) nd.red = out;
+      else nd.result = out;
+    }
+    if (!gj.empty()) {
+      ProfScope ps(c, PC_DENSE, 0, 0);
+      launch_gemm(scratch.upload(gj), (int)gj.size(), gtiles, c->stream);
+      HM_CHECK_LAUNCH();
+    }
+    trunc_batched(c, scratch, tr, eps);
+    sync_ranks(d_ranks, tr_fp);
+    for (size_t i = 0; i < tr.size(); i++) {
+      const double k = fps[tr_fp[i]].k;
+      fl_trunc += trunc_flops(tr[i].m, tr[i].n, tr[i].l, k);
+      by_trunc += trunc_bytes(tr[i].m, tr[i].n, tr[i].l, k);
+      n_cols += tr[i].l;
+    }
+    n_trunc += (int64_t)tr.size();
+    for (auto& s : stacks) {
+      Node& nd = nodes[s.node];
+      if (s.kind == 2 && nd.zt == ZA) zresult[nd.zb] = nd.result;
+    }
+    scratch.release();
+  }
+
+  // Fig. 6 split for every node with pending products -> next level.
+  std::vector<Node> split_level(std::vector<Node>& nodes) {
+    std::vector<Node> next;
+    for (auto& nd : nodes) {
+      if (nd.pend.empty()) continue;
+      const int t = nd.t, r = nd.r;
+      const int nts = T.cl_nsons[t], nrs = T.cl_nsons[r];
+      nd.child0 = (int)next.size();
+      for (int i = 0; i < nts; i++) {
+        for (int j = 0; j < nrs; j++) {
+          Node ch;
+          ch.t = T.cl_son0[t] + i;
+          ch.r = T.cl_son0[r] + j;
+          if (nd.zt == ZS) {
+            const int zb = T.son(nd.zb, i, j);
+            ch.zb = zb;
+            ch.zt = T.bl_kind[zb] == HM_BLOCK_SUB ? ZS : (T.bl_kind[zb] == HM_BLOCK_ADM ? ZA : ZD);
+          } else {
+            ch.zt = ZV;
+            ch.zb = nd.zb;   // the real admissible leaf the temporaries restrict
+          }
+          ch.base = nd.red;
+          for (auto& p : nd.pend) {
+            const int s = T.bl_col[p.bx];
+            for (int l = 0; l < T.cl_nsons[s]; l++)
+              addproduct(ch, T.son(p.bx, i, l), T.son(p.by, l, j));
+          }
+          next.push_back(std::move(ch));
+        }
+      }
+    }
+    return next;
+  }
+
+  // Fig. 4 rkmerge of the temporaries below admissible leaves, bottom-up.
+  void merges() {
+    for (int lev = (int)levels.size() - 2; lev >= 0; lev--) {
+      std::vector<int> mn;
+      for (int i = 0; i < (int)levels[lev].size(); i++) {
+        const Node& nd = levels[lev][i];
+        if (!nd.pend.empty() && (nd.zt == ZA || nd.zt == ZV)) mn.push_back(i);
+      }
+      if (mn.empty()) continue;
+      std::vector<Node>& kids = levels[lev + 1];
+      // stage a: block columns (exact vertical stacks)
+      std::vector<std::vector<int>> colfp(mn.size());
+      for (int stage = 0; stage < 2; stage++) {
+        Arena scratch(c);
+        struct S { int m, n, l; double *A, *B; int out; };
+        std::vector<S> ss;
+        std::vector<CopyJob> cj;
+        int64_t ctiles = 0;
+        std::vector<std::pair<int, int>> who;   // (merge idx, column j) for stage a
+        size_t total = 0;
+        std::vector<S> pre;
+        for (size_t mi = 0; mi < mn.size(); mi++) {
+          const Node& nd = levels[lev][mn[mi]];
+          const int nts = T.cl_nsons[nd.t], nrs = T.cl_nsons[nd.r];
+          if (stage == 0) {
+            for (int j = 0; j < nrs; j++) {
+              int l = 0;
+              for (int i = 0; i < nts; i++) l += fps[kids[nd.child0 + i * nrs + j].result].k;
+              pre.push_back(S{csize(nd.t), csize(T.cl_son0[nd.r] + j), l, nullptr, nullptr, -1});
+              who.push_back({(int)mi, j});
+            }
+          } else {
+            int l = 0;
+            for (int j = 0; j < nrs; j++) l += fps[colfp[mi][j]].k;
+            pre.push_back(S{csize(nd.t), csize(nd.r), l, nullptr, nullptr, -1});
+            who.push_back({(int)mi, -1});
+          }
+        }
+        for (auto& s : pre) total += (size_t)(s.m + s.n) * s.l;
+        double* buf = scratch.alloc(total + 1);
+        HM_CUDA(cudaMemsetAsync(buf, 0, total * sizeof(double), c->stream));
+        size_t off = 0;
+        for (auto& s : pre) {
+          s.A = buf + off; off += (size_t)s.m * s.l;
+          s.B = buf + off; off += (size_t)s.n * s.l;
+        }
+        for (size_t w = 0; w < pre.size(); w++) {
+          S& s = pre[w];
+          const Node& nd = levels[lev][mn[who[w].first]];
+          const int nts = T.cl_nsons[nd.t], nrs = T.cl_nsons[nd.r];
+          int col = 0;
+          if (stage == 0) {
+            const int j = who[w].second;
+            for (int i = 0; i < nts; i++) {
+              const FP& f = fps[kids[nd.child0 + i * nrs + j].result];
+              const int ti = T.cl_son0[nd.t] + i;
+              const int ro = cstart(ti) - cstart(nd.t);
+              if (f.k > 0) {
+                add_copy(cj, ctiles, s.A + ro + (size_t)col * s.m, s.m, f.A, f.lda, csize(ti), f.k, 0, 0, 1.0);
+                add_copy(cj, ctiles, s.B + (size_t)col * s.n, s.n, f.B, f.ldb, s.n, f.k, 0, 0, 1.0);
+              }
+              col += f.k;
+            }
+          } else {
+            const int mi = who[w].first;
+            for (int j = 0; j < nrs; j++) {
+              const FP& f = fps[colfp[mi][j]];
+              const int rj = T.cl_son0[nd.r] + j;
+              const int co = cstart(rj) - cstart(nd.r);
+              if (f.k > 0) {
+                add_copy(cj, ctiles, s.A + (size_t)col * s.m, s.m, f.A, f.lda, s.m, f.k, 0, 0, 1.0);
+                add_copy(cj, ctiles, s.B + co + (size_t)col * s.n, s.n, f.B, f.ldb, csize(rj), f.k, 0, 0, 1.0);
+              }
+              col += f.k;
+            }
+          }
+        }
+        {
+          ProfScope ps(c, PC_COPY, 0, 0);
+          launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
+          HM_CHECK_LAUNCH();
+        }
+        std::vector<TruncReq> tr;
+        std::vector<int> tr_fp;
+        int* d_ranks = static_cast<int*>(scratch.alloc_bytes(sizeof(int) * (pre.size() + 1)));
+        for (size_t w = 0; w < pre.size(); w++) {
+          S& s = pre[w];
+          const Node& nd = levels[lev][mn[who[w].first]];
+          const int r0 = stage == 0 ? cstart(T.cl_son0[nd.r] + who[w].second) : cstart(nd.r);
+          const int out = new_fp(s.m, s.n, trunc_kcap(s.m, s.n, s.l), cstart(nd.t), r0);
+          s.out = out;
+          tr.push_back(TruncReq{s.m, s.n, s.l, s.A, s.B, fps[out].A, fps[out].B, d_ranks + tr.size(), nullptr});
+          tr_fp.push_back(out);
+        }
+        trunc_batched(c, scratch, tr, eps);
+        sync_ranks(d_ranks, tr_fp);
+        for (size_t i = 0; i < tr.size(); i++) {
+          const double k = fps[tr_fp[i]].k;
+          fl_trunc += trunc_flops(tr[i].m, tr[i].n, tr[i].l, k);
+          by_trunc += trunc_bytes(tr[i].m, tr[i].n, tr[i].l, k);
+          n_cols += tr[i].l;
+        }
+        n_trunc += (int64_t)tr.size();
+        for (size_t w = 0; w < pre.size(); w++) {
+          const int mi = who[w].first;
+          if (stage == 0) colfp[mi].push_back(pre[w].out);
+          else {
+            Node& nd = levels[lev][mn[mi]];
+            nd.result = pre[w].out;
+            if (nd.zt == ZA) zresult[nd.zb] = nd.result;
+          }
+        }
+        scratch.release();
+      }
+      n_merge += (int64_t)mn.size();
+    }
+  }
+
+  void finish() {
+    // compact the new admissible-leaf factors of Z into one owned pool
+    size_t total = 0;
+    const int nb = T.nblocks();
+    for (int b = 0; b < nb; b++) {
+      if (T.bl_kind[b] != HM_BLOCK_ADM) continue;
+      if (zresult[b] < 0) throw Error(HM_ESTRUCT, "internal: admissible Z leaf without update");
+      const FP& f = fps[zresult[b]];
+      total += (size_t)(f.lda + f.ldb) * f.k;
+    }
+    double* pool = static_cast<double*>(c->dmalloc((total + 1) * sizeof(double)));
+    std::vector<CopyJob> cj;
+    int64_t ctiles = 0;
+    size_t off = 0;
+    std::vector<double*> nA(nb, nullptr), nB(nb, nullptr);
+    std::vector<int> nk(nb, 0);
+    for (int b = 0; b < nb; b++) {
+      if (T.bl_kind[b] != HM_BLOCK_ADM) continue;
+      const FP& f = fps[zresult[b]];
+      nA[b] = pool + off;
+      off += (size_t)f.lda * f.k;
+      nB[b] = pool + off;
+      off += (size_t)f.ldb * f.k;
+      nk[b] = f.k;
+      add_copy(cj, ctiles, nA[b], f.lda, f.A, f.lda, f.lda, f.k, 0, 0, 1.0);
+      add_copy(cj, ctiles, nB[b], f.ldb, f.B, f.ldb, f.ldb, f.k, 0, 0, 1.0);
+    }
+    Arena scratch(c);
+    launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
+    HM_CHECK_LAUNCH();
+    HM_CUDA(cudaStreamSynchronize(c->stream));
+    scratch.release();
+    // release Z's old factor pool (the dense pool stays: updated in place)
+    c->dfree(Z->fpool.first, Z->fpool.second);
+    for (int b = 0; b < nb; b++) {
+      if (T.bl_kind[b] != HM_BLOCK_ADM) continue;
+      Z->pA[b] = nA[b];
+      Z->pB[b] = nB[b];
+      Z->rank[b] = nk[b];
+    }
+    Z->fpool = {pool, (total + 1) * sizeof(double)};
+  }
+
+  void run() {
+    zresult.assign(T.nblocks(), -1);
+    lx = leaf_table(*X);
+    ly = leaf_table(*Y);
+    dlx = persist.upload(lx);
+    dly = persist.upload(ly);
+    Node root;
+    root.t = T.bl_row[0];
+    root.r = T.bl_col[0];
+    root.zb = 0;
+    root.zt = T.bl_kind[0] == HM_BLOCK_SUB ? ZS : (T.bl_kind[0] == HM_BLOCK_ADM ? ZA : ZD);
+    addproduct(root, 0, 0);
+    levels.push_back({});
+    levels.back().push_back(std::move(root));
+    while (true) {
+      run_level(levels.back());
+      std::vector<Node> next = split_level(levels.back());
+      if (next.empty()) break;
+      levels.push_back(std::move(next));
+    }
+    merges();
+    finish();
+  }
+};
+
+}  // namespace
+
+void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps) {
+  if (!X || !Y || !Z) throw Error(HM_EINVAL, "hm_addmul: null matrix");
+  if (Z == X || Z == Y) throw Error(HM_ESTRUCT, "hm_addmul: Z aliases X or Y (use hm_clone)");
+  if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_addmul: eps must be >= 0");
+  const Tree& T = *Z->tree;
+  if (!(X->tree->same_structure(T) && Y->tree->same_structure(T)))
+    throw Error(HM_ESTRUCT, "hm_addmul: X, Y and Z must share one block tree");
+  Planner P(c, T, X, Y, Z, alpha, eps);
+  P.run();
+  hm_stats_t& s = c->last;
+  s.addproduct_calls = P.n_addproduct;
+  s.evaluated_terms = P.n_eval;
+  s.truncations = P.n_trunc;
+  s.trunc_cols = P.n_cols;
+  s.merges = P.n_merge;
+  s.dense_adds = P.n_dense;
+  s.levels = (int64_t)P.levels.size();
+  s.flops_trunc = P.fl_trunc;
+  s.bytes_trunc = P.by_trunc;
+  s.flops_eval = P.fl_eval;
+  s.bytes_eval = P.by_eval;
+  s.flops_dense = P.fl_dense;
+  s.bytes_dense = P.by_dense;
+  P.persist.release();
+  HM_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace hm

@@ -1,0 +1,121 @@
+// Context, device arena, profiling and matrix bookkeeping of libhm.
+#include <cstdlib>
+#include <cstring>
+
+#include "hm_internal.h"
+
+namespace hm {
+
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HM_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+void* Ctx::dmalloc(size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  void* p = nullptr;
+  if (has_alloc) {
+    p = alloc.alloc(bytes, stream, alloc.user);
+    if (!p) throw Error(HM_ENOMEM, "device allocation hook failed (" + std::to_string(bytes) + " B)");
+    return p;
+  }
+  cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(HM_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  return p;
+}
+
+void Ctx::dfree(void* p, size_t bytes) {
+  if (!p) return;
+  if (has_alloc) {
+    alloc.free(p, bytes, stream, alloc.user);
+    return;
+  }
+  cudaFreeAsync(p, stream);
+}
+
+cudaEvent_t Ctx::get_event() {
+  if (!free_events.empty()) {
+    cudaEvent_t e = free_events.back();
+    free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  HM_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::prof_begin(int cls, cudaEvent_t* a) {
+  (void)cls;
+  if (!prof) return;
+  *a = get_event();
+  HM_CUDA(cudaEventRecord(*a, stream));
+}
+
+void Ctx::prof_end(int cls, cudaEvent_t a, double fl, double by) {
+  if (!prof || !a) return;
+  cudaEvent_t b = get_event();
+  cudaEventRecord(b, stream);
+  pend.push_back(Pending{cls, a, b, fl, by});
+  if (pend.size() > 4096) prof_collect();
+}
+
+void Ctx::prof_collect() {
+  for (auto& p : pend) {
+    cudaEventSynchronize(p.b);
+    float ms_ = 0.f;
+    cudaEventElapsedTime(&ms_, p.a, p.b);
+    ms[p.cls] += ms_;
+    launches[p.cls] += 1;
+    flops[p.cls] += p.flops;
+    bytes[p.cls] += p.bytes;
+    free_events.push_back(p.a);
+    free_events.push_back(p.b);
+  }
+  pend.clear();
+}
+
+void* Arena::alloc_bytes(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  void* p = ctx->dmalloc(bytes);
+  blocks.push_back({p, bytes});
+  return p;
+}
+
+void Arena::release() {
+  for (auto& b : blocks) ctx->dfree(b.first, b.second);
+  blocks.clear();
+}
+
+void Mat::free_all(Ctx* c) {
+  c->dfree(fpool.first, fpool.second);
+  c->dfree(dpool.first, dpool.second);
+  fpool = {nullptr, 0};
+  dpool = {nullptr, 0};
+}
+
+std::vector<LeafDesc> leaf_table(const Mat& M) {
+  const Tree& T = *M.tree;
+  std::vector<LeafDesc> v(T.leaf_order.size());
+  for (size_t i = 0; i < T.leaf_order.size(); i++) {
+    const int b = T.leaf_order[i];
+    LeafDesc& d = v[i];
+    d.kind = T.bl_kind[b];
+    d.row0 = T.cl_start[T.bl_row[b]];
+    d.col0 = T.cl_start[T.bl_col[b]];
+    d.m = T.cl_size[T.bl_row[b]];
+    d.n = T.cl_size[T.bl_col[b]];
+    d.k = (d.kind == HM_BLOCK_ADM) ? M.rank[b] : 0;
+    d.A = M.pA[b];
+    d.B = M.pB[b];
+  }
+  return v;
+}
+
+}  // namespace hm

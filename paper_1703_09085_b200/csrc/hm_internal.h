@@ -1,0 +1,162 @@
+// libhm internals: context, trees, matrices, device arena, profiling.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hm.h"
+#include "kernels.h"
+
+namespace hm {
+
+struct Error : std::runtime_error {
+  hm_status code;
+  Error(hm_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define HM_CUDA(call)                                                                 \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw ::hm::Error(HM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+bool debug_sync();   // HM_DEBUG_SYNC=1: synchronize and check after every launch
+
+#define HM_CHECK_LAUNCH()                                                                      \
+  do {                                                                                         \
+    HM_CUDA(cudaGetLastError());                                                               \
+    if (::hm::debug_sync()) {                                                                  \
+      cudaError_t e2_ = cudaDeviceSynchronize();                                               \
+      if (e2_ != cudaSuccess)                                                                  \
+        throw ::hm::Error(HM_ECUDA, std::string(__FILE__) + ":" + std::to_string(__LINE__) + \
+                                        ": " + cudaGetErrorString(e2_));                       \
+    }                                                                                          \
+  } while (0)
+
+enum ProfClass {
+  PC_QR = 0, PC_GEMM_M, PC_SVD, PC_APPLYQ, PC_COPY, PC_EVAL, PC_DENSE, PC_MEMSET,
+  PC_GEN, PC_BUILD_GEMM, PC_NORM, PC_MATVEC, PC_COUNT
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  hm_allocator alloc{};
+  bool has_alloc = false;
+  std::string err;
+  hm_stats_t last{};
+  // profiling
+  bool prof = false;
+  struct Pending { int cls; cudaEvent_t a, b; double flops, bytes; };
+  std::vector<Pending> pend;
+  std::vector<cudaEvent_t> free_events;
+  double ms[PC_COUNT] = {0};
+  int64_t launches[PC_COUNT] = {0};
+  double flops[PC_COUNT] = {0};
+  double bytes[PC_COUNT] = {0};
+
+  void* dmalloc(size_t bytes);
+  void dfree(void* p, size_t bytes);
+  cudaEvent_t get_event();
+  void prof_begin(int cls, cudaEvent_t* a);
+  void prof_end(int cls, cudaEvent_t a, double flops, double bytes);
+  void prof_collect();   // synchronizes pending events
+};
+
+// Stream-ordered device arena: every allocation is released by release().
+struct Arena {
+  Ctx* ctx;
+  std::vector<std::pair<void*, size_t>> blocks;
+  explicit Arena(Ctx* c) : ctx(c) {}
+  ~Arena() { release(); }
+  void* alloc_bytes(size_t bytes);
+  double* alloc(size_t ndoubles) { return static_cast<double*>(alloc_bytes(ndoubles * sizeof(double))); }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    if (v.empty()) return nullptr;
+    T* d = static_cast<T*>(alloc_bytes(v.size() * sizeof(T)));
+    HM_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    return d;
+  }
+  void release();
+};
+
+struct ProfScope {
+  Ctx* c;
+  int cls;
+  double fl, by;
+  cudaEvent_t a = nullptr;
+  ProfScope(Ctx* c_, int cls_, double fl_ = 0, double by_ = 0) : c(c_), cls(cls_), fl(fl_), by(by_) {
+    c->prof_begin(cls, &a);
+  }
+  ~ProfScope() { c->prof_end(cls, a, fl, by); }
+};
+
+// Cluster tree + block tree, breadth-first numbered.
+struct Tree {
+  int64_t n = 0;
+  std::vector<int32_t> cl_start, cl_size, cl_son0, cl_nsons, cl_level;
+  std::vector<double> cl_bbox;
+  std::vector<int32_t> bl_row, bl_col, bl_kind, bl_son0, bl_nsons, bl_level;
+  std::vector<int64_t> perm;
+  // derived
+  std::vector<int32_t> leaf_order;        // leaf block ids in DFS order
+  std::vector<int32_t> bl_lbeg, bl_lend;  // DFS leaf range of every block
+  int depth = 0;
+  int nclusters() const { return (int)cl_start.size(); }
+  int nblocks() const { return (int)bl_row.size(); }
+  int son(int b, int i, int j) const {   // block son (t_i, s_j)
+    return bl_son0[b] + i * cl_nsons[bl_col[b]] + j;
+  }
+  void finalize();                        // leaf ranges, depth
+  bool same_structure(const Tree& o) const;
+};
+
+std::shared_ptr<Tree> build_trees(const double* pts, int64_t n, int leaf_size, double eta);
+
+// H-matrix: leaf payload pointers into owned device allocations.
+struct Mat {
+  std::shared_ptr<Tree> tree;
+  std::vector<int32_t> rank;       // per block
+  std::vector<double*> pA, pB;     // adm: A, B ; dense: pA = N
+  std::pair<void*, size_t> fpool{nullptr, 0};   // admissible-leaf factors
+  std::pair<void*, size_t> dpool{nullptr, 0};   // inadmissible-leaf entries
+  // export staging
+  std::vector<int32_t> ex_rank;
+  std::vector<int64_t> ex_off;
+  std::vector<double> ex_factors, ex_dense;
+  // geometry kept by hm_build (for diagnostics)
+  int kernel = 0;
+  void free_all(Ctx* c);
+};
+
+std::vector<LeafDesc> leaf_table(const Mat& m);
+
+// Batched TRUNC_eps: independent stacks -> (U_k, V_k S_k), ranks on device.
+struct TruncReq {
+  int m, n, l;
+  double* A;      // m x l (ld m), consumed
+  double* B;      // n x l (ld n), consumed
+  double* Aout;   // m x kcap (ld m)
+  double* Bout;   // n x kcap (ld n)
+  int* d_rank;
+  double* d_sigma;
+};
+int trunc_kcap(int m, int n, int l);
+void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double eps);
+
+// SURVEY §8(d) convention flops/bytes of one truncation.
+double trunc_flops(double m, double n, double l, double k);
+double trunc_bytes(double m, double n, double l, double k);
+
+void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps);
+Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int kernel,
+                  int leaf_size, double eta, double eps, int64_t* perm_out);
+void matvec(Ctx* c, Mat* G, int op, double alpha, const double* x, int64_t ldx, double beta,
+            double* y, int64_t ldy, int ncols);
+
+}  // namespace hm

@@ -1,0 +1,163 @@
+// Batched TRUNC_eps (§3 "Truncation" P:L336-384, Fig. 2 rkadd
+// P:L416-436): for every stack (A, B) compute the eps-truncated SVD of the
+// exact A B^T.
+//
+// Route on the device: Householder QR of A if l < m and of B
+// if l < n (otherwise that factor is used as is), M = R_A R_B^T (p x q), one-sided
+// Jacobi SVD of M with the relative-Frobenius rank rule, then
+// A' = Q_A [U_k; 0], B' = Q_B [V_k S_k; 0].  Same exact matrix as the oracle's
+// route (QR of B, SVD of A R_B^T), so ranks and represented matrices agree up
+// to rounding.
+#include <algorithm>
+#include <cmath>
+
+#include "hm_internal.h"
+
+namespace hm {
+
+int trunc_kcap(int m, int n, int l) {
+  const int p = l < m ? l : m;
+  const int q = l < n ? l : n;
+  return std::min(p, q);
+}
+
+double trunc_flops(double m, double n, double l, double k) {
+  // QR path 2(m+n)l^2 - 4/3 l^3 + l^3/3 + 22 l^3 + 2(m+n) l k ;
+  // dense path (l >= min(m,n)): 2 m n l + 14 p q^2 + 8 q^3.
+  if (l <= 0) return 0.0;
+  if (l < std::min(m, n))
+    return 2.0 * (m + n) * l * l - (4.0 / 3.0) * l * l * l + l * l * l / 3.0 + 22.0 * l * l * l +
+           2.0 * (m + n) * l * k;
+  const double p = std::max(m, n), q = std::min(m, n);
+  return 2.0 * m * n * l + 14.0 * p * q * q + 8.0 * q * q * q;
+}
+
+double trunc_bytes(double m, double n, double l, double k) {
+  return 8.0 * (m + n) * (l + k);
+}
+
+namespace {
+int bucket_cap(int64_t need) {
+  if (need <= 3 * 1024) return 3 * 1024;
+  if (need <= 8 * 1024) return 8 * 1024;
+  if (need <= 26 * 1024) return 26 * 1024;
+  return 0;  // global path
+}
+}  // namespace
+
+void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double eps) {
+  if (reqs.empty()) return;
+  cudaStream_t st = c->stream;
+  const int nj = (int)reqs.size();
+  std::vector<int> p(nj), q(nj);
+  std::vector<char> qa(nj), qb(nj);
+  size_t tau_total = 0, m_total = 0;
+  for (int i = 0; i < nj; i++) {
+    const TruncReq& r = reqs[i];
+    qa[i] = r.l < r.m;
+    qb[i] = r.l < r.n;
+    p[i] = qa[i] ? r.l : r.m;
+    q[i] = qb[i] ? r.l : r.n;
+    if (qa[i]) tau_total += r.l;
+    if (qb[i]) tau_total += r.l;
+    m_total += (size_t)p[i] * q[i];
+  }
+  double* tau = ar.alloc(tau_total + 1);
+  double* Mbuf = ar.alloc(m_total + 1);
+  // --- QR jobs, bucketed by shared-memory need
+  std::vector<QrJob> qr_small, qr_big, qr_glob;
+  std::vector<double*> tauA(nj, nullptr), tauB(nj, nullptr), Mp(nj, nullptr);
+  size_t to = 0, mo = 0;
+  double fl_qr = 0;
+  for (int i = 0; i < nj; i++) {
+    const TruncReq& r = reqs[i];
+    Mp[i] = Mbuf + mo;
+    mo += (size_t)p[i] * q[i];
+    for (int side = 0; side < 2; side++) {
+      const bool doit = side == 0 ? qa[i] : qb[i];
+      if (!doit) continue;
+      const int rows = side == 0 ? r.m : r.n;
+      QrJob j{side == 0 ? r.A : r.B, rows, r.l, rows, tau + to, nullptr};
+      (side == 0 ? tauA : tauB)[i] = tau + to;
+      to += r.l;
+      const int64_t need = (int64_t)rows * r.l;
+      fl_qr += 2.0 * rows * r.l * r.l;
+      if (need <= 4 * 1024) qr_small.push_back(j);
+      else if (need <= qr_smem_capacity()) qr_big.push_back(j);
+      else qr_glob.push_back(j);
+    }
+  }
+  {
+    ProfScope ps(c, PC_QR, fl_qr, 0);
+    if (!qr_small.empty()) launch_qr(ar.upload(qr_small), (int)qr_small.size(), 4 * 1024, st);
+    if (!qr_big.empty()) launch_qr(ar.upload(qr_big), (int)qr_big.size(), qr_smem_capacity(), st);
+    if (!qr_glob.empty()) launch_qr(ar.upload(qr_glob), (int)qr_glob.size(), 0, st);
+    HM_CHECK_LAUNCH();
+  }
+  // --- M = R_A R_B^T
+  std::vector<GemmJob> gj;
+  gj.reserve(nj);
+  int64_t tiles = 0;
+  double fl_m = 0;
+  for (int i = 0; i < nj; i++) {
+    const TruncReq& r = reqs[i];
+    if (p[i] == 0 || q[i] == 0) continue;
+    GemmJob g{};
+    g.A = r.A; g.lda = r.m; g.transA = 0; g.maskA = qa[i];
+    g.B = r.B; g.ldb = r.n; g.transB = 1; g.maskB = qb[i];
+    g.C = Mp[i]; g.ldc = p[i];
+    g.m = p[i]; g.n = q[i]; g.k = r.l;
+    g.alpha = 1.0; g.beta = 0.0;
+    g.tile0 = tiles;
+    tiles += (int64_t)((p[i] + 63) / 64) * ((q[i] + 63) / 64);
+    fl_m += 2.0 * p[i] * q[i] * r.l;
+    gj.push_back(g);
+  }
+  {
+    ProfScope ps(c, PC_GEMM_M, fl_m, 0);
+    launch_gemm(ar.upload(gj), (int)gj.size(), tiles, st);
+    HM_CHECK_LAUNCH();
+  }
+  // --- Jacobi SVD + rank rule + U_k / V_k S_k, bucketed by smem need
+  std::vector<SvdJob> sj[4];
+  int caps[4] = {3 * 1024, 8 * 1024, 26 * 1024, 0};
+  double fl_svd = 0;
+  for (int i = 0; i < nj; i++) {
+    const TruncReq& r = reqs[i];
+    SvdJob s{};
+    s.M = Mp[i]; s.p = p[i]; s.q = q[i]; s.ldm = std::max(p[i], 1);
+    s.Aout = r.Aout; s.lda = r.m; s.ma = r.m;
+    s.Bout = r.Bout; s.ldb = r.n; s.nb = r.n;
+    s.rank = r.d_rank;
+    s.sigma = r.d_sigma;
+    const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
+    const int64_t need = (int64_t)L * cc + (int64_t)cc * cc + 2 * (int64_t)cc;
+    const int cap = bucket_cap(need);
+    fl_svd += 22.0 * (double)cc * cc * cc;
+    int b = 3;
+    for (int k = 0; k < 3; k++)
+      if (cap == caps[k]) { b = k; break; }
+    if (b == 3) s.work = ar.alloc((size_t)need);
+    sj[b].push_back(s);
+  }
+  {
+    ProfScope ps(c, PC_SVD, fl_svd, 0);
+    for (int b = 0; b < 4; b++)
+      if (!sj[b].empty()) launch_svd(ar.upload(sj[b]), (int)sj[b].size(), eps, caps[b], st);
+    HM_CHECK_LAUNCH();
+  }
+  // --- apply Q_A, Q_B
+  std::vector<ApplyQJob> aq;
+  for (int i = 0; i < nj; i++) {
+    const TruncReq& r = reqs[i];
+    if (qa[i]) aq.push_back(ApplyQJob{r.A, tauA[i], r.m, r.l, r.m, r.Aout, r.m, 0, r.d_rank});
+    if (qb[i]) aq.push_back(ApplyQJob{r.B, tauB[i], r.n, r.l, r.n, r.Bout, r.n, 0, r.d_rank});
+  }
+  {
+    ProfScope ps(c, PC_APPLYQ, 0, 0);
+    launch_applyq(ar.upload(aq), (int)aq.size(), st);
+    HM_CHECK_LAUNCH();
+  }
+}
+
+}  // namespace hm

@@ -1,0 +1,678 @@
+// Batched FP64 kernels of libhm (sm_100a).
+//
+// FP64 on B200 runs on the DFMA pipe (mma.sync f64 lowers to DMMA 8x8x4 with
+// the same peak; tcgen05 has no f64 kind -- DESIGN.md §5).  All kernels are
+// "one job list per launch": a device array of heterogeneous job
+// descriptors, one CTA (or a tile range) per job, so one launch covers a
+// whole level of the block tree (Parallelization remark).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace hm {
+
+static constexpr double kU = 1.1102230246251565e-16;  // unit roundoff 2^-53
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum for blockDim.x == 256; result broadcast to all threads.
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) red[0] = s;
+  }
+  __syncthreads();
+  s = red[0];
+  __syncthreads();
+  return s;
+}
+
+template <class J>
+__device__ __forceinline__ int find_job(const J* jobs, int njobs, int64_t tile) {
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------ GEMM
+// 64x64 output tile per CTA, K chunks of 16, 256 threads x (4x4) outputs.
+__global__ void __launch_bounds__(256) k_gemm(const GemmJob* __restrict__ jobs, int njobs) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int64_t tile = blockIdx.x;
+  const GemmJob& J = jobs[find_job(jobs, njobs, tile)];
+  const int m = J.m;
+  const int n = J.ndyn ? *J.ndyn : J.n;
+  const int k = J.kdyn ? *J.kdyn : J.k;
+  const int mt = (m + 63) >> 6;
+  const int64_t local = tile - J.tile0;
+  const int ti = (int)(local % mt), tj = (int)(local / mt);
+  if (tj * 64 >= n || ti * 64 >= m) return;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
+  for (int p0 = 0; p0 < k; p0 += 16) {
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      int i, p;
+      if (!J.transA) { i = e & 63; p = e >> 6; } else { p = e & 15; i = e >> 4; }
+      const int gi = ti * 64 + i, gp = p0 + p;
+      double v = 0.0;
+      if (gi < m && gp < k) {
+        const int r = J.transA ? gp : gi, c = J.transA ? gi : gp;
+        if (!(J.maskA && r > c)) v = J.A[r + (int64_t)c * J.lda];
+      }
+      As[p][i] = v;
+    }
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      int j, p;
+      if (!J.transB) { p = e & 15; j = e >> 4; } else { j = e & 63; p = e >> 6; }
+      const int gj = tj * 64 + j, gp = p0 + p;
+      double v = 0.0;
+      if (gj < n && gp < k) {
+        const int r = J.transB ? gj : gp, c = J.transB ? gp : gj;
+        if (!(J.maskB && r > c)) v = J.B[r + (int64_t)c * J.ldb];
+      }
+      Bs[p][j] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < 16; p++) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) { a[q] = As[p][tx + 16 * q]; b[q] = Bs[p][ty + 16 * q]; }
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int y = 0; y < 4; y++) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int y = 0; y < 4; y++) {
+    const int gj = tj * 64 + ty + 16 * y;
+    if (gj >= n) continue;
+#pragma unroll
+    for (int x = 0; x < 4; x++) {
+      const int gi = ti * 64 + tx + 16 * x;
+      if (gi >= m) continue;
+      double* c = J.C + gi + (int64_t)gj * J.ldc;
+      const double v = J.alpha * acc[x][y];
+      *c = (J.beta == 0.0) ? v : fma(J.beta, *c, v);
+    }
+  }
+}
+
+void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st) {
+  if (njobs <= 0 || ntiles <= 0) return;
+  k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs);
+}
+
+// ------------------------------------------------------------------ QR
+// Householder QR (dgeqr2) of one tall panel per CTA; in shared memory when
+// m*n <= cap, else in place in global memory.
+__global__ void __launch_bounds__(256) k_qr(const QrJob* __restrict__ jobs, int cap) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ double s_tau, s_scale;
+  const QrJob J = jobs[blockIdx.x];
+  const int m = J.m, n = J.n;
+  const bool use_sm = (int64_t)m * n <= cap;
+  double* A = use_sm ? sm : J.A;
+  const int lda = use_sm ? m : J.lda;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (use_sm) {
+    for (int64_t e = tid; e < (int64_t)m * n; e += 256) {
+      const int i = (int)(e % m), c = (int)(e / m);
+      sm[e] = J.A[i + (int64_t)c * J.lda];
+    }
+    __syncthreads();
+  }
+  for (int j = 0; j < n; j++) {
+    double* x = A + (int64_t)j * lda;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < m; i += 256) part += x[i] * x[i];
+    const double xn2 = block_sum(part, red);
+    if (tid == 0) {
+      const double alpha = x[j];
+      double tau = 0.0, scale = 0.0, beta = alpha;
+      if (xn2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      x[j] = beta;
+      J.tau[j] = tau;
+      s_tau = tau;
+      s_scale = scale;
+    }
+    __syncthreads();
+    const double tau = s_tau, scale = s_scale;
+    if (tau != 0.0)
+      for (int i = j + 1 + tid; i < m; i += 256) x[i] *= scale;
+    __syncthreads();
+    if (tau != 0.0) {
+      for (int c = j + 1 + warp; c < n; c += 8) {
+        double* y = A + (int64_t)c * lda;
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) s += x[i] * y[i];
+        s = warp_sum(s) + y[j];
+        s *= tau;
+        if (lane == 0) y[j] -= s;
+        for (int i = j + 1 + lane; i < m; i += 32) y[i] -= s * x[i];
+      }
+    }
+    __syncthreads();
+  }
+  if (use_sm) {
+    for (int64_t e = tid; e < (int64_t)m * n; e += 256) {
+      const int i = (int)(e % m), c = (int)(e / m);
+      J.A[i + (int64_t)c * J.lda] = sm[e];
+    }
+  }
+}
+
+int qr_smem_capacity() { return 24 * 1024; }
+
+void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static bool attr = false;
+  if (cap > qr_smem_capacity()) cap = qr_smem_capacity();
+  const size_t bytes = (size_t)cap * sizeof(double);
+  if (!attr) {
+    cudaFuncSetAttribute(k_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         qr_smem_capacity() * 8);
+    attr = true;
+  }
+  k_qr<<<njobs, 256, bytes, st>>>(d_jobs, cap);
+}
+
+// ------------------------------------------------------------------ apply Q
+// X <- H_0 ... H_{r-1} X ; one warp per column of X, reflectors from L2.
+__global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jobs) {
+  const ApplyQJob J = jobs[blockIdx.x];
+  const int c = J.cdyn ? *J.cdyn : J.c;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int col = warp; col < c; col += 8) {
+    double* x = J.X + (int64_t)col * J.ldx;
+    for (int j = J.r - 1; j >= 0; j--) {
+      const double tau = J.tau[j];
+      if (tau == 0.0) continue;
+      const double* v = J.V + (int64_t)j * J.ldv;
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < J.m; i += 32) s += v[i] * x[i];
+      s = (warp_sum(s) + x[j]) * tau;
+      if (lane == 0) x[j] -= s;
+      for (int i = j + 1 + lane; i < J.m; i += 32) x[i] -= s * v[i];
+      __syncwarp();
+    }
+  }
+}
+
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st) {
+  if (njobs <= 0) return;
+  k_applyq<<<njobs, 256, 0, st>>>(d_jobs);
+}
+
+// ------------------------------------------------------------------ SVD
+// One-sided (Hestenes) Jacobi on C = M or M^T (L x c, c = min(p,q)),
+// round-robin parallel ordering, one warp per column pair.
+__device__ __forceinline__ int rr_pos(int k, int r, int cp) {
+  return k == 0 ? 0 : ((k - 1 + r) % (cp - 1)) + 1;
+}
+
+__global__ void __launch_bounds__(256) k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ int s_rank;
+  const SvdJob J = jobs[blockIdx.x];
+  const int p = J.p, q = J.q;
+  const bool tr = p < q;
+  const int L = tr ? q : p, c = tr ? p : q;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (c == 0) {
+    if (tid == 0) *J.rank = 0;
+    return;
+  }
+  const int64_t need = (int64_t)L * c + (int64_t)c * c + 2 * (int64_t)c;
+  double* C = (need <= cap) ? sm : J.work;
+  double* Vr = C + (int64_t)L * c;          // accumulated rotations (c x c)
+  double* sig = Vr + (int64_t)c * c;
+  int* order = reinterpret_cast<int*>(sig + c);
+  for (int64_t e = tid; e < (int64_t)L * c; e += 256) {
+    const int i = (int)(e % L), j = (int)(e / L);
+    C[e] = tr ? J.M[j + (int64_t)i * J.ldm] : J.M[i + (int64_t)j * J.ldm];
+  }
+  for (int64_t e = tid; e < (int64_t)c * c; e += 256) Vr[e] = ((e % c) == (e / c)) ? 1.0 : 0.0;
+  __syncthreads();
+  double part = 0.0;
+  for (int64_t e = tid; e < (int64_t)L * c; e += 256) part += C[e] * C[e];
+  const double fro2 = block_sum(part, red);
+  const double tol = 2.0 * kU * sqrt((double)L);
+  const double tiny2 = (kU * kU) * fro2;   // both columns at rounding level
+  const int cp = c + (c & 1);
+  for (int sweep = 0; sweep < 80 && c > 1; sweep++) {
+    int rot = 0;
+    for (int r = 0; r < cp - 1; r++) {
+      for (int pr = warp; pr < (cp >> 1); pr += 8) {
+        const int a = rr_pos(pr, r, cp), b = rr_pos(cp - 1 - pr, r, cp);
+        if (a >= c || b >= c) continue;
+        double* x = C + (int64_t)a * L;
+        double* y = C + (int64_t)b * L;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < L; i += 32) {
+          const double xv = x[i], yv = y[i];
+          al = fma(xv, xv, al);
+          be = fma(yv, yv, be);
+          ga = fma(xv, yv, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (fabs(ga) > tol * sqrt(al) * sqrt(be) && fmax(al, be) > tiny2) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          for (int i = lane; i < L; i += 32) {
+            const double xv = x[i], yv = y[i];
+            x[i] = cs * xv - sn * yv;
+            y[i] = sn * xv + cs * yv;
+          }
+          double* u = Vr + (int64_t)a * c;
+          double* v = Vr + (int64_t)b * c;
+          for (int i = lane; i < c; i += 32) {
+            const double uv = u[i], vv = v[i];
+            u[i] = cs * uv - sn * vv;
+            v[i] = sn * uv + cs * vv;
+          }
+          rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rot)) break;   // converged: no pair rotated in this sweep
+  }
+  // singular values = column norms of C V
+  for (int j = warp; j < c; j += 8) {
+    const double* x = C + (int64_t)j * L;
+    double s = 0.0;
+    for (int i = lane; i < L; i += 32) s = fma(x[i], x[i], s);
+    s = warp_sum(s);
+    if (lane == 0) sig[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < c; j += 256) {
+    const double sj = sig[j];
+    int pos = 0;
+    for (int i = 0; i < c; i++) {
+      const double si = sig[i];
+      pos += (si > sj) || (si == sj && i < j);
+    }
+    order[pos] = j;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // rank rule (DESIGN.md §3 R1): smallest k with sum_{i>k} s_i^2 <= eps^2 sum s_i^2,
+    // tails accumulated from the smallest singular value upward.
+    double acc = 0.0;
+    for (int i = c - 1; i >= 0; i--) { const double s = sig[order[i]]; acc += s * s; }
+    const double total = acc;
+    int k = 0;
+    if (total > 0.0) {
+      const double thr = (eps * eps) * total;
+      double tail = 0.0;
+      k = c;
+      for (int kk = c; kk >= 0; kk--) {
+        if (kk < c) { const double s = sig[order[kk]]; tail += s * s; }
+        if (tail <= thr) k = kk; else break;
+      }
+    }
+    s_rank = k;
+    *J.rank = k;
+  }
+  __syncthreads();
+  const int k = s_rank;
+  if (J.sigma)
+    for (int i = tid; i < c; i += 256) J.sigma[i] = sig[order[i]];
+  if (!tr) {
+    // C V = M V = U Sigma:  A = U_k = (C V)_k / sigma ; B = V_k Sigma_k
+    for (int64_t e = tid; e < (int64_t)J.ma * k; e += 256) {
+      const int r = (int)(e % J.ma), i = (int)(e / J.ma);
+      const int j = order[i];
+      J.Aout[r + (int64_t)i * J.lda] = (r < p) ? C[r + (int64_t)j * L] / sig[j] : 0.0;
+    }
+    for (int64_t e = tid; e < (int64_t)J.nb * k; e += 256) {
+      const int r = (int)(e % J.nb), i = (int)(e / J.nb);
+      const int j = order[i];
+      J.Bout[r + (int64_t)i * J.ldb] = (r < q) ? Vr[r + (int64_t)j * c] * sig[j] : 0.0;
+    }
+  } else {
+    // C V = M^T V = V_M Sigma:  A = U_k = V_k(rotations) ; B = (C V)_k
+    for (int64_t e = tid; e < (int64_t)J.ma * k; e += 256) {
+      const int r = (int)(e % J.ma), i = (int)(e / J.ma);
+      J.Aout[r + (int64_t)i * J.lda] = (r < p) ? Vr[r + (int64_t)order[i] * c] : 0.0;
+    }
+    for (int64_t e = tid; e < (int64_t)J.nb * k; e += 256) {
+      const int r = (int)(e % J.nb), i = (int)(e / J.nb);
+      J.Bout[r + (int64_t)i * J.ldb] = (r < q) ? C[r + (int64_t)order[i] * L] : 0.0;
+    }
+  }
+}
+
+int svd_smem_capacity() { return 26 * 1024; }
+
+void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_svd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         svd_smem_capacity() * 8);
+    attr = true;
+  }
+  if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
+  k_svd<<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, eps, cap);
+}
+
+// ------------------------------------------------------------------ copy
+__global__ void __launch_bounds__(256) k_copy(const CopyJob* __restrict__ jobs, int njobs) {
+  const int64_t tile = blockIdx.x;
+  const CopyJob& J = jobs[find_job(jobs, njobs, tile)];
+  const int mt = (J.rows + 31) >> 5;
+  const int64_t local = tile - J.tile0;
+  const int ti = (int)(local % mt), tj = (int)(local / mt);
+  for (int e = threadIdx.x; e < 1024; e += 256) {
+    const int i = ti * 32 + (e & 31), j = tj * 32 + (e >> 5);
+    if (i >= J.rows || j >= J.cols) continue;
+    double v;
+    if (J.identity) {
+      if (i != j) continue;
+      v = J.coef;
+    } else {
+      v = J.coef * (J.trans ? J.src[j + (int64_t)i * J.lds] : J.src[i + (int64_t)j * J.lds]);
+    }
+    double* d = J.dst + i + (int64_t)j * J.ldd;
+    *d = J.accumulate ? (*d + v) : v;
+  }
+}
+
+void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st) {
+  if (njobs <= 0 || ntiles <= 0) return;
+  k_copy<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs);
+}
+
+// ------------------------------------------------------------------ eval
+// CTA-wide out[0:M,0:N] += coef * opA(M x K) * opB(K x N), 32x32 tiles,
+// 256 threads, operands staged through shared memory.  bid: opB = I.
+struct Op {
+  const double* p;
+  int ld, tr;
+  __device__ __forceinline__ double at(int i, int j) const {
+    return tr ? p[j + (int64_t)i * ld] : p[i + (int64_t)j * ld];
+  }
+};
+
+__device__ void cta_gemm_acc(double* out, int ldo, int M, int N, int K, double coef, Op A, Op B,
+                             double* sA, double* sB) {
+  const int tid = threadIdx.x;
+  const int ri = tid & 31, cj = tid >> 5;  // rows ri, cols cj + 8*x
+  for (int i0 = 0; i0 < M; i0 += 32) {
+    for (int j0 = 0; j0 < N; j0 += 32) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int p0 = 0; p0 < K; p0 += 32) {
+        for (int e = tid; e < 1024; e += 256) {
+          int a, b;
+          if (!A.tr) { a = e & 31; b = e >> 5; } else { b = e & 31; a = e >> 5; }
+          const int gi = i0 + a, gp = p0 + b;
+          sA[a * 33 + b] = (gi < M && gp < K) ? A.at(gi, gp) : 0.0;
+          int c2, d2;
+          if (!B.tr) { d2 = e & 31; c2 = e >> 5; } else { c2 = e & 31; d2 = e >> 5; }
+          const int gq = p0 + d2, gj = j0 + c2;
+          sB[d2 * 33 + c2] = (gq < K && gj < N) ? B.at(gq, gj) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int pp = 0; pp < 32; pp++) {
+          const double av = sA[ri * 33 + pp];
+#pragma unroll
+          for (int x = 0; x < 4; x++) acc[x] = fma(av, sB[pp * 33 + cj + 8 * x], acc[x]);
+        }
+        __syncthreads();
+      }
+      const int gi = i0 + ri;
+      if (gi < M) {
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+          const int gj = j0 + cj + 8 * x;
+          if (gj < N) out[gi + (int64_t)gj * ldo] += coef * acc[x];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_eval(const EvalJob* __restrict__ jobs) {
+  __shared__ double sA[32 * 33];
+  __shared__ double sB[32 * 33];
+  __shared__ double sT[32 * 33];
+  const EvalJob J = jobs[blockIdx.x];
+  const int tid = threadIdx.x;
+  for (int li = J.leaf_begin; li < J.leaf_end; li++) {
+    const LeafDesc L = J.leaves[li];
+    const int ro = L.row0 - J.t0, co = L.col0 - J.s0;   // offsets inside block (t,s)
+    // non-trans: out rows ro.., V rows co.. ; trans: out rows co.., V rows ro..
+    const int orow = J.trans ? co : ro;
+    const int vrow = J.trans ? ro : co;
+    const int mo = J.trans ? L.n : L.m;   // rows of op(L)
+    const int ko = J.trans ? L.m : L.n;   // cols of op(L)
+    if (J.videntity) {
+      // out[orow + i, vrow + p] += coef * op(L)(i, p)
+      double* o = J.out + orow + (int64_t)vrow * J.ldo;
+      if (L.kind == 2) {
+        for (int64_t e = tid; e < (int64_t)mo * ko; e += 256) {
+          const int i = (int)(e % mo), p = (int)(e / mo);
+          const double v = J.trans ? L.A[p + (int64_t)i * L.m] : L.A[i + (int64_t)p * L.m];
+          o[i + (int64_t)p * J.ldo] += J.coef * v;
+        }
+        __syncthreads();
+      } else if (L.k > 0) {
+        // op(L) = A B^T (or B A^T): out += coef * X Y^T with X,Y the factors
+        const Op X{J.trans ? L.B : L.A, J.trans ? L.n : L.m, 0};
+        const Op Yt{J.trans ? L.A : L.B, J.trans ? L.m : L.n, 1};
+        cta_gemm_acc(o, J.ldo, mo, ko, L.k, J.coef, X, Yt, sA, sB);
+      }
+      continue;
+    }
+    const Op V{J.V + (J.vtrans ? (int64_t)vrow * J.ldv : (int64_t)vrow), J.ldv, J.vtrans};
+    double* o = J.out + orow;
+    if (L.kind == 2) {
+      const Op N{L.A, L.m, J.trans};
+      cta_gemm_acc(o, J.ldo, mo, J.w, ko, J.coef, N, V, sA, sB);
+    } else if (L.k > 0) {
+      // tmp (k x 32 chunk) = F2^T V ; out += coef * F1 tmp, F1 = A (B for trans)
+      const double* F1 = J.trans ? L.B : L.A;
+      const int ld1 = J.trans ? L.n : L.m;
+      const double* F2 = J.trans ? L.A : L.B;
+      const int ld2 = J.trans ? L.m : L.n;
+      for (int j0 = 0; j0 < J.w; j0 += 32) {
+        const int wc = min(32, J.w - j0);
+        const Op Vc{J.vtrans ? V.p + j0 : V.p + (int64_t)j0 * V.ld, V.ld, V.tr};
+        for (int q0 = 0; q0 < L.k; q0 += 32) {
+          const int kc = min(32, L.k - q0);
+          for (int e = tid; e < 32 * 33; e += 256) sT[e] = 0.0;
+          __syncthreads();
+          const Op F2t{F2 + (int64_t)q0 * ld2, ld2, 1};
+          cta_gemm_acc(sT, 33, kc, wc, ko, 1.0, F2t, Vc, sA, sB);
+          const Op F1o{F1 + (int64_t)q0 * ld1, ld1, 0};
+          const Op T{sT, 33, 0};
+          cta_gemm_acc(o + (int64_t)j0 * J.ldo, J.ldo, mo, wc, kc, J.coef, F1o, T, sA, sB);
+        }
+      }
+    }
+  }
+}
+
+void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st) {
+  if (njobs <= 0) return;
+  k_eval<<<njobs, 256, 0, st>>>(d_jobs);
+}
+
+// ------------------------------------------------------------------ entries
+// G_ij = w_j / (4 pi |x_i - x_j|), G_ii = sqrt(w_i/pi)/2 (BASELINE.json),
+// evaluated with explicit round-to-nearest ops (no FMA contraction).
+__device__ __forceinline__ double g_slp(const double* x, const double* w, int64_t i, int64_t j) {
+  if (i == j) return __dmul_rn(__dsqrt_rn(__ddiv_rn(w[i], M_PI)), 0.5);
+  const double dx = __dsub_rn(x[3 * i], x[3 * j]);
+  const double dy = __dsub_rn(x[3 * i + 1], x[3 * j + 1]);
+  const double dz = __dsub_rn(x[3 * i + 2], x[3 * j + 2]);
+  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  return __ddiv_rn(w[j], __dmul_rn(4.0 * M_PI, __dsqrt_rn(r2)));
+}
+
+__global__ void __launch_bounds__(256) k_gen(const GenJob* __restrict__ jobs, int njobs,
+                                             const double* __restrict__ x,
+                                             const double* __restrict__ w,
+                                             const int64_t* __restrict__ perm, int kernel) {
+  const int64_t tile = blockIdx.x;
+  const GenJob& J = jobs[find_job(jobs, njobs, tile)];
+  const int mt = (J.m + 31) >> 5;
+  const int64_t local = tile - J.tile0;
+  const int ti = (int)(local % mt), tj = (int)(local / mt);
+  for (int e = threadIdx.x; e < 1024; e += 256) {
+    const int i = ti * 32 + (e & 31), j = tj * 32 + (e >> 5);
+    if (i >= J.m || j >= J.n) continue;
+    const int64_t oi = perm[J.r0 + i], oj = perm[J.c0 + j];
+    double v = g_slp(x, w, oi, oj);
+    if (kernel == 1) v = __dmul_rn(0.5, __dadd_rn(v, g_slp(x, w, oj, oi)));
+    J.dst[i + (int64_t)j * J.ld] = v;
+  }
+}
+
+void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x, const double* w,
+                const int64_t* perm, int kernel, cudaStream_t st) {
+  if (njobs <= 0 || ntiles <= 0) return;
+  k_gen<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, x, w, perm, kernel);
+}
+
+// ------------------------------------------------------------------ norms
+__global__ void __launch_bounds__(256) k_norm(const NormJob* __restrict__ jobs, double* out) {
+  __shared__ double red[32];
+  const NormJob J = jobs[blockIdx.x];
+  const int n = J.ndyn ? *J.ndyn : J.n;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)J.m * n; e += 256) {
+    const double v = J.A[(e % J.m) + (e / J.m) * J.lda];
+    s = fma(v, v, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+void launch_norm(const NormJob* d_jobs, int njobs, double* out, cudaStream_t st) {
+  if (njobs <= 0) return;
+  k_norm<<<njobs, 256, 0, st>>>(d_jobs, out);
+}
+
+// ------------------------------------------------------------------ randn
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_randn(double* dst, int64_t count, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = splitmix(seed ^ (2 * (uint64_t)i));
+    const uint64_t b = splitmix(seed ^ (2 * (uint64_t)i + 1));
+    const double u1 = ((a >> 11) + 1) * (1.0 / 9007199254740993.0);
+    const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
+    dst[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
+void launch_randn(double* dst, int64_t count, uint64_t seed, cudaStream_t st) {
+  if (count <= 0) return;
+  k_randn<<<1184, 256, 0, st>>>(dst, count, seed);
+}
+
+// ------------------------------------------------------------------ matvec
+// y += alpha op(G) x over all leaves (one CTA per leaf, FP64 atomics).
+__global__ void __launch_bounds__(256) k_matvec(const LeafDesc* __restrict__ leaves, int trans,
+                                                double alpha, const double* __restrict__ x,
+                                                int64_t ldx, double* y, int64_t ldy, int ncols) {
+  __shared__ double tmp[4096];  // k x ncols (host guarantees k*ncols <= 4096)
+  const LeafDesc L = leaves[blockIdx.x];
+  const int orow = trans ? L.col0 : L.row0, vrow = trans ? L.row0 : L.col0;
+  const int mo = trans ? L.n : L.m, ko = trans ? L.m : L.n;
+  if (L.kind == 2) {
+    for (int64_t e = threadIdx.x; e < (int64_t)mo * ncols; e += 256) {
+      const int i = (int)(e % mo), j = (int)(e / mo);
+      double s = 0.0;
+      for (int p = 0; p < ko; p++) {
+        const double a = trans ? L.A[p + (int64_t)i * L.m] : L.A[i + (int64_t)p * L.m];
+        s = fma(a, x[vrow + p + (int64_t)j * ldx], s);
+      }
+      atomicAdd(&y[orow + i + (int64_t)j * ldy], alpha * s);
+    }
+  } else if (L.k > 0) {
+    const double* F1 = trans ? L.B : L.A;
+    const int ld1 = trans ? L.n : L.m;
+    const double* F2 = trans ? L.A : L.B;
+    const int ld2 = trans ? L.m : L.n;
+    for (int e = threadIdx.x; e < L.k * ncols; e += 256) {
+      const int q = e % L.k, j = e / L.k;
+      double s = 0.0;
+      for (int p = 0; p < ko; p++) s = fma(F2[p + (int64_t)q * ld2], x[vrow + p + (int64_t)j * ldx], s);
+      tmp[e] = s;
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < (int64_t)mo * ncols; e += 256) {
+      const int i = (int)(e % mo), j = (int)(e / mo);
+      double s = 0.0;
+      for (int q = 0; q < L.k; q++) s = fma(F1[i + (int64_t)q * ld1], tmp[q + j * L.k], s);
+      atomicAdd(&y[orow + i + (int64_t)j * ldy], alpha * s);
+    }
+  }
+}
+
+void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double alpha,
+                          const double* x, int64_t ldx, double* y, int64_t ldy, int ncols,
+                          cudaStream_t st) {
+  if (nleaves <= 0) return;
+  k_matvec<<<nleaves, 256, 0, st>>>(leaves, trans, alpha, x, ldx, y, ldy, ncols);
+}
+
+__global__ void k_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double* p = y + (e % rows) + (e / rows) * ldy;
+    *p = (beta == 0.0) ? 0.0 : beta * *p;
+  }
+}
+
+void launch_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  k_scale<<<592, 256, 0, st>>>(y, ldy, rows, cols, beta);
+}
+
+}  // namespace hm

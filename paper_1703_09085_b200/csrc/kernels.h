@@ -1,0 +1,132 @@
+// Batched FP64 kernels for sm_100a (libhm internal).  Every launcher takes a
+// device array of job descriptors and enqueues ONE kernel on `st`.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hm {
+
+// C = alpha * op(A) * op(B) + beta * C   (column-major, per-job shapes)
+// mask bit 1: the STORED operand is upper triangular (entries below the
+// diagonal of the stored matrix read as 0) -- used for R factors that share
+// storage with Householder vectors.
+struct GemmJob {
+  const double* A;
+  const double* B;
+  double* C;
+  int m, n, k;
+  int lda, ldb, ldc;
+  int transA, transB;
+  int maskA, maskB;
+  double alpha, beta;
+  int64_t tile0;       // first 64x64 tile id of this job (prefix sum)
+  const int* kdyn;     // optional: if non-null, k = *kdyn (device-known width)
+  const int* ndyn;     // optional: if non-null, n = *ndyn
+};
+
+// In-place Householder QR of a tall panel A (m x n, m > n, lda):
+// R in the upper triangle, reflector v_j below the diagonal (v_j[0] = 1
+// implicit), tau[j].  LAPACK dgeqr2 convention.
+struct QrJob {
+  double* A;
+  int m, n, lda;
+  double* tau;
+  double* work;        // unused by the smem path
+};
+
+// X <- Q X with Q = H_0 H_1 ... H_{r-1} from a QrJob (X: m x c, ldx); c is
+// read from *cdyn (device) when cdyn != nullptr.
+struct ApplyQJob {
+  const double* V;     // reflectors (m x r, ldv)
+  const double* tau;
+  int m, r, ldv;
+  double* X;
+  int ldx, c;
+  const int* cdyn;
+};
+
+// One-sided Jacobi SVD of M (p x q, ldm) + eps rank rule + factor output:
+//   Aout[0:p, 0:k] = U_k (orthonormal), rows p..ma-1 zeroed  (ld lda)
+//   Bout[0:q, 0:k] = V_k Sigma_k,         rows q..nb-1 zeroed (ld ldb)
+//   *rank = k, sigma[0:min(p,q)] (descending) if sigma != nullptr
+struct SvdJob {
+  const double* M;
+  int p, q, ldm;
+  double* Aout;
+  int lda, ma;
+  double* Bout;
+  int ldb, nb;
+  int* rank;
+  double* sigma;
+  double* work;        // global work (L x c doubles) when it does not fit smem
+};
+
+// dst[0:rows, 0:cols] (+)= coef * op(src); identity: dst[d,d] = coef.
+struct CopyJob {
+  double* dst;
+  const double* src;
+  int ldd, lds, rows, cols;
+  int trans, identity, accumulate;
+  double coef;
+  int64_t tile0;
+};
+
+// A leaf of an H-matrix in DFS order (for addeval / addevaltrans).
+struct LeafDesc {
+  int kind;            // 1 admissible, 2 dense
+  int row0, col0;      // absolute starts (tree order)
+  int m, n, k;
+  const double* A;     // adm: m x k ; dense: N (m x n)
+  const double* B;     // adm: n x k
+};
+
+// out += coef * H|_{t x s} V   (trans=0; out rows = #t, V rows = #s) or
+// out += coef * H|_{t x s}^T V (trans=1; out rows = #s, V rows = #t),
+// summed over the leaves [leaf_begin, leaf_end) of block (t,s)  (Fig. 1).
+// V(p, j) = vtrans ? V[j + p*ldv] : V[p + j*ldv]; videntity: V = I.
+struct EvalJob {
+  const LeafDesc* leaves;
+  int leaf_begin, leaf_end;
+  int trans;
+  int t0, s0;
+  double coef;
+  double* out;
+  int ldo, w;
+  const double* V;
+  int ldv, vtrans, videntity;
+  int64_t cost;        // for scheduling (largest first)
+};
+
+// Kernel-matrix generation: dst[i,j] = G(perm[r0+i], perm[c0+j]).
+struct GenJob {
+  double* dst;
+  int ld, m, n, r0, c0;
+  int64_t tile0;
+};
+
+// Frobenius norm squared of a column-major panel -> out[job].
+struct NormJob {
+  const double* A;
+  int m, n, lda;
+  const int* ndyn;
+};
+
+void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
+void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st);
+void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
+void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
+void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st);
+void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x,
+                const double* w, const int64_t* perm, int kernel, cudaStream_t st);
+void launch_norm(const NormJob* d_jobs, int njobs, double* out, cudaStream_t st);
+void launch_randn(double* dst, int64_t count, uint64_t seed, cudaStream_t st);
+void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double alpha,
+                          const double* x, int64_t ldx, double* y, int64_t ldy, int ncols,
+                          cudaStream_t st);
+void launch_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta, cudaStream_t st);
+
+int svd_smem_capacity();   // doubles available for the smem Jacobi path
+int qr_smem_capacity();
+
+}  // namespace hm

@@ -1,0 +1,73 @@
+"""Comparison helpers for GPU <-> oracle parity (test infrastructure)."""
+from __future__ import annotations
+
+import numpy as np
+
+ADM, DENSE = 1, 2
+
+
+def leaf_payloads(d):
+    """dict block id -> ('adm', A, B) | ('dense', N) from an hm_host_desc dict."""
+    out = {}
+    cs, cz = d["cl_start"], d["cl_size"]
+    for b in range(len(d["bl_row"])):
+        kind = int(d["bl_kind"][b])
+        if kind == 0:
+            continue
+        m = int(cz[d["bl_row"][b]])
+        n = int(cz[d["bl_col"][b]])
+        o = int(d["bl_off"][b])
+        if kind == ADM:
+            k = int(d["bl_rank"][b])
+            A = d["factors"][o:o + m * k].reshape((m, k), order="F")
+            B = d["factors"][o + m * k:o + (m + n) * k].reshape((n, k), order="F")
+            out[b] = ("adm", A, B)
+        else:
+            out[b] = ("dense", d["dense"][o:o + m * n].reshape((m, n), order="F"))
+    return out
+
+
+def lowrank_diff(Ag, Bg, Ao, Bo):
+    """||Ag Bg^T - Ao Bo^T||_F via QR of the stacks (never the Gram expansion)."""
+    A = np.hstack([Ag, -Ao])
+    B = np.hstack([Bg, Bo])
+    if A.shape[1] == 0:
+        return 0.0
+    _, Ra = np.linalg.qr(A)
+    _, Rb = np.linalg.qr(B)
+    return float(np.linalg.norm(Ra @ Rb.T))
+
+
+def lowrank_norm(A, B):
+    if A.shape[1] == 0:
+        return 0.0
+    _, Ra = np.linalg.qr(A)
+    _, Rb = np.linalg.qr(B)
+    return float(np.linalg.norm(Ra @ Rb.T))
+
+
+def compare(dg, do, near_blocks=(), tol=1e-9):
+    """Per-block parity (north star): identical ranks (except flagged blocks) and
+    relative Frobenius difference <= tol.  Returns a report dict."""
+    pg, po = leaf_payloads(dg), leaf_payloads(do)
+    assert pg.keys() == po.keys()
+    total = 0.0
+    for b, v in po.items():
+        total += np.linalg.norm(v[1]) ** 2 if v[0] == "dense" else lowrank_norm(v[1], v[2]) ** 2
+    znorm = np.sqrt(total)
+    rank_mis, worst, worst_b = [], 0.0, None
+    for b, vo in po.items():
+        vg = pg[b]
+        if vo[0] == "dense":
+            den = max(np.linalg.norm(vo[1]), 1e-12 * znorm)
+            rel = np.linalg.norm(vg[1] - vo[1]) / den
+        else:
+            if vg[1].shape[1] != vo[1].shape[1]:
+                rank_mis.append(b)
+            den = max(lowrank_norm(vo[1], vo[2]), 1e-12 * znorm)
+            rel = lowrank_diff(vg[1], vg[2], vo[1], vo[2]) / den
+        if b in near_blocks:
+            continue
+        if rel > worst:
+            worst, worst_b = rel, b
+    return dict(rank_mismatch=rank_mis, worst=worst, worst_block=worst_b, znorm=znorm)

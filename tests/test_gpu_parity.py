@@ -1,0 +1,187 @@
+"""GPU <-> oracle parity through the C-ABI (pytest -m gpu).
+
+The oracle (oracle/, CPU, FP64) builds the H-matrix; the same host
+description is imported into libhm; both sides run Z <- Z + alpha X Y with
+the S2 schedule; per admissible block the ranks must be identical and the
+relative Frobenius difference <= 1e-9 (north star; BASELINE.json), dense
+blocks entrywise in relative Frobenius.
+"""
+import numpy as np
+import pytest
+
+from hm_inputs import random_points, sphere_points
+from oracle.hmatrix import Problem, build, export, matvec as o_matvec
+from oracle.lowrank import TruncCtx, trunc
+from oracle.product import addmul_s2
+from tests.hm_compare import compare, leaf_payloads, lowrank_diff, lowrank_norm
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def hm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1703_09085_b200 as hm
+    return hm
+
+
+@pytest.fixture(scope="module")
+def ctx(hm):
+    return hm.Context(0)
+
+
+def _prescribed(rng, m, n, s, junk):
+    q = len(s)
+    U, _ = np.linalg.qr(rng.standard_normal((m, q)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, q)))
+    As, Bs = [U * s], [V]
+    for _ in range(junk):
+        X = rng.standard_normal((m, 2))
+        Y = rng.standard_normal((n, 2))
+        As += [X, -X]
+        Bs += [Y, Y]
+    return np.hstack(As), np.hstack(Bs)
+
+
+@pytest.mark.parametrize("eps", [1e-4, 1e-6])
+def test_trunc_kernel_prescribed_sigma(hm, ctx, eps):
+    """Batched TRUNC vs the closed-form Eckart-Young rank/error
+    and vs the oracle's TRUNC on the same stacks; sizes span every path
+    (QR both sides, one side, dense; smem buckets and the global path)."""
+    rng = np.random.default_rng(12)
+    shapes = [(40, 30, 12, 0), (200, 150, 20, 2), (64, 64, 64, 1), (300, 40, 25, 3), (17, 500, 16, 2),
+              (130, 170, 90, 4), (5, 3, 3, 0), (1, 1, 1, 0), (700, 650, 60, 3), (260, 240, 240, 2)]
+    stacks, svals = [], []
+    for m, n, q, junk in shapes:
+        s = 10.0 ** (-0.31 * np.arange(q))    # no singular value sits on the eps threshold
+        A, B = _prescribed(rng, m, n, s, junk)
+        stacks.append((A, B))
+        svals.append(s)
+    out, ranks, sig = hm.test_trunc_batched(ctx, stacks, eps)
+    for (A, B), (U, V), k, s in zip(stacks, out, ranks, svals):
+        tot = np.sum(s ** 2)
+        kk = next(j for j in range(len(s) + 1) if np.sum(s[j:] ** 2) <= eps ** 2 * tot)
+        assert k == kk
+        err = np.linalg.norm(A @ B.T - U @ V.T)
+        np.testing.assert_allclose(err, np.sqrt(np.sum(s[k:] ** 2)), rtol=1e-7, atol=1e-13 * np.linalg.norm(A) * np.linalg.norm(B))
+        np.testing.assert_allclose(U.T @ U, np.eye(k), atol=1e-12)
+        Uo, Vo = trunc(A, B, TruncCtx(eps))
+        assert Uo.shape[1] == k
+        assert lowrank_diff(U, V, Uo, Vo) <= TOL * lowrank_norm(Uo, Vo) + 1e-14
+
+
+def test_trunc_kernel_degenerate(hm, ctx):
+    rng = np.random.default_rng(3)
+    R = (rng.standard_normal((30, 4)), rng.standard_normal((25, 4)))
+    stacks = [(np.hstack([R[0], -R[0]]), np.hstack([R[1], R[1]])),        # exact cancellation
+              (np.zeros((12, 3)), np.zeros((9, 3))),                         # zero
+              (rng.standard_normal((8, 0)), rng.standard_normal((6, 0)))]    # empty stack
+    out, ranks, _ = hm.test_trunc_batched(ctx, stacks, 1e-8)
+    assert ranks[1] == 0 and ranks[2] == 0
+    U, V = out[0]
+    assert ranks[0] == 0 or np.linalg.norm(U @ V.T) <= 1e-12 * np.linalg.norm(R[0] @ R[1].T)
+
+
+def _cfg(L, leaf, eps):
+    x, w = sphere_points(L)
+    P = Problem(x, w, leaf, 2.0)
+    G = build(P, eps)
+    return P, G
+
+
+@pytest.mark.parametrize("L,leaf,eps,alpha", [
+    (1, 4, 0.0, 1.0),       # n=80: Fig. 5 / Fig. 7 branches, exact arithmetic
+    (2, 8, 0.0, -0.5),      # n=320: + nested virtual recursion, eps = 0
+    (2, 8, 1e-4, 1.0),      # n=320, eps = 1e-4
+    (3, 32, 1e-4, 1.0),     # config 1 (BASELINE.json configs[0])
+])
+def test_addmul_parity(hm, ctx, L, leaf, eps, alpha):
+    P, G = _cfg(L, leaf, eps)
+    octx = TruncCtx(eps)
+    Zo, octx, st = addmul_s2(alpha, G.clone(), G.clone(), G.clone(), eps, ctx=octx)
+    do = export(Zo)
+    Gg = ctx.import_desc(export(G))
+    X, Y, Z = Gg.clone(), Gg.clone(), Gg.clone()
+    hm.addmul(alpha, X, Y, Z, eps)
+    dg = Z.export()
+    s = ctx.last_stats()
+    assert s["addproduct_calls"] == st.addproduct
+    assert s["truncations"] == octx.count
+    rep = compare(dg, do)
+    assert not rep["rank_mismatch"] or octx.near, rep
+    assert rep["worst"] <= TOL, rep
+    if eps == 0.0:
+        Gd = G.to_dense()
+        ref = Gd + alpha * Gd @ Gd
+        from oracle.hmatrix import import_payload
+        Zg = import_payload(P.bt, dg).to_dense()
+        assert np.linalg.norm(Zg - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_addmul_distinct_operands(hm, ctx):
+    """X != Y != Z (ragged random geometry, odd n)."""
+    x, w = random_points(333, 4)
+    P = Problem(x, w, 7, 2.0)
+    X = build(P, 1e-6)
+    Y = X.clone()
+    for k in Y.A:
+        Y.B[k] = 0.5 * Y.B[k]
+    for k in Y.N:
+        Y.N[k] = Y.N[k].T.copy() if Y.N[k].shape[0] == Y.N[k].shape[1] else Y.N[k] * 2.0
+    Z = X.clone()
+    Zo, octx, _ = addmul_s2(0.7, X.clone(), Y.clone(), Z.clone(), 1e-6)
+    Xg, Yg, Zg = ctx.import_desc(export(X)), ctx.import_desc(export(Y)), ctx.import_desc(export(Z))
+    hm.addmul(0.7, Xg, Yg, Zg, 1e-6)
+    rep = compare(Zg.export(), export(Zo))
+    assert not rep["rank_mismatch"] or octx.near, rep
+    assert rep["worst"] <= TOL, rep
+
+
+def test_addmul_rejects_alias(hm, ctx):
+    P, G = _cfg(1, 4, 1e-4)
+    Gg = ctx.import_desc(export(G))
+    with pytest.raises(hm.HMError) as ei:
+        hm.addmul(1.0, Gg, Gg, Gg, 1e-4)
+    assert "ESTRUCT" in str(ei.value)
+
+
+@pytest.mark.parametrize("L,leaf,kernel", [(3, 32, 0), (2, 8, 1)])
+def test_build_parity(hm, ctx, L, leaf, kernel):
+    """hm_build on the device vs the oracle build: identical trees (bit-exact
+    integer arrays and bounding boxes), identical ranks, per-block <= 1e-9."""
+    x, w = sphere_points(L)
+    eps = 1e-4
+    P = Problem(x, w, leaf, 2.0, kernel=kernel)
+    Go = build(P, eps)
+    do = export(Go)
+    Gg = ctx.build(x, w, leaf, 2.0, eps, kernel=kernel)
+    dg = Gg.export()
+    for k in ("cl_start", "cl_size", "cl_son0", "cl_nsons", "cl_level", "bl_row", "bl_col", "bl_kind",
+              "bl_son0", "bl_nsons"):
+        np.testing.assert_array_equal(dg[k], do[k], err_msg=k)
+    np.testing.assert_array_equal(dg["perm"], do["perm"])
+    np.testing.assert_array_equal(dg["cl_bbox"], do["cl_bbox"])
+    rep = compare(dg, do)
+    assert not rep["rank_mismatch"], rep
+    assert rep["worst"] <= TOL, rep
+
+
+def test_matvec(hm, ctx):
+    import torch
+    P, G = _cfg(2, 8, 1e-4)
+    Gg = ctx.import_desc(export(G))
+    n = P.ct.n
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((n, 8))
+    Y0 = rng.standard_normal((n, 8))
+    for op in (0, 1):
+        ref = Y0 * 0.5
+        o_matvec(G, 2.0, X, ref, trans=bool(op))
+        xg = torch.from_numpy(X.T.copy()).cuda().T
+        yg = torch.from_numpy(Y0.T.copy()).cuda().T
+        hm.matvec(Gg, xg, yg, alpha=2.0, beta=0.5, op=op)
+        np.testing.assert_allclose(yg.cpu().numpy(), ref, atol=1e-13 * np.abs(ref).max())
