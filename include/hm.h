@@ -106,6 +106,7 @@ typedef struct {
   int64_t merges;
   int64_t dense_adds;
   int64_t levels;
+  int64_t kernel_launches;    /* process-wide count of libhm kernel launches so far */
   double flops_trunc;         /* SURVEY §8(d) convention flops */
   double flops_eval;
   double flops_dense;

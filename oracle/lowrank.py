@@ -38,6 +38,12 @@ class TruncCtx:
         self.tag = None         # optional caller-provided label of the current truncation
         self.forced = {}        # count index -> forced rank (forced-rank replay)
         self.ranks = []         # per call: (tag, k)
+        self.counter = None     # optional oracle.flops.ConventionCounter (timing reports only)
+
+    def record(self, m, n, l, k):
+        self.ranks.append((self.tag, k))
+        if self.counter is not None:
+            self.counter.on_trunc(m, n, l, k)
 
 
 def choose_rank(s, eps):
@@ -84,7 +90,7 @@ def trunc(A, B, ctx: TruncCtx):
     ctx.count += 1
     ctx.cols += l
     if l == 0 or m == 0 or n == 0:
-        ctx.ranks.append((ctx.tag, 0))
+        ctx.record(m, n, l, 0)
         return np.zeros((m, 0)), np.zeros((n, 0))
     if l < min(m, n):
         QB, RB = np.linalg.qr(B)              # thin QR  B = Q_B R_B
@@ -94,7 +100,7 @@ def trunc(A, B, ctx: TruncCtx):
         k = ctx.forced.get(idx, k)
         if ctx.log_near and _near(ctx, s, k, tail):
             ctx.near.append((idx, ctx.tag, k, s.copy()))
-        ctx.ranks.append((ctx.tag, k))
+        ctx.record(m, n, l, k)
         return U[:, :k].copy(), QB @ (Vh[:k].T * s[:k])   # V = Q_B V_hat
     S = A @ B.T
     U, s, Vh = _svd(S)
@@ -102,7 +108,7 @@ def trunc(A, B, ctx: TruncCtx):
     k = ctx.forced.get(idx, k)
     if ctx.log_near and _near(ctx, s, k, tail):
         ctx.near.append((idx, ctx.tag, k, s.copy()))
-    ctx.ranks.append((ctx.tag, k))
+    ctx.record(m, n, l, k)
     return U[:, :k].copy(), Vh[:k].T * s[:k]
 
 
@@ -130,16 +136,17 @@ def rowmerge(parts, ctx):
     Ahat = np.hstack(Ahats)
     idx = ctx.count
     ctx.count += 1
-    ctx.cols += sum(p[0].shape[1] for p in parts)
+    lsum = sum(p[0].shape[1] for p in parts)
+    ctx.cols += lsum
     if Ahat.shape[1] == 0 or m == 0:
-        ctx.ranks.append((ctx.tag, 0))
+        ctx.record(m, sum(ns), lsum, 0)
         return np.zeros((m, 0)), np.zeros((sum(ns), 0))
     U, s, Vh = _svd(Ahat)
     k, tail = choose_rank(s, ctx.eps)
     k = ctx.forced.get(idx, k)
     if ctx.log_near and _near(ctx, s, k, tail):
         ctx.near.append((idx, ctx.tag, k, s.copy()))
-    ctx.ranks.append((ctx.tag, k))
+    ctx.record(m, sum(ns), lsum, k)
     W = Vh[:k].T * s[:k]
     Bout = np.zeros((sum(ns), k))
     r0 = c0 = 0

@@ -49,7 +49,7 @@ class Stats:
 
 # --------------------------------------------------------------- Fig. 5
 
-def evaluate(alpha, bx, by, X: HMatrix, Y: HMatrix, st: Stats | None = None):
+def evaluate(alpha, bx, by, X: HMatrix, Y: HMatrix, st: Stats | None = None, counter=None):
     """Low-rank factorization A_hat B_hat^* = alpha X|_{ts} Y|_{sr} of a product
     whose (t,s) or (s,r) block is a leaf, in Fig. 5's printed branch order
     (P:L969-1006).  Returns (A_hat, B_hat) or None if the product is pending.
@@ -97,6 +97,9 @@ def evaluate(alpha, bx, by, X: HMatrix, Y: HMatrix, st: Stats | None = None):
     if st is not None:
         st.evaluated += 1
         st.branch[br] += 1
+    if counter is not None:   # convention flops of the addeval/addevaltrans just done
+        H, blk = (Y, by) if br in (0, 1, 4) else (X, bx)
+        counter.on_eval(H, blk, Ah.shape[1], br in (1, 3))
     return Ah, Bh
 
 
@@ -195,14 +198,17 @@ class Acc2:
 class S2:
     """Level-batched accumulated product (the GPU parity schedule)."""
 
-    def __init__(self, X, Y, ctx: TruncCtx, stats: Stats | None = None):
+    def __init__(self, X, Y, ctx: TruncCtx, stats: Stats | None = None, counter=None):
         self.X, self.Y, self.ctx = X, Y, ctx
         self.st = stats or Stats()
+        self.counter = counter
+        if counter is not None:
+            ctx.counter = counter
 
     def addproduct(self, acc: Acc2, alpha, bx, by):
         """Fig. 5, S2: evaluated terms are appended exactly."""
         self.st.addproduct += 1
-        ev = evaluate(alpha, bx, by, self.X, self.Y, self.st)
+        ev = evaluate(alpha, bx, by, self.X, self.Y, self.st, self.counter)
         if ev is None:
             acc.pending.append((alpha, bx, by))
         else:
@@ -254,6 +260,8 @@ class S2:
                 self.st.fb("ii_dense")
                 A, B = acc.stack()
                 z.h.N[z.b.id] += A @ B.T
+                if self.counter is not None:
+                    self.counter.on_dense(A.shape[0], B.shape[0], A.shape[1])
                 self._leaf_update(z.b.id)
             else:                                               # (iii)
                 self.st.fb("iii_sub")
@@ -307,11 +315,11 @@ class S2:
                                   B[c.s.start - s0:c.s.start - s0 + c.s.size])
 
 
-def addmul_s2(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps, ctx=None, stats=None):
+def addmul_s2(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps, ctx=None, stats=None, counter=None):
     """Z <- blocktrunc(Z + alpha X Y) with accumulated updates: addproduct for
     the root of the product tree, then flush (Theorem)."""
     ctx = ctx or TruncCtx(eps)
-    alg = S2(X, Y, ctx, stats)
+    alg = S2(X, Y, ctx, stats, counter)
     bt = Z.bt
     root = bt.root
     acc = Acc2(root.t, root.s)

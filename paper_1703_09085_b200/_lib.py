@@ -41,7 +41,7 @@ class Stats(C.Structure):
         ("factor_doubles", C.c_int64), ("dense_doubles", C.c_int64),
         ("addproduct_calls", C.c_int64), ("evaluated_terms", C.c_int64),
         ("truncations", C.c_int64), ("trunc_cols", C.c_int64), ("merges", C.c_int64),
-        ("dense_adds", C.c_int64), ("levels", C.c_int64),
+        ("dense_adds", C.c_int64), ("levels", C.c_int64), ("kernel_launches", C.c_int64),
         ("flops_trunc", C.c_double), ("flops_eval", C.c_double), ("flops_dense", C.c_double),
         ("bytes_trunc", C.c_double), ("bytes_eval", C.c_double), ("bytes_dense", C.c_double),
     ]

@@ -272,6 +272,7 @@ struct Planner {
     std::vector<CopyJob> cj;
     std::vector<EvalJob> ej;
     int64_t ctiles = 0;
+    const double fl_eval0 = fl_eval, by_eval0 = by_eval;
     for (auto& s : stacks) {
       Node& nd = nodes[s.node];
       int col = 0;
@@ -299,8 +300,7 @@ struct Planner {
     if (!ej.empty()) {
       std::stable_sort(ej.begin(), ej.end(),
                        [](const EvalJob& a, const EvalJob& b) { return a.cost > b.cost; });
-      double fl = 0, by = 0;
-      ProfScope ps(c, PC_EVAL, fl, by);
+      ProfScope ps(c, PC_EVAL, fl_eval - fl_eval0, by_eval - by_eval0);
       launch_eval(scratch.upload(ej), (int)ej.size(), c->stream);
       HM_CHECK_LAUNCH();
     }
@@ -310,6 +310,7 @@ struct Planner {
     std::vector<GemmJob> gj;
     int64_t gtiles = 0;
     int* d_ranks = static_cast<int*>(scratch.alloc_bytes(sizeof(int) * (stacks.size() + 1)));
+    const double fl_dense0 = fl_dense, by_dense0 = by_dense;
     for (auto& s : stacks) {
       Node& nd = nodes[s.node];
       if (s.kind == 3) {
@@ -337,7 +338,7 @@ struct Planner {
       else nd.result = out;
     }
     if (!gj.empty()) {
-      ProfScope ps(c, PC_DENSE, 0, 0);
+      ProfScope ps(c, PC_DENSE, fl_dense - fl_dense0, by_dense - by_dense0);
       launch_gemm(scratch.upload(gj), (int)gj.size(), gtiles, c->stream);
       HM_CHECK_LAUNCH();
     }

@@ -342,6 +342,7 @@ hm_status hm_stats(hm_ctx ctx, hm_mat m, hm_stats_t* out) {
   if (!ctx || !out) return HM_EINVAL;
   return guard(ctx, [&] {
     *out = ctx->c.last;
+    out->kernel_launches = launch_count();
     if (!m) return;
     const Mat& M = m->m;
     const Tree& T = *M.tree;

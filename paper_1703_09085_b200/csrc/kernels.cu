@@ -9,11 +9,17 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "kernels.h"
 
 namespace hm {
 
 static constexpr double kU = 1.1102230246251565e-16;  // unit roundoff 2^-53
+
+static std::atomic<long long> g_launches{0};
+static inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -123,6 +129,7 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmJob* __restrict__ jobs, 
 
 void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
+  count_launch();
   k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs);
 }
 
@@ -202,6 +209,7 @@ void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
                          qr_smem_capacity() * 8);
     attr = true;
   }
+  count_launch();
   k_qr<<<njobs, 256, bytes, st>>>(d_jobs, cap);
 }
 
@@ -229,6 +237,7 @@ __global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jo
 
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st) {
   if (njobs <= 0) return;
+  count_launch();
   k_applyq<<<njobs, 256, 0, st>>>(d_jobs);
 }
 
@@ -388,6 +397,7 @@ void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream
     attr = true;
   }
   if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
+  count_launch();
   k_svd<<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, eps, cap);
 }
 
@@ -415,6 +425,7 @@ __global__ void __launch_bounds__(256) k_copy(const CopyJob* __restrict__ jobs, 
 
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
+  count_launch();
   k_copy<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs);
 }
 
@@ -532,6 +543,7 @@ __global__ void __launch_bounds__(256) k_eval(const EvalJob* __restrict__ jobs) 
 
 void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st) {
   if (njobs <= 0) return;
+  count_launch();
   k_eval<<<njobs, 256, 0, st>>>(d_jobs);
 }
 
@@ -569,6 +581,7 @@ __global__ void __launch_bounds__(256) k_gen(const GenJob* __restrict__ jobs, in
 void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x, const double* w,
                 const int64_t* perm, int kernel, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
+  count_launch();
   k_gen<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, x, w, perm, kernel);
 }
 
@@ -588,6 +601,7 @@ __global__ void __launch_bounds__(256) k_norm(const NormJob* __restrict__ jobs, 
 
 void launch_norm(const NormJob* d_jobs, int njobs, double* out, cudaStream_t st) {
   if (njobs <= 0) return;
+  count_launch();
   k_norm<<<njobs, 256, 0, st>>>(d_jobs, out);
 }
 
@@ -612,6 +626,7 @@ __global__ void k_randn(double* dst, int64_t count, uint64_t seed) {
 
 void launch_randn(double* dst, int64_t count, uint64_t seed, cudaStream_t st) {
   if (count <= 0) return;
+  count_launch();
   k_randn<<<1184, 256, 0, st>>>(dst, count, seed);
 }
 
@@ -659,6 +674,7 @@ void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double
                           const double* x, int64_t ldx, double* y, int64_t ldy, int ncols,
                           cudaStream_t st) {
   if (nleaves <= 0) return;
+  count_launch();
   k_matvec<<<nleaves, 256, 0, st>>>(leaves, trans, alpha, x, ldx, y, ldy, ncols);
 }
 
@@ -672,6 +688,7 @@ __global__ void k_scale(double* y, int64_t ldy, int64_t rows, int cols, double b
 
 void launch_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return;
+  count_launch();
   k_scale<<<592, 256, 0, st>>>(y, ldy, rows, cols, beta);
 }
 

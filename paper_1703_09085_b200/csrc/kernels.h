@@ -126,6 +126,7 @@ void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double
                           cudaStream_t st);
 void launch_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta, cudaStream_t st);
 
+int64_t launch_count();     // process-wide number of kernel launches
 int svd_smem_capacity();   // doubles available for the smem Jacobi path
 int qr_smem_capacity();
 
