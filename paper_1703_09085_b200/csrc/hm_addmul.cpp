@@ -15,6 +15,9 @@
 // exact stack once (DESIGN.md §3 R2), so the truncated matrices are the
 // oracle's (oracle/product.py S2).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -57,6 +60,8 @@ struct Planner {
   std::vector<std::vector<Node>> levels;
   std::vector<int> zresult;   // real adm leaf id -> FP id
   std::vector<LeafDesc> lx, ly;
+  std::vector<double> lx_mat, lx_mn, ly_mat, ly_mn;   // DFS prefix sums (convention counts)
+  double t_wait = 0;
   LeafDesc *dlx = nullptr, *dly = nullptr;
   // stats
   int64_t n_addproduct = 0, n_eval = 0, n_trunc = 0, n_cols = 0, n_merge = 0, n_dense = 0;
@@ -159,19 +164,14 @@ struct Planner {
     e.ldv = ldv;
     e.vtrans = vtrans;
     e.videntity = videntity;
-    const std::vector<LeafDesc>& lt = yside ? ly : lx;
-    double fl = 0, by = 0;
-    for (int i = e.leaf_begin; i < e.leaf_end; i++) {
-      const LeafDesc& L = lt[i];
-      if (L.kind == HM_BLOCK_DENSE) {
-        fl += 2.0 * L.m * L.n * w;
-        by += 8.0 * ((double)L.m * L.n + (double)(L.m + L.n) * w);
-      } else {
-        fl += 2.0 * L.k * (double)(L.m + L.n) * w;
-        by += 8.0 * ((double)L.k * (L.m + L.n) + (double)(L.m + L.n) * w);
-      }
-    }
-    if (videntity) fl = 0;   // expansion: a copy, not arithmetic
+    // convention work from DFS prefix sums over the leaf table (O(1) per term):
+    // dense leaf 2 m'n' w flops, low-rank leaf 2 k'(m'+n') w; bytes = payload + panels
+    const std::vector<double>& pm = yside ? ly_mat : lx_mat;
+    const std::vector<double>& pn = yside ? ly_mn : lx_mn;
+    const double smat = pm[e.leaf_end] - pm[e.leaf_begin];
+    const double smn = pn[e.leaf_end] - pn[e.leaf_begin];
+    double fl = videntity ? 0.0 : 2.0 * w * smat;   // expansion: a copy, not arithmetic
+    const double by = 8.0 * (smat + smn * w);
     fl_eval += fl;
     by_eval += by;
     e.cost = (int64_t)(by + fl);
@@ -224,7 +224,10 @@ struct Planner {
   void sync_ranks(int* d_ranks, const std::vector<int>& fp_ids) {
     if (fp_ids.empty()) return;
     std::vector<int> h(fp_ids.size());
+    auto a = std::chrono::steady_clock::now();
     HM_CUDA(cudaStreamSynchronize(c->stream));
+    c->pinned_reset();   // every staged upload has completed
+    t_wait += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
     HM_CUDA(cudaMemcpy(h.data(), d_ranks, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < fp_ids.size(); i++) fps[fp_ids[i]].k = h[i];
   }
@@ -557,6 +560,18 @@ struct Planner {
     zresult.assign(T.nblocks(), -1);
     lx = leaf_table(*X);
     ly = leaf_table(*Y);
+    for (int side = 0; side < 2; side++) {
+      const std::vector<LeafDesc>& lt = side ? ly : lx;
+      std::vector<double>& pm = side ? ly_mat : lx_mat;
+      std::vector<double>& pn = side ? ly_mn : lx_mn;
+      pm.assign(lt.size() + 1, 0.0);
+      pn.assign(lt.size() + 1, 0.0);
+      for (size_t i = 0; i < lt.size(); i++) {
+        const LeafDesc& L = lt[i];
+        pm[i + 1] = pm[i] + (L.kind == HM_BLOCK_DENSE ? (double)L.m * L.n : (double)L.k * (L.m + L.n));
+        pn[i + 1] = pn[i] + (double)(L.m + L.n);
+      }
+    }
     dlx = persist.upload(lx);
     dly = persist.upload(ly);
     Node root;
@@ -567,14 +582,30 @@ struct Planner {
     addproduct(root, 0, 0);
     levels.push_back({});
     levels.back().push_back(std::move(root));
+    using clk = std::chrono::steady_clock;
+    auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+    double t_level = 0, t_split = 0, t_merge = 0, t_fin = 0;
     while (true) {
+      auto a = clk::now();
       run_level(levels.back());
+      auto b = clk::now();
       std::vector<Node> next = split_level(levels.back());
+      auto d = clk::now();
+      t_level += sec(a, b);
+      t_split += sec(b, d);
       if (next.empty()) break;
       levels.push_back(std::move(next));
     }
+    auto a = clk::now();
     merges();
+    auto b = clk::now();
     finish();
+    auto d = clk::now();
+    t_merge = sec(a, b);
+    t_fin = sec(b, d);
+    if (std::getenv("HM_DEBUG_TIMING"))
+      std::fprintf(stderr, "[hm_addmul] levels %.3fs (sync wait %.3fs) split %.3fs merges %.3fs finish %.3fs\n",
+                   t_level, t_wait, t_split, t_merge, t_fin);
   }
 };
 

@@ -144,6 +144,13 @@ hm_status hm_ctx_create(int device, void* cuda_stream, const hm_allocator* alloc
     int major = 0;
     HM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
     if (major != 10) throw Error(HM_EUNSUPPORTED, "libhm is built for sm_100a (B200) only");
+    // keep freed stream-ordered allocations cached in the pool: every level of
+    // hm_addmul allocates and frees its stacks, and re-mapping tens of GB per
+    // level would dominate the run time.
+    cudaMemPool_t pool;
+    HM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    HM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   });
   if (s != HM_OK) {
     delete c;
@@ -394,7 +401,8 @@ hm_status hm_profile_get(hm_ctx ctx, hm_prof_t* out) {
   return guard(ctx, [&] {
     ctx->c.prof_collect();
     static const char* names[PC_COUNT] = {"qr", "gemm_M", "jacobi_svd", "apply_q", "copy", "eval",
-                                          "dense_add", "memset", "gen", "build_gemm", "norm", "matvec"};
+                                          "dense_add", "memset", "gen", "build_gemm", "norm", "matvec",
+                                          "svd_smem3k", "svd_smem8k", "svd_smem26k", "svd_global"};
     std::memset(out, 0, sizeof(*out));
     out->count = PC_COUNT;
     for (int i = 0; i < PC_COUNT; i++) {

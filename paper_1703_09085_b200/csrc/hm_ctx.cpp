@@ -1,4 +1,5 @@
 // Context, device arena, profiling and matrix bookkeeping of libhm.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -13,6 +14,29 @@ bool debug_sync() {
     v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
+}
+
+void* Ctx::pinned(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  if (pin_used + bytes > pin_cap) {
+    // recycle: wait until every copy from the staging buffer has completed
+    HM_CUDA(cudaStreamSynchronize(stream));
+    pin_used = 0;
+    if (bytes > pin_cap) {
+      if (pin) cudaFreeHost(pin);
+      pin = nullptr;
+      size_t cap = std::max(bytes, (size_t)256 << 20);
+      HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pin), cap));
+      pin_cap = cap;
+    }
+  }
+  void* p = pin + pin_used;
+  pin_used += bytes;
+  return p;
+}
+
+Ctx::~Ctx() {
+  if (pin) cudaFreeHost(pin);
 }
 
 void* Ctx::dmalloc(size_t bytes) {

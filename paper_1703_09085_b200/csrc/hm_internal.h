@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -39,7 +40,7 @@ bool debug_sync();   // HM_DEBUG_SYNC=1: synchronize and check after every launc
 
 enum ProfClass {
   PC_QR = 0, PC_GEMM_M, PC_SVD, PC_APPLYQ, PC_COPY, PC_EVAL, PC_DENSE, PC_MEMSET,
-  PC_GEN, PC_BUILD_GEMM, PC_NORM, PC_MATVEC, PC_COUNT
+  PC_GEN, PC_BUILD_GEMM, PC_NORM, PC_MATVEC, PC_SVD_B0, PC_SVD_B1, PC_SVD_B2, PC_SVD_B3, PC_COUNT
 };
 
 struct Ctx {
@@ -58,6 +59,14 @@ struct Ctx {
   int64_t launches[PC_COUNT] = {0};
   double flops[PC_COUNT] = {0};
   double bytes[PC_COUNT] = {0};
+
+  // pinned staging for job-descriptor uploads: bump allocation, recycled only
+  // after the stream has been synchronized (so in-flight copies are complete)
+  char* pin = nullptr;
+  size_t pin_cap = 0, pin_used = 0;
+  void* pinned(size_t bytes);
+  void pinned_reset() { pin_used = 0; }
+  ~Ctx();
 
   void* dmalloc(size_t bytes);
   void dfree(void* p, size_t bytes);
@@ -78,8 +87,11 @@ struct Arena {
   template <class T>
   T* upload(const std::vector<T>& v) {
     if (v.empty()) return nullptr;
-    T* d = static_cast<T*>(alloc_bytes(v.size() * sizeof(T)));
-    HM_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t bytes = v.size() * sizeof(T);
+    T* d = static_cast<T*>(alloc_bytes(bytes));
+    void* h = ctx->pinned(bytes);
+    std::memcpy(h, v.data(), bytes);
+    HM_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     return d;
   }
   void release();

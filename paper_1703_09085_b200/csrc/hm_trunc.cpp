@@ -10,6 +10,8 @@
 // to rounding.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "hm_internal.h"
 
@@ -121,30 +123,52 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
   // --- Jacobi SVD + rank rule + U_k / V_k S_k, bucketed by smem need
   std::vector<SvdJob> sj[4];
   int caps[4] = {3 * 1024, 8 * 1024, 26 * 1024, 0};
-  double fl_svd = 0;
+  double fl_svd = 0, fl_b[4] = {0, 0, 0, 0};
+  const char* dump = std::getenv("HM_DUMP_JOBS");
+  int* d_sw = dump ? static_cast<int*>(ar.alloc_bytes(sizeof(int) * (nj + 1))) : nullptr;
+  std::vector<int> bucket_of(nj);
   for (int i = 0; i < nj; i++) {
     const TruncReq& r = reqs[i];
     SvdJob s{};
+    s.nsweep = d_sw ? d_sw + i : nullptr;
     s.M = Mp[i]; s.p = p[i]; s.q = q[i]; s.ldm = std::max(p[i], 1);
     s.Aout = r.Aout; s.lda = r.m; s.ma = r.m;
     s.Bout = r.Bout; s.ldb = r.n; s.nb = r.n;
     s.rank = r.d_rank;
     s.sigma = r.d_sigma;
     const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
-    const int64_t need = (int64_t)L * cc + (int64_t)cc * cc + 2 * (int64_t)cc;
+    const int64_t need = (int64_t)L * cc + 2 * (int64_t)cc * cc + 6 * (int64_t)cc;
     const int cap = bucket_cap(need);
     fl_svd += 22.0 * (double)cc * cc * cc;
     int b = 3;
     for (int k = 0; k < 3; k++)
       if (cap == caps[k]) { b = k; break; }
+    fl_b[b] += 22.0 * (double)cc * cc * cc;
+    bucket_of[i] = b;
     if (b == 3) s.work = ar.alloc((size_t)need);
     sj[b].push_back(s);
   }
   {
     ProfScope ps(c, PC_SVD, fl_svd, 0);
-    for (int b = 0; b < 4; b++)
-      if (!sj[b].empty()) launch_svd(ar.upload(sj[b]), (int)sj[b].size(), eps, caps[b], st);
+    for (int b = 0; b < 4; b++) {
+      if (sj[b].empty()) continue;
+      ProfScope pb(c, PC_SVD_B0 + b, fl_b[b], (double)sj[b].size());
+      launch_svd(ar.upload(sj[b]), (int)sj[b].size(), eps, caps[b], st);
+    }
     HM_CHECK_LAUNCH();
+  }
+  if (dump) {
+    std::vector<int> sw(nj);
+    HM_CUDA(cudaStreamSynchronize(st));
+    HM_CUDA(cudaMemcpy(sw.data(), d_sw, sizeof(int) * nj, cudaMemcpyDeviceToHost));
+    FILE* f = std::fopen(dump, "a");
+    if (f) {
+      for (int i = 0; i < nj; i++)
+        std::fprintf(f, "%d %d %d %d %d %d %d\n", reqs[i].m, reqs[i].n, reqs[i].l, p[i], q[i], sw[i],
+                     bucket_of[i]);
+      std::fprintf(f, "# batch %d\n", nj);
+      std::fclose(f);
+    }
   }
   // --- apply Q_A, Q_B
   std::vector<ApplyQJob> aq;

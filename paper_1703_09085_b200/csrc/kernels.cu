@@ -18,7 +18,7 @@ namespace hm {
 static constexpr double kU = 1.1102230246251565e-16;  // unit roundoff 2^-53
 
 static std::atomic<long long> g_launches{0};
-static inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(); }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -241,165 +241,7 @@ void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st) {
   k_applyq<<<njobs, 256, 0, st>>>(d_jobs);
 }
 
-// ------------------------------------------------------------------ SVD
-// One-sided (Hestenes) Jacobi on C = M or M^T (L x c, c = min(p,q)),
-// round-robin parallel ordering, one warp per column pair.
-__device__ __forceinline__ int rr_pos(int k, int r, int cp) {
-  return k == 0 ? 0 : ((k - 1 + r) % (cp - 1)) + 1;
-}
-
-__global__ void __launch_bounds__(256) k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
-  extern __shared__ double sm[];
-  __shared__ double red[32];
-  __shared__ int s_rank;
-  const SvdJob J = jobs[blockIdx.x];
-  const int p = J.p, q = J.q;
-  const bool tr = p < q;
-  const int L = tr ? q : p, c = tr ? p : q;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (c == 0) {
-    if (tid == 0) *J.rank = 0;
-    return;
-  }
-  const int64_t need = (int64_t)L * c + (int64_t)c * c + 2 * (int64_t)c;
-  double* C = (need <= cap) ? sm : J.work;
-  double* Vr = C + (int64_t)L * c;          // accumulated rotations (c x c)
-  double* sig = Vr + (int64_t)c * c;
-  int* order = reinterpret_cast<int*>(sig + c);
-  for (int64_t e = tid; e < (int64_t)L * c; e += 256) {
-    const int i = (int)(e % L), j = (int)(e / L);
-    C[e] = tr ? J.M[j + (int64_t)i * J.ldm] : J.M[i + (int64_t)j * J.ldm];
-  }
-  for (int64_t e = tid; e < (int64_t)c * c; e += 256) Vr[e] = ((e % c) == (e / c)) ? 1.0 : 0.0;
-  __syncthreads();
-  double part = 0.0;
-  for (int64_t e = tid; e < (int64_t)L * c; e += 256) part += C[e] * C[e];
-  const double fro2 = block_sum(part, red);
-  const double tol = 2.0 * kU * sqrt((double)L);
-  const double tiny2 = (kU * kU) * fro2;   // both columns at rounding level
-  const int cp = c + (c & 1);
-  for (int sweep = 0; sweep < 80 && c > 1; sweep++) {
-    int rot = 0;
-    for (int r = 0; r < cp - 1; r++) {
-      for (int pr = warp; pr < (cp >> 1); pr += 8) {
-        const int a = rr_pos(pr, r, cp), b = rr_pos(cp - 1 - pr, r, cp);
-        if (a >= c || b >= c) continue;
-        double* x = C + (int64_t)a * L;
-        double* y = C + (int64_t)b * L;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < L; i += 32) {
-          const double xv = x[i], yv = y[i];
-          al = fma(xv, xv, al);
-          be = fma(yv, yv, be);
-          ga = fma(xv, yv, ga);
-        }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (fabs(ga) > tol * sqrt(al) * sqrt(be) && fmax(al, be) > tiny2) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          for (int i = lane; i < L; i += 32) {
-            const double xv = x[i], yv = y[i];
-            x[i] = cs * xv - sn * yv;
-            y[i] = sn * xv + cs * yv;
-          }
-          double* u = Vr + (int64_t)a * c;
-          double* v = Vr + (int64_t)b * c;
-          for (int i = lane; i < c; i += 32) {
-            const double uv = u[i], vv = v[i];
-            u[i] = cs * uv - sn * vv;
-            v[i] = sn * uv + cs * vv;
-          }
-          rot = 1;
-        }
-      }
-      __syncthreads();
-    }
-    if (!__syncthreads_or(rot)) break;   // converged: no pair rotated in this sweep
-  }
-  // singular values = column norms of C V
-  for (int j = warp; j < c; j += 8) {
-    const double* x = C + (int64_t)j * L;
-    double s = 0.0;
-    for (int i = lane; i < L; i += 32) s = fma(x[i], x[i], s);
-    s = warp_sum(s);
-    if (lane == 0) sig[j] = sqrt(s);
-  }
-  __syncthreads();
-  for (int j = tid; j < c; j += 256) {
-    const double sj = sig[j];
-    int pos = 0;
-    for (int i = 0; i < c; i++) {
-      const double si = sig[i];
-      pos += (si > sj) || (si == sj && i < j);
-    }
-    order[pos] = j;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // rank rule (DESIGN.md §3 R1): smallest k with sum_{i>k} s_i^2 <= eps^2 sum s_i^2,
-    // tails accumulated from the smallest singular value upward.
-    double acc = 0.0;
-    for (int i = c - 1; i >= 0; i--) { const double s = sig[order[i]]; acc += s * s; }
-    const double total = acc;
-    int k = 0;
-    if (total > 0.0) {
-      const double thr = (eps * eps) * total;
-      double tail = 0.0;
-      k = c;
-      for (int kk = c; kk >= 0; kk--) {
-        if (kk < c) { const double s = sig[order[kk]]; tail += s * s; }
-        if (tail <= thr) k = kk; else break;
-      }
-    }
-    s_rank = k;
-    *J.rank = k;
-  }
-  __syncthreads();
-  const int k = s_rank;
-  if (J.sigma)
-    for (int i = tid; i < c; i += 256) J.sigma[i] = sig[order[i]];
-  if (!tr) {
-    // C V = M V = U Sigma:  A = U_k = (C V)_k / sigma ; B = V_k Sigma_k
-    for (int64_t e = tid; e < (int64_t)J.ma * k; e += 256) {
-      const int r = (int)(e % J.ma), i = (int)(e / J.ma);
-      const int j = order[i];
-      J.Aout[r + (int64_t)i * J.lda] = (r < p) ? C[r + (int64_t)j * L] / sig[j] : 0.0;
-    }
-    for (int64_t e = tid; e < (int64_t)J.nb * k; e += 256) {
-      const int r = (int)(e % J.nb), i = (int)(e / J.nb);
-      const int j = order[i];
-      J.Bout[r + (int64_t)i * J.ldb] = (r < q) ? Vr[r + (int64_t)j * c] * sig[j] : 0.0;
-    }
-  } else {
-    // C V = M^T V = V_M Sigma:  A = U_k = V_k(rotations) ; B = (C V)_k
-    for (int64_t e = tid; e < (int64_t)J.ma * k; e += 256) {
-      const int r = (int)(e % J.ma), i = (int)(e / J.ma);
-      J.Aout[r + (int64_t)i * J.lda] = (r < p) ? Vr[r + (int64_t)order[i] * c] : 0.0;
-    }
-    for (int64_t e = tid; e < (int64_t)J.nb * k; e += 256) {
-      const int r = (int)(e % J.nb), i = (int)(e / J.nb);
-      J.Bout[r + (int64_t)i * J.ldb] = (r < q) ? C[r + (int64_t)order[i] * L] : 0.0;
-    }
-  }
-}
-
-int svd_smem_capacity() { return 26 * 1024; }
-
-void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
-  if (njobs <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_svd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         svd_smem_capacity() * 8);
-    attr = true;
-  }
-  if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
-  count_launch();
-  k_svd<<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, eps, cap);
-}
+// SVD kernels: see svd.cu
 
 // ------------------------------------------------------------------ copy
 __global__ void __launch_bounds__(256) k_copy(const CopyJob* __restrict__ jobs, int njobs) {

@@ -59,6 +59,7 @@ struct SvdJob {
   int* rank;
   double* sigma;
   double* work;        // global work (L x c doubles) when it does not fit smem
+  int* nsweep;         // optional: number of Jacobi sweeps used (diagnostics)
 };
 
 // dst[0:rows, 0:cols] (+)= coef * op(src); identity: dst[d,d] = coef.
@@ -127,6 +128,7 @@ void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double
 void launch_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta, cudaStream_t st);
 
 int64_t launch_count();     // process-wide number of kernel launches
+void count_launch();        // called by every launcher
 int svd_smem_capacity();   // doubles available for the smem Jacobi path
 int qr_smem_capacity();
 

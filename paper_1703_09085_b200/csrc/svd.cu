@@ -1,0 +1,349 @@
+// Batched small SVD with the eps rank rule for TRUNC (§3 "Truncation",
+// P:L336-384; rank rule = DESIGN.md §3 R1), one CTA per matrix M (p x q).
+//
+// Algorithm, on C = M (p >= q) or C = M^T (p < q), L x c:
+//   1. Householder QR with column pivoting C P = Q R (Businger-Golub), stopped
+//      at step r~ once the trailing Frobenius norm is <= delta =
+//      4 u sqrt(c) ||M||_F: the dropped block only perturbs M by rounding-level
+//      amounts (the backward error of the QR/GEMM that formed M).  QRCP is
+//      also the classic preconditioner of one-sided Jacobi (Drmac-Veselic):
+//      kernel blocks need ~6 sweeps on R^T instead of ~25 on M.
+//   2. One-sided Jacobi (Hestenes) on X = R^T (c x r~), round-robin parallel
+//      ordering, one warp per column pair, rotations accumulated in V (r~ x r~).
+//   3. sigma_i = ||X V e_i||, descending order, smallest k with
+//      sum_{i>k} sigma_i^2 <= eps^2 sum_i sigma_i^2 (tails from the bottom).
+//   4. Factors: C = Q V Sigma (W/sigma)^T P^T with W = X V, so
+//        p >= q: U_k = Q [V_k; 0],        V_k S_k = P W_k
+//        p <  q: U_k = P W_k / sigma_k,   V_k S_k = Q [V_k S_k; 0]
+//      (Q applied from the stored reflectors).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace hm {
+
+static constexpr double kUs = 1.1102230246251565e-16;  // 2^-53
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ double bsum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = wsum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s = (lane < nw) ? red[lane] : 0.0;
+    s = wsum(s);
+    if (lane == 0) red[0] = s;
+  }
+  __syncthreads();
+  const double s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// block argmax (value, lowest index on ties) and sum; results broadcast.
+__device__ void bargmax_sum(double v, int idx, double s, double* redv, int* redi, double* reds,
+                            double& vmax, int& imax, double& ssum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  __syncthreads();
+  if (lane == 0) { redv[warp] = v; redi[warp] = idx; reds[warp] = s; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = (lane < nw) ? redv[lane] : -1.0;
+    idx = (lane < nw) ? redi[lane] : 0x7fffffff;
+    s = (lane < nw) ? reds[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if (lane == 0) { redv[0] = v; redi[0] = idx; reds[0] = s; }
+  }
+  __syncthreads();
+  vmax = redv[0];
+  imax = redi[0];
+  ssum = reds[0];
+  __syncthreads();
+}
+
+__device__ __forceinline__ int rr_pos(int k, int r, int cp) {
+  return k == 0 ? 0 : ((k - 1 + r) % (cp - 1)) + 1;
+}
+
+int svd_smem_need(int p, int q) {
+  const int64_t L = p > q ? p : q, c = p < q ? p : q;
+  return (int)(L * c + 2 * c * c + 6 * c);
+}
+
+__global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
+  extern __shared__ double sm[];
+  __shared__ double red[32], redv[32], reds[32];
+  __shared__ int redi[32];
+  __shared__ int s_rank;
+  __shared__ double s_tau, s_scale;
+  const SvdJob J = jobs[blockIdx.x];
+  const int p = J.p, q = J.q;
+  const bool tr = p < q;
+  const int L = tr ? q : p, c = tr ? p : q;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
+  if (c == 0) {
+    if (tid == 0) *J.rank = 0;
+    if (J.nsweep && tid == 0) *J.nsweep = 0;
+    return;
+  }
+  const int64_t need = (int64_t)L * c + 2 * (int64_t)c * c + 6 * (int64_t)c;
+  double* C = (need <= cap) ? sm : J.work;      // L x c, QRCP in place
+  double* X = C + (int64_t)L * c;               // c x rt   (R^T, then W = X V)
+  double* V = X + (int64_t)c * c;               // rt x rt  (rotations)
+  double* tau = V + (int64_t)c * c;             // c
+  double* nrm = tau + c;                        // c
+  double* sig = nrm + c;                        // c
+  int* perm = reinterpret_cast<int*>(sig + c);  // c
+  int* order = perm + c;                        // c
+  for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
+    const int i = (int)(e % L), j = (int)(e / L);
+    C[e] = tr ? J.M[j + (int64_t)i * J.ldm] : J.M[i + (int64_t)j * J.ldm];
+  }
+  for (int j = tid; j < c; j += NT) perm[j] = j;
+  __syncthreads();
+  for (int j = warp; j < c; j += NW) {
+    const double* x = C + (int64_t)j * L;
+    double s = 0.0;
+    for (int i = lane; i < L; i += 32) s = fma(x[i], x[i], s);
+    s = wsum(s);
+    if (lane == 0) nrm[j] = s;
+  }
+  __syncthreads();
+  double part = 0.0;
+  for (int j = tid; j < c; j += NT) part += nrm[j];
+  const double fro2 = bsum(part, red);
+  const double delta2 = (16.0 * kUs * kUs) * (double)c * fro2;
+  // ---------------------------------------------------------------- 1. QRCP
+  int rt = 0;
+  for (int j = 0; j < c && j < L; j++) {
+    double v = -1.0, s = 0.0;
+    int idx = 0x7fffffff;
+    for (int col = j + tid; col < c; col += NT) {
+      const double w = nrm[col];
+      s += w;
+      if (w > v) { v = w; idx = col; }
+    }
+    double vmax, rem;
+    int piv;
+    bargmax_sum(v, idx, s, redv, redi, reds, vmax, piv, rem);
+    if (!(rem > delta2)) break;
+    if (piv != j) {
+      double* a = C + (int64_t)j * L;
+      double* b = C + (int64_t)piv * L;
+      for (int i = tid; i < L; i += NT) { const double t = a[i]; a[i] = b[i]; b[i] = t; }
+      if (tid == 0) {
+        const double t = nrm[j]; nrm[j] = nrm[piv]; nrm[piv] = t;
+        const int pt = perm[j]; perm[j] = perm[piv]; perm[piv] = pt;
+      }
+      __syncthreads();
+    }
+    double* x = C + (int64_t)j * L;
+    double pp = 0.0;
+    for (int i = j + 1 + tid; i < L; i += NT) pp = fma(x[i], x[i], pp);
+    const double xn2 = bsum(pp, red);
+    if (tid == 0) {
+      const double alpha = x[j];
+      double t = 0.0, sc = 0.0, beta = alpha;
+      if (xn2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        t = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+      x[j] = beta;
+      tau[j] = t;
+      s_tau = t;
+      s_scale = sc;
+    }
+    __syncthreads();
+    const double t = s_tau, sc = s_scale;
+    if (t != 0.0)
+      for (int i = j + 1 + tid; i < L; i += NT) x[i] *= sc;
+    __syncthreads();
+    for (int col = j + 1 + warp; col < c; col += NW) {
+      double* y = C + (int64_t)col * L;
+      double d = 0.0;
+      if (t != 0.0) {
+        for (int i = j + 1 + lane; i < L; i += 32) d = fma(x[i], y[i], d);
+        d = (wsum(d) + y[j]) * t;
+        if (lane == 0) y[j] -= d;
+      }
+      double nn = 0.0;
+      for (int i = j + 1 + lane; i < L; i += 32) {
+        const double yi = y[i] - d * x[i];
+        y[i] = yi;
+        nn = fma(yi, yi, nn);
+      }
+      nn = wsum(nn);
+      if (lane == 0) nrm[col] = nn;
+    }
+    __syncthreads();
+    rt = j + 1;
+  }
+  // X = R^T (c x rt), V = I
+  for (int64_t e = tid; e < (int64_t)c * rt; e += NT) {
+    const int col = (int)(e % c), i = (int)(e / c);
+    X[e] = (col >= i) ? C[i + (int64_t)col * L] : 0.0;
+  }
+  for (int64_t e = tid; e < (int64_t)rt * rt; e += NT) V[e] = ((e % rt) == (e / rt)) ? 1.0 : 0.0;
+  __syncthreads();
+  // ---------------------------------------------------------------- 2. Jacobi
+  const double tol = kUs * sqrt((double)c);
+  const int cp = rt + (rt & 1);
+  int sweep = 0;
+  for (; sweep < 60 && rt > 1; sweep++) {
+    int rot = 0;
+    for (int r = 0; r < cp - 1; r++) {
+      for (int pr = warp; pr < (cp >> 1); pr += NW) {
+        const int a = rr_pos(pr, r, cp), b = rr_pos(cp - 1 - pr, r, cp);
+        if (a >= rt || b >= rt) continue;
+        double* x = X + (int64_t)a * c;
+        double* y = X + (int64_t)b * c;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < c; i += 32) {
+          const double xv = x[i], yv = y[i];
+          al = fma(xv, xv, al);
+          be = fma(yv, yv, be);
+          ga = fma(xv, yv, ga);
+        }
+        al = wsum(al);
+        be = wsum(be);
+        ga = wsum(ga);
+        if (fabs(ga) > tol * sqrt(al) * sqrt(be) && fmin(al, be) > delta2) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tt = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
+          const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+          for (int i = lane; i < c; i += 32) {
+            const double xv = x[i], yv = y[i];
+            x[i] = cs * xv - sn * yv;
+            y[i] = sn * xv + cs * yv;
+          }
+          double* u = V + (int64_t)a * rt;
+          double* w = V + (int64_t)b * rt;
+          for (int i = lane; i < rt; i += 32) {
+            const double uv = u[i], wv = w[i];
+            u[i] = cs * uv - sn * wv;
+            w[i] = sn * uv + cs * wv;
+          }
+          rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rot)) break;
+  }
+  if (tid == 0 && J.nsweep) *J.nsweep = sweep + 1000 * rt;
+  // ---------------------------------------------------------------- 3. rank
+  for (int j = warp; j < rt; j += NW) {
+    const double* x = X + (int64_t)j * c;
+    double s = 0.0;
+    for (int i = lane; i < c; i += 32) s = fma(x[i], x[i], s);
+    s = wsum(s);
+    if (lane == 0) sig[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < rt; j += NT) {
+    const double sj = sig[j];
+    int pos = 0;
+    for (int i = 0; i < rt; i++) {
+      const double si = sig[i];
+      pos += (si > sj) || (si == sj && i < j);
+    }
+    order[pos] = j;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double acc = 0.0;
+    for (int i = rt - 1; i >= 0; i--) { const double s = sig[order[i]]; acc += s * s; }
+    int k = 0;
+    if (acc > 0.0) {
+      const double thr = (eps * eps) * acc;
+      double tail = 0.0;
+      k = rt;
+      for (int kk = rt; kk >= 0; kk--) {
+        if (kk < rt) { const double s = sig[order[kk]]; tail += s * s; }
+        if (tail <= thr) k = kk; else break;
+      }
+    }
+    s_rank = k;
+    *J.rank = k;
+  }
+  __syncthreads();
+  const int k = s_rank;
+  if (J.sigma)
+    for (int i = tid; i < c; i += NT) J.sigma[i] = (i < rt) ? sig[order[i]] : 0.0;
+  // ---------------------------------------------------------------- 4. factors
+  // permuted side:  out[perm[r], i] = W[r, order[i]] * f   (r < c), zero rows c..
+  // Q side:         out[:, i] = Q [V[:, order[i]] * g ; 0]   (L rows), zero rows L..
+  double* Pout = tr ? J.Aout : J.Bout;
+  const int Pld = tr ? J.lda : J.ldb, Prows = tr ? J.ma : J.nb;
+  double* Qout = tr ? J.Bout : J.Aout;
+  const int Qld = tr ? J.ldb : J.lda, Qrows = tr ? J.nb : J.ma;
+  for (int64_t e = tid; e < (int64_t)Prows * k; e += NT) {
+    const int r = (int)(e % Prows), i = (int)(e / Prows);
+    if (r >= c) Pout[r + (int64_t)i * Pld] = 0.0;
+  }
+  for (int64_t e = tid; e < (int64_t)c * k; e += NT) {
+    const int r = (int)(e % c), i = (int)(e / c);
+    const int j = order[i];
+    const double f = tr ? 1.0 / sig[j] : 1.0;
+    Pout[perm[r] + (int64_t)i * Pld] = X[r + (int64_t)j * c] * f;
+  }
+  for (int i = warp; i < k; i += NW) {
+    const int j = order[i];
+    const double g = tr ? sig[j] : 1.0;
+    double* y = Qout + (int64_t)i * Qld;
+    for (int r = lane; r < Qrows; r += 32) y[r] = (r < rt) ? V[r + (int64_t)j * rt] * g : 0.0;
+    __syncwarp();
+    for (int jj = rt - 1; jj >= 0; jj--) {
+      const double t = tau[jj];
+      if (t == 0.0) continue;
+      const double* v = C + (int64_t)jj * L;
+      double d = 0.0;
+      for (int r = jj + 1 + lane; r < L; r += 32) d = fma(v[r], y[r], d);
+      d = (wsum(d) + y[jj]) * t;
+      if (lane == 0) y[jj] -= d;
+      for (int r = jj + 1 + lane; r < L; r += 32) y[r] -= d * v[r];
+      __syncwarp();
+    }
+  }
+}
+
+int svd_smem_capacity() { return 26 * 1024; }
+
+void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, svd_smem_capacity() * 8);
+    attr = true;
+  }
+  if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
+  const int threads = (cap == 0 || cap > 8 * 1024) ? 512 : 256;
+  count_launch();
+  k_svd<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, cap);
+}
+
+}  // namespace hm
