@@ -232,7 +232,13 @@ struct Planner {
     for (size_t i = 0; i < fp_ids.size(); i++) fps[fp_ids[i]].k = h[i];
   }
 
+  double t_a = 0, t_b = 0, t_c = 0, t_d = 0;
+  static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+
   void run_level(std::vector<Node>& nodes) {
+    double t0 = now_s();
     Arena scratch(c);
     std::vector<Stack> stacks;
     for (int i = 0; i < (int)nodes.size(); i++) {
@@ -272,6 +278,8 @@ struct Planner {
       s.B = buf + off;
       off += (size_t)s.n * s.l;
     }
+    double t1 = now_s();
+    t_a += t1 - t0;
     std::vector<CopyJob> cj;
     std::vector<EvalJob> ej;
     int64_t ctiles = 0;
@@ -300,6 +308,8 @@ struct Planner {
       launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
       HM_CHECK_LAUNCH();
     }
+    double t2 = now_s();
+    t_b += t2 - t1;
     if (!ej.empty()) {
       std::stable_sort(ej.begin(), ej.end(),
                        [](const EvalJob& a, const EvalJob& b) { return a.cost > b.cost; });
@@ -345,7 +355,10 @@ struct Planner {
       launch_gemm(scratch.upload(gj), (int)gj.size(), gtiles, c->stream);
       HM_CHECK_LAUNCH();
     }
+    double t3 = now_s();
+    t_c += t3 - t2;
     trunc_batched(c, scratch, tr, eps);
+    t_d += now_s() - t3;
     sync_ranks(d_ranks, tr_fp);
     for (size_t i = 0; i < tr.size(); i++) {
       const double k = fps[tr_fp[i]].k;
@@ -604,8 +617,10 @@ struct Planner {
     t_merge = sec(a, b);
     t_fin = sec(b, d);
     if (std::getenv("HM_DEBUG_TIMING"))
-      std::fprintf(stderr, "[hm_addmul] levels %.3fs (sync wait %.3fs) split %.3fs merges %.3fs finish %.3fs\n",
-                   t_level, t_wait, t_split, t_merge, t_fin);
+      std::fprintf(stderr,
+                   "[hm_addmul] levels %.3fs (sync wait %.3fs; host: layout %.3f jobs %.3f launch %.3f trunc %.3f) "
+                   "split %.3fs merges %.3fs finish %.3fs\n",
+                   t_level, t_wait, t_a, t_b, t_c, t_d, t_split, t_merge, t_fin);
   }
 };
 

@@ -107,14 +107,29 @@ void Ctx::prof_collect() {
 
 void* Arena::alloc_bytes(size_t bytes) {
   bytes = (bytes + 255) & ~size_t(255);
-  void* p = ctx->dmalloc(bytes);
-  blocks.push_back({p, bytes});
+  if (bytes > cur_left) {
+    if (bytes >= chunk_min) {   // large request: its own block, keep the current chunk
+      void* p = ctx->dmalloc(bytes);
+      blocks.push_back({p, bytes});
+      return p;
+    }
+    const size_t sz = chunk_min;
+    chunk_min = std::min(chunk_min * 2, (size_t)1 << 30);
+    cur = static_cast<char*>(ctx->dmalloc(sz));
+    blocks.push_back({cur, sz});
+    cur_left = sz;
+  }
+  void* p = cur;
+  cur += bytes;
+  cur_left -= bytes;
   return p;
 }
 
 void Arena::release() {
   for (auto& b : blocks) ctx->dfree(b.first, b.second);
   blocks.clear();
+  cur = nullptr;
+  cur_left = 0;
 }
 
 void Mat::free_all(Ctx* c) {

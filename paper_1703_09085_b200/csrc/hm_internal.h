@@ -76,10 +76,14 @@ struct Ctx {
   void prof_collect();   // synchronizes pending events
 };
 
-// Stream-ordered device arena: every allocation is released by release().
+// Stream-ordered device arena: bump allocation inside large chunks (few
+// cudaMallocAsync calls per level); everything is released by release().
 struct Arena {
   Ctx* ctx;
   std::vector<std::pair<void*, size_t>> blocks;
+  char* cur = nullptr;
+  size_t cur_left = 0;
+  size_t chunk_min = (size_t)64 << 20;
   explicit Arena(Ctx* c) : ctx(c) {}
   ~Arena() { release(); }
   void* alloc_bytes(size_t bytes);

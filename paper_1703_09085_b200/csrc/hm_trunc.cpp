@@ -92,8 +92,19 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
   {
     ProfScope ps(c, PC_QR, fl_qr, 0);
     if (!qr_small.empty()) launch_qr(ar.upload(qr_small), (int)qr_small.size(), 4 * 1024, st);
-    if (!qr_big.empty()) launch_qr(ar.upload(qr_big), (int)qr_big.size(), qr_smem_capacity(), st);
-    if (!qr_glob.empty()) launch_qr(ar.upload(qr_glob), (int)qr_glob.size(), 0, st);
+    // blocked (compact-WY) QR, bucketed by panel height so that small panels
+    // get several CTAs per SM: cap = 16 * rows doubles of shared memory
+    std::vector<QrJob> qb[4], qr_huge;
+    const int qcap[4] = {6 * 1024, 12 * 1024, 24 * 1024, 24 * 1024};
+    for (auto* v : {&qr_big, &qr_glob})
+      for (auto& j : *v) {
+        if (j.m > 24 * 1024) { qr_huge.push_back(j); continue; }
+        const int b = j.m <= 384 ? 0 : (j.m <= 768 ? 1 : (j.m <= 1536 ? 2 : 3));
+        qb[b].push_back(j);
+      }
+    for (int b = 0; b < 4; b++)
+      if (!qb[b].empty()) launch_qr_blocked(ar.upload(qb[b]), (int)qb[b].size(), qcap[b], st);
+    if (!qr_huge.empty()) launch_qr(ar.upload(qr_huge), (int)qr_huge.size(), 0, st);
     HM_CHECK_LAUNCH();
   }
   // --- M = R_A R_B^T

@@ -114,6 +114,7 @@ struct NormJob {
 
 void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
+void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);   // rows <= 24576
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
