@@ -222,15 +222,19 @@ class S2:
             acc.base = trunc(A, B, self.ctx)
             acc.terms = []
 
-    def split(self, acc: Acc2, tag):
+    def split(self, acc: Acc2, tag, lower_only=False):
         """Fig. 6 after reduce: sons inherit restrictions of the
-        base, pending products are expanded over sons(s)."""
+        base, pending products are expanded over sons(s).
+        lower_only (H-Cholesky): strictly upper sons are not created."""
         self.reduce(acc, tag)
         t, r = acc.t, acc.r
         grid = []
         for i, ti in enumerate(t.sons):
             row = []
             for j, rj in enumerate(r.sons):
+                if lower_only and ti.start < rj.start:
+                    row.append(None)
+                    continue
                 base = None
                 if acc.base is not None:
                     A0, B0 = acc.base

@@ -1,0 +1,30 @@
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel."""
+import collections
+import csv
+import sys
+
+
+def summarise(path):
+    rows = list(csv.reader(open(path)))
+    i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr, data = rows[i], rows[i + 1:]
+    ki, ui, vi = hdr.index("Kernel Name"), hdr.index("Metric Unit"), hdr.index("Metric Value")
+    scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in data:
+        if len(r) <= vi:
+            continue
+        ms = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        name = r[ki].split("(")[0]
+        agg[name][0] += 1
+        agg[name][1] += ms
+    tot = sum(v[1] for v in agg.values())
+    out = [f"| kernel | launches | ms (cold, serialised) | share |", "|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"| `{k}` | {v[0]} | {v[1]:.1f} | {100 * v[1] / tot:.1f}% |")
+    out.append(f"| total | {sum(v[0] for v in agg.values())} | {tot:.1f} | 100% |")
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    print(summarise(sys.argv[1]))
