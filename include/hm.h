@@ -113,6 +113,7 @@ typedef struct {
   double bytes_trunc;         /* SURVEY §8(d) convention bytes */
   double bytes_eval;
   double bytes_dense;
+  double min_pivot;           /* last hm_lr / hm_chol: min |pivot| of the leaf factorizations */
 } hm_stats_t;
 
 /* Per-kernel-class device timing (CUDA events on the context stream,

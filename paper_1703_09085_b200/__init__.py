@@ -205,6 +205,18 @@ def addmul(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps):
     Z.ctx.check(lib().hm_addmul(Z.ctx.h, float(alpha), X.h, Y.h, Z.h, float(eps)))
 
 
+def lr(G: HMatrix, eps):
+    """In-place H-LR with accumulated updates (hm_lr): strict lower part = L
+    (unit diagonal), upper part = R."""
+    G.ctx.check(lib().hm_lr(G.ctx.h, G.h, float(eps)))
+
+
+def chol(G: HMatrix, eps, shift=0.0):
+    """In-place H-Cholesky with accumulated updates of G + shift I (hm_chol);
+    lower part = L.  Raises HMError(HM_EPIVOT) naming the cluster on breakdown."""
+    G.ctx.check(lib().hm_chol(G.ctx.h, G.h, float(eps), float(shift)))
+
+
 def matvec(G: HMatrix, x, y, alpha=1.0, beta=0.0, op=0):
     """y <- alpha op(G) x + beta y for torch CUDA float64 tensors (n x c, column-major
     = x.T contiguous, or 1-D)."""
@@ -275,4 +287,4 @@ def test_trunc_batched(ctx: Context, stacks, eps):
     return out, ranks, sigmas
 
 
-__all__ = ["Context", "HMatrix", "HMError", "addmul", "matvec", "lib", "test_trunc_batched"]
+__all__ = ["Context", "HMatrix", "HMError", "addmul", "chol", "lr", "matvec", "lib", "test_trunc_batched"]

@@ -44,6 +44,7 @@ class Stats(C.Structure):
         ("dense_adds", C.c_int64), ("levels", C.c_int64), ("kernel_launches", C.c_int64),
         ("flops_trunc", C.c_double), ("flops_eval", C.c_double), ("flops_dense", C.c_double),
         ("bytes_trunc", C.c_double), ("bytes_eval", C.c_double), ("bytes_dense", C.c_double),
+        ("min_pivot", C.c_double),
     ]
 
 

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <unordered_map>
 
 #include "hm_internal.h"
 
@@ -48,6 +49,7 @@ struct Node {
   int red = -1;
   int result = -1;
   int child0 = -1;
+  bool force_split = false;   // H-LR/H-Cholesky: split (reduce + expand) even with P = 0
 };
 
 struct Planner {
@@ -67,11 +69,19 @@ struct Planner {
   int64_t n_addproduct = 0, n_eval = 0, n_trunc = 0, n_cols = 0, n_merge = 0, n_dense = 0;
   double fl_trunc = 0, by_trunc = 0, fl_eval = 0, by_eval = 0, fl_dense = 0, by_dense = 0;
 
+  // Y as a transpose view of a matrix over the same (symmetric) block tree
+  // (H-Cholesky: addproduct(-1, L_21, L_21^T)): block (s,r) of the view is
+  // block tmap[(s,r)] = (r,s) of *Y, transposed.
+  bool ytrans = false;
+  std::vector<int> tmap;
+  Arena* fp_arena = nullptr;   // where new_fp allocates (default: persist)
+
   Planner(Ctx* c_, const Tree& T_, Mat* X_, Mat* Y_, Mat* Z_, double a, double e)
       : c(c_), persist(c_), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {}
 
   int csize(int cl) const { return T.cl_size[cl]; }
   int cstart(int cl) const { return T.cl_start[cl]; }
+  int yb(int by) const { return ytrans ? tmap[by] : by; }
 
   // Fig. 5 classification in printed branch order.
   bool classify(int bx, int by, Term& out) const {
@@ -88,7 +98,7 @@ struct Planner {
     } else if (kx == HM_BLOCK_ADM) {
       out.br = 4; out.w = X->rank[bx];
     } else if (ky == HM_BLOCK_ADM) {
-      out.br = 5; out.w = Y->rank[by];
+      out.br = 5; out.w = Y->rank[yb(by)];
     } else {
       return false;
     }
@@ -116,8 +126,9 @@ struct Planner {
 
   int new_fp(int m, int n, int kcap, int t0, int r0) {
     FP f;
-    f.A = persist.alloc((size_t)m * std::max(kcap, 1));
-    f.B = persist.alloc((size_t)n * std::max(kcap, 1));
+    Arena& ar = fp_arena ? *fp_arena : persist;
+    f.A = ar.alloc((size_t)m * std::max(kcap, 1));
+    f.B = ar.alloc((size_t)n * std::max(kcap, 1));
     f.lda = m;
     f.ldb = n;
     f.t0 = t0;
@@ -146,14 +157,16 @@ struct Planner {
     cj.push_back(j);
   }
 
-  void add_eval(std::vector<EvalJob>& ej, bool yside, int blk, double coef, double* out, int ldo,
-                int w, const double* V, int ldv, int vtrans, int videntity) {
+  // H-side product over the DFS leaves of block blk of X (yside = false) or Y
+  // (yside = true); trans: out += coef H|_blk^T V instead of H|_blk V.
+  void add_eval(std::vector<EvalJob>& ej, bool yside, int blk, int trans, double coef, double* out,
+                int ldo, int w, const double* V, int ldv, int vtrans, int videntity) {
     if (w <= 0) return;
     EvalJob e{};
     e.leaves = yside ? dly : dlx;
     e.leaf_begin = T.bl_lbeg[blk];
     e.leaf_end = T.bl_lend[blk];
-    e.trans = yside ? 1 : 0;
+    e.trans = trans;
     e.t0 = cstart(T.bl_row[blk]);
     e.s0 = cstart(T.bl_col[blk]);
     e.coef = coef;
@@ -186,30 +199,36 @@ struct Planner {
     const int nt = csize(t), ns = csize(s), nr = csize(r);
     double* a = SA + (size_t)col * m;
     double* b = SB + (size_t)col * n;
+    // Y|sr^T V: addevaltrans over Y's block (s,r); for a transpose view it is
+    // addeval (no transpose) over the stored block (r,s).
+    const int ybk = yb(by);
+    const int ytr = ytrans ? 0 : 1;
     switch (tm.br) {
       case 0:  // A = alpha I_t ; B = Y|sr^T N_X^T
         add_copy(cj, ctiles, a, m, nullptr, 0, nt, nt, 0, 1, alpha);
-        add_eval(ej, true, by, 1.0, b, n, w, X->pA[bx], nt, 1, 0);
+        add_eval(ej, true, ybk, ytr, 1.0, b, n, w, X->pA[bx], nt, 1, 0);
         break;
       case 1:  // A = alpha N_X ; B = Y|sr^T I
         add_copy(cj, ctiles, a, m, X->pA[bx], nt, nt, ns, 0, 0, alpha);
-        add_eval(ej, true, by, 1.0, b, n, w, nullptr, 0, 0, 1);
+        add_eval(ej, true, ybk, ytr, 1.0, b, n, w, nullptr, 0, 0, 1);
         break;
-      case 2:  // B = I_r ; A = alpha X|ts N_Y
+      case 2:  // B = I_r ; A = alpha X|ts N_Y   (view: N_Y = N_(r,s)^T)
         add_copy(cj, ctiles, b, n, nullptr, 0, nr, nr, 0, 1, 1.0);
-        add_eval(ej, false, bx, alpha, a, m, w, Y->pA[by], ns, 0, 0);
+        if (ytrans) add_eval(ej, false, bx, 0, alpha, a, m, w, Y->pA[ybk], nr, 1, 0);
+        else add_eval(ej, false, bx, 0, alpha, a, m, w, Y->pA[by], ns, 0, 0);
         break;
-      case 3:  // B = N_Y^T ; A = alpha X|ts I
-        add_copy(cj, ctiles, b, n, Y->pA[by], ns, nr, ns, 1, 0, 1.0);
-        add_eval(ej, false, bx, alpha, a, m, w, nullptr, 0, 0, 1);
+      case 3:  // B = N_Y^T ; A = alpha X|ts I  (view: N_Y^T = N_(r,s))
+        if (ytrans) add_copy(cj, ctiles, b, n, Y->pA[ybk], nr, nr, ns, 0, 0, 1.0);
+        else add_copy(cj, ctiles, b, n, Y->pA[by], ns, nr, ns, 1, 0, 1.0);
+        add_eval(ej, false, bx, 0, alpha, a, m, w, nullptr, 0, 0, 1);
         break;
       case 4:  // A = alpha A_X ; B = Y|sr^T B_X
         add_copy(cj, ctiles, a, m, X->pA[bx], nt, nt, w, 0, 0, alpha);
-        add_eval(ej, true, by, 1.0, b, n, w, X->pB[bx], ns, 0, 0);
+        add_eval(ej, true, ybk, ytr, 1.0, b, n, w, X->pB[bx], ns, 0, 0);
         break;
-      case 5:  // B = B_Y ; A = alpha X|ts A_Y
-        add_copy(cj, ctiles, b, n, Y->pB[by], nr, nr, w, 0, 0, 1.0);
-        add_eval(ej, false, bx, alpha, a, m, w, Y->pA[by], ns, 0, 0);
+      case 5:  // B = B_Y ; A = alpha X|ts A_Y   (view: A_Y = B_(r,s), B_Y = A_(r,s))
+        add_copy(cj, ctiles, b, n, ytrans ? Y->pA[ybk] : Y->pB[by], nr, nr, w, 0, 0, 1.0);
+        add_eval(ej, false, bx, 0, alpha, a, m, w, ytrans ? Y->pB[ybk] : Y->pA[by], ns, 0, 0);
         break;
     }
   }
@@ -248,8 +267,8 @@ struct Planner {
       const int kb = nd.base >= 0 ? fps[nd.base].k : 0;
       int wt = 0;
       for (auto& tm : nd.terms) wt += tm.w;
-      if (!nd.pend.empty()) {
-        if (nd.zt == ZD)
+      if (!nd.pend.empty() || nd.force_split) {
+        if (nd.zt == ZD && !nd.force_split)
           throw Error(HM_ESTRUCT, "flush: pending products into an inadmissible leaf");
         if (!nd.terms.empty()) { kind = 1; l = kb + wt; }
         else nd.red = nd.base;
@@ -379,33 +398,46 @@ struct Planner {
     std::vector<Node> next;
     for (auto& nd : nodes) {
       if (nd.pend.empty()) continue;
-      const int t = nd.t, r = nd.r;
-      const int nts = T.cl_nsons[t], nrs = T.cl_nsons[r];
       nd.child0 = (int)next.size();
-      for (int i = 0; i < nts; i++) {
-        for (int j = 0; j < nrs; j++) {
-          Node ch;
-          ch.t = T.cl_son0[t] + i;
-          ch.r = T.cl_son0[r] + j;
-          if (nd.zt == ZS) {
-            const int zb = T.son(nd.zb, i, j);
-            ch.zb = zb;
-            ch.zt = T.bl_kind[zb] == HM_BLOCK_SUB ? ZS : (T.bl_kind[zb] == HM_BLOCK_ADM ? ZA : ZD);
-          } else {
-            ch.zt = ZV;
-            ch.zb = nd.zb;   // the real admissible leaf the temporaries restrict
-          }
-          ch.base = nd.red;
-          for (auto& p : nd.pend) {
-            const int s = T.bl_col[p.bx];
-            for (int l = 0; l < T.cl_nsons[s]; l++)
-              addproduct(ch, T.son(p.bx, i, l), T.son(p.by, l, j));
-          }
-          next.push_back(std::move(ch));
-        }
-      }
+      expand(nd, false, next);
     }
     return next;
+  }
+
+  // Fig. 6 sons of one accumulator (row-major over sons(t) x sons(r)); the sons
+  // inherit nd.red as base; pending products are expanded over sons(s).
+  // lower_only (H-Cholesky): strictly upper sons are not created (a null
+  // placeholder with t = -1 keeps the row-major indexing).
+  void expand(const Node& nd, bool lower_only, std::vector<Node>& out) {
+    const int t = nd.t, r = nd.r;
+    const int nts = T.cl_nsons[t], nrs = T.cl_nsons[r];
+    for (int i = 0; i < nts; i++) {
+      for (int j = 0; j < nrs; j++) {
+        Node ch;
+        ch.t = T.cl_son0[t] + i;
+        ch.r = T.cl_son0[r] + j;
+        if (lower_only && cstart(ch.t) < cstart(ch.r)) {
+          ch.t = -1;
+          out.push_back(std::move(ch));
+          continue;
+        }
+        if (nd.zt == ZS) {
+          const int zb = T.son(nd.zb, i, j);
+          ch.zb = zb;
+          ch.zt = T.bl_kind[zb] == HM_BLOCK_SUB ? ZS : (T.bl_kind[zb] == HM_BLOCK_ADM ? ZA : ZD);
+        } else {
+          ch.zt = ZV;
+          ch.zb = nd.zb;   // the real admissible leaf the temporaries restrict
+        }
+        ch.base = nd.red;
+        for (auto& p : nd.pend) {
+          const int s = T.bl_col[p.bx];
+          for (int l = 0; l < T.cl_nsons[s]; l++)
+            addproduct(ch, T.son(p.bx, i, l), T.son(p.by, l, j));
+        }
+        out.push_back(std::move(ch));
+      }
+    }
   }
 
   // Fig. 4 rkmerge of the temporaries below admissible leaves, bottom-up.
@@ -569,7 +601,31 @@ struct Planner {
     Z->fpool = {pool, (total + 1) * sizeof(double)};
   }
 
-  void run() {
+  // Level-synchronous flush of the given root accumulators (Fig. 7 with
+  // split/addproduct per level) followed by the bottom-up merges.
+  double t_level = 0, t_split = 0, t_merge = 0;
+  void run_from(std::vector<Node> roots) {
+    using clk = std::chrono::steady_clock;
+    auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+    levels.clear();
+    levels.push_back(std::move(roots));
+    while (true) {
+      auto a = clk::now();
+      run_level(levels.back());
+      auto b = clk::now();
+      std::vector<Node> next = split_level(levels.back());
+      auto d = clk::now();
+      t_level += sec(a, b);
+      t_split += sec(b, d);
+      if (next.empty()) break;
+      levels.push_back(std::move(next));
+    }
+    auto a = clk::now();
+    merges();
+    t_merge += sec(a, clk::now());
+  }
+
+  void setup_tables(bool upload) {
     zresult.assign(T.nblocks(), -1);
     lx = leaf_table(*X);
     ly = leaf_table(*Y);
@@ -585,37 +641,26 @@ struct Planner {
         pn[i + 1] = pn[i] + (double)(L.m + L.n);
       }
     }
-    dlx = persist.upload(lx);
-    dly = persist.upload(ly);
+    if (upload) {
+      dlx = persist.upload(lx);
+      dly = persist.upload(ly);
+    }
+  }
+
+  void run() {
+    setup_tables(true);
     Node root;
     root.t = T.bl_row[0];
     root.r = T.bl_col[0];
     root.zb = 0;
     root.zt = T.bl_kind[0] == HM_BLOCK_SUB ? ZS : (T.bl_kind[0] == HM_BLOCK_ADM ? ZA : ZD);
     addproduct(root, 0, 0);
-    levels.push_back({});
-    levels.back().push_back(std::move(root));
-    using clk = std::chrono::steady_clock;
-    auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
-    double t_level = 0, t_split = 0, t_merge = 0, t_fin = 0;
-    while (true) {
-      auto a = clk::now();
-      run_level(levels.back());
-      auto b = clk::now();
-      std::vector<Node> next = split_level(levels.back());
-      auto d = clk::now();
-      t_level += sec(a, b);
-      t_split += sec(b, d);
-      if (next.empty()) break;
-      levels.push_back(std::move(next));
-    }
-    auto a = clk::now();
-    merges();
-    auto b = clk::now();
+    std::vector<Node> roots;
+    roots.push_back(std::move(root));
+    run_from(std::move(roots));
+    auto b = std::chrono::steady_clock::now();
     finish();
-    auto d = clk::now();
-    t_merge = sec(a, b);
-    t_fin = sec(b, d);
+    const double t_fin = std::chrono::duration<double>(std::chrono::steady_clock::now() - b).count();
     if (std::getenv("HM_DEBUG_TIMING"))
       std::fprintf(stderr,
                    "[hm_addmul] levels %.3fs (sync wait %.3fs; host: layout %.3f jobs %.3f launch %.3f trunc %.3f) "
@@ -624,7 +669,379 @@ struct Planner {
   }
 };
 
+// ---------------------------------------------------------------------------
+// H-LR / H-Cholesky with accumulated updates (§6; the
+// recursion is the reading O8/O9 of SURVEY §8(c), also implemented in
+// oracle/factor.py).  Host-driven recursion; every accumulator operation
+// (reduce = T1, flush into a leaf incl. temporaries + rkmerge, addproduct)
+// goes through the Planner above, triangular solves through the H-structure
+// run as one k_trsm CTA per panel, dense diagonal leaves as k_leaf_factor.
+struct Factorizer {
+  Ctx* c;
+  Mat* G;
+  const Tree& T;
+  bool chol;
+  Planner P;
+  std::vector<LeafDesc> lt;
+  std::vector<int> leafpos;
+  LeafDesc* dlt = nullptr;
+  std::vector<std::pair<void*, size_t>> own;   // per block: factor buffer owned here
+  std::unordered_map<int64_t, int> bmap;       // (row, col) -> block id
+  int* d_fail = nullptr;
+  double* d_minpiv = nullptr;
+  int64_t n_trsm = 0, n_leaf = 0, n_flush = 0;
+
+  Factorizer(Ctx* c_, Mat* G_, double eps, bool ch)
+      : c(c_), G(G_), T(*G_->tree), chol(ch), P(c_, *G_->tree, G_, G_, G_, -1.0, eps) {
+    const int nb = T.nblocks();
+    for (int b = 0; b < nb; b++) bmap[key(T.bl_row[b], T.bl_col[b])] = b;
+    if (chol) {
+      P.ytrans = true;
+      P.tmap.resize(nb);
+      for (int b = 0; b < nb; b++) {
+        auto it = bmap.find(key(T.bl_col[b], T.bl_row[b]));
+        if (it == bmap.end() || T.bl_kind[it->second] != T.bl_kind[b])
+          throw Error(HM_ESTRUCT, "hm_chol: the block tree is not symmetric");
+        P.tmap[b] = it->second;
+      }
+    }
+    for (int t = 0; t < T.nclusters(); t++)
+      if (T.cl_nsons[t] != 0 && T.cl_nsons[t] != 2)
+        throw Error(HM_EUNSUPPORTED, "H-LR/H-Cholesky need a binary cluster tree (P:L1361-1363)");
+    P.setup_tables(false);
+    lt = P.lx;
+    leafpos.assign(nb, -1);
+    for (size_t i = 0; i < T.leaf_order.size(); i++) leafpos[T.leaf_order[i]] = (int)i;
+    dlt = P.persist.upload(lt);
+    P.dlx = P.dly = dlt;
+    own.assign(nb, {nullptr, 0});
+    d_fail = static_cast<int*>(P.persist.alloc_bytes(sizeof(int)));
+    HM_CUDA(cudaMemsetAsync(d_fail, 0, sizeof(int), c->stream));
+    d_minpiv = P.persist.alloc(T.nclusters());
+    HM_CUDA(cudaMemsetAsync(d_minpiv, 0, sizeof(double) * T.nclusters(), c->stream));
+  }
+
+  static int64_t key(int a, int b) { return ((int64_t)a << 32) | (uint32_t)b; }
+  int blk(int a, int b) const {
+    auto it = bmap.find(key(a, b));
+    if (it == bmap.end()) throw Error(HM_ESTRUCT, "internal: missing block");
+    return it->second;
+  }
+  int son0(int t) const { return T.cl_son0[t]; }
+
+  void patch_leaf(int b) {
+    const int pos = leafpos[b];
+    lt[pos].A = G->pA[b];
+    lt[pos].B = G->pB[b];
+    lt[pos].k = T.bl_kind[b] == HM_BLOCK_ADM ? G->rank[b] : 0;
+    void* h = c->pinned(sizeof(LeafDesc));
+    std::memcpy(h, &lt[pos], sizeof(LeafDesc));
+    HM_CUDA(cudaMemcpyAsync(dlt + pos, h, sizeof(LeafDesc), cudaMemcpyHostToDevice, c->stream));
+  }
+
+  Node acc_for(int b) const {
+    Node nd;
+    nd.t = T.bl_row[b];
+    nd.r = T.bl_col[b];
+    nd.zb = b;
+    nd.zt = T.bl_kind[b] == HM_BLOCK_SUB ? ZS : (T.bl_kind[b] == HM_BLOCK_ADM ? ZA : ZD);
+    return nd;
+  }
+
+  // Fig. 7 flush of an accumulator into the leaf nd.zb of G (branches i, ii, v).
+  void flush(const Node& nd) {
+    n_flush++;
+    Arena local(c);
+    P.fp_arena = &local;
+    const int zb = nd.zb;
+    P.zresult[zb] = -1;
+    std::vector<Node> roots{nd};
+    P.run_from(std::move(roots));
+    if (T.bl_kind[zb] == HM_BLOCK_ADM) {
+      const int f = P.zresult[zb];
+      if (f < 0) throw Error(HM_ESTRUCT, "internal: flush produced no result");
+      const FP& fp = P.fps[f];
+      const int m = fp.lda, n = fp.ldb, k = fp.k;
+      const size_t bytes = sizeof(double) * ((size_t)(m + n) * k + 1);
+      double* buf = static_cast<double*>(c->dmalloc(bytes));
+      if (k > 0) {
+        HM_CUDA(cudaMemcpyAsync(buf, fp.A, sizeof(double) * (size_t)m * k, cudaMemcpyDeviceToDevice, c->stream));
+        HM_CUDA(cudaMemcpyAsync(buf + (size_t)m * k, fp.B, sizeof(double) * (size_t)n * k,
+                                cudaMemcpyDeviceToDevice, c->stream));
+      }
+      if (own[zb].first) c->dfree(own[zb].first, own[zb].second);
+      own[zb] = {buf, bytes};
+      G->pA[zb] = buf;
+      G->pB[zb] = buf + (size_t)m * k;
+      G->rank[zb] = k;
+      patch_leaf(zb);
+    }
+    P.fp_arena = nullptr;
+    local.release();
+  }
+
+  // T1 reduce of an accumulator that is split (Fig. 6); result persists.
+  void reduce(Node& nd) {
+    if (nd.terms.empty()) {
+      nd.red = nd.base;
+      return;
+    }
+    std::vector<Node> one{nd};
+    one[0].force_split = true;
+    P.run_level(one);
+    nd.red = one[0].red;
+  }
+
+  std::vector<Node> split(Node& nd, bool lower_only) {
+    reduce(nd);
+    std::vector<Node> ch;
+    P.expand(nd, lower_only, ch);
+    return ch;
+  }
+
+  // ---- triangular solves through the H-structure (k_trsm step lists)
+  void steps_lower(int t, bool unit, int panel0, std::vector<TrsmStep>& st) {
+    if (T.cl_nsons[t] == 0) {
+      const int d = blk(t, t);
+      st.push_back(TrsmStep{0, T.cl_start[t] - panel0, T.cl_size[t], G->pA[d], T.cl_size[t], 0, unit ? 1 : 0, 0, 0});
+      return;
+    }
+    const int t1 = son0(t), t2 = t1 + 1;
+    steps_lower(t1, unit, panel0, st);
+    const int b = blk(t2, t1);
+    st.push_back(TrsmStep{1, 0, 0, nullptr, 0, 0, 0, T.bl_lbeg[b], T.bl_lend[b]});
+    steps_lower(t2, unit, panel0, st);
+  }
+
+  void steps_rt(int s, int panel0, std::vector<TrsmStep>& st) {
+    if (T.cl_nsons[s] == 0) {
+      const int d = blk(s, s);
+      st.push_back(TrsmStep{0, T.cl_start[s] - panel0, T.cl_size[s], G->pA[d], T.cl_size[s], 1, 0, 0, 0});
+      return;
+    }
+    const int s1 = son0(s), s2 = s1 + 1;
+    steps_rt(s1, panel0, st);
+    const int b = blk(s1, s2);
+    st.push_back(TrsmStep{1, 0, 0, nullptr, 0, 1, 0, T.bl_lbeg[b], T.bl_lend[b]});
+    steps_rt(s2, panel0, st);
+  }
+
+  // mode 0: V <- L^{-1} V (unit), 1: V <- R^{-T} V, 2: V <- L^{-1} V (Cholesky factor)
+  void trsm(int mode, int t, double* V, int ldv, int ncols) {
+    if (ncols <= 0) return;
+    n_trsm++;
+    std::vector<TrsmStep> st;
+    if (mode == 1) steps_rt(t, T.cl_start[t], st);
+    else steps_lower(t, mode == 0, T.cl_start[t], st);
+    Arena ar(c);
+    std::vector<TrsmJob> jb{TrsmJob{V, ldv, ncols, T.cl_start[t], 0, (int)st.size()}};
+    launch_trsm(ar.upload(jb), 1, ar.upload(st), dlt, c->stream);
+    HM_CHECK_LAUNCH();
+  }
+
+  // panel solve on the rows of a dense leaf's transpose: N <- N op^{-1}
+  void trsm_right_dense(int mode, int s, int b) {
+    const int m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
+    Arena ar(c);
+    double* tmp = ar.alloc((size_t)m * n);
+    std::vector<CopyJob> cj{CopyJob{tmp, G->pA[b], n, m, n, m, 1, 0, 0, 1.0, 0}};
+    launch_copy(ar.upload(cj), 1, (int64_t)((n + 31) / 32) * ((m + 31) / 32), c->stream);
+    trsm(mode, s, tmp, n, m);
+    std::vector<CopyJob> cb{CopyJob{G->pA[b], tmp, m, n, m, n, 1, 0, 0, 1.0, 0}};
+    launch_copy(ar.upload(cb), 1, (int64_t)((m + 31) / 32) * ((n + 31) / 32), c->stream);
+    HM_CHECK_LAUNCH();
+  }
+
+  void leaf_factor(int t) {
+    n_leaf++;
+    const int d = blk(t, t);
+    const int m = T.cl_size[t];
+    Arena ar(c);
+    std::vector<LeafFactorJob> j{LeafFactorJob{G->pA[d], m, m, t}};
+    launch_leaf_factor(ar.upload(j), 1, chol ? 1 : 0, d_fail, d_minpiv + t, m, c->stream);
+    HM_CHECK_LAUNCH();
+  }
+
+  // ---- LR (O8)
+  void lr(int t, Node acc) {
+    if (T.cl_nsons[t] == 0) {
+      flush(acc);
+      leaf_factor(t);
+      return;
+    }
+    std::vector<Node> ch = split(acc, false);
+    const int t1 = son0(t), t2 = t1 + 1;
+    lr(t1, ch[0]);
+    solve_l(t1, blk(t1, t2), ch[1]);
+    solve_r(t1, blk(t2, t1), ch[2]);
+    P.addproduct(ch[3], blk(t2, t1), blk(t1, t2));
+    lr(t2, ch[3]);
+  }
+
+  void solve_l(int t, int b, Node acc) {
+    const int kind = T.bl_kind[b];
+    if (kind == HM_BLOCK_ADM) {
+      flush(acc);
+      trsm(0, t, G->pA[b], T.cl_size[T.bl_row[b]], G->rank[b]);
+    } else if (kind == HM_BLOCK_DENSE) {
+      flush(acc);
+      trsm(0, t, G->pA[b], T.cl_size[T.bl_row[b]], T.cl_size[T.bl_col[b]]);
+    } else {
+      std::vector<Node> ch = split(acc, false);
+      const int t1 = son0(t), t2 = t1 + 1;
+      for (int j = 0; j < T.cl_nsons[T.bl_col[b]]; j++) {
+        const int b1 = T.son(b, 0, j), b2 = T.son(b, 1, j);
+        solve_l(t1, b1, ch[j]);
+        P.addproduct(ch[2 + j], blk(t2, t1), b1);
+        solve_l(t2, b2, ch[2 + j]);
+      }
+    }
+  }
+
+  void solve_r(int s, int b, Node acc) {
+    const int kind = T.bl_kind[b];
+    if (kind == HM_BLOCK_ADM) {
+      flush(acc);
+      trsm(1, s, G->pB[b], T.cl_size[T.bl_col[b]], G->rank[b]);
+    } else if (kind == HM_BLOCK_DENSE) {
+      flush(acc);
+      trsm_right_dense(1, s, b);
+    } else {
+      std::vector<Node> ch = split(acc, false);
+      const int s1 = son0(s), s2 = s1 + 1;
+      for (int i = 0; i < T.cl_nsons[T.bl_row[b]]; i++) {
+        const int b1 = T.son(b, i, 0), b2 = T.son(b, i, 1);
+        solve_r(s1, b1, ch[2 * i]);
+        P.addproduct(ch[2 * i + 1], b1, blk(s1, s2));
+        solve_r(s2, b2, ch[2 * i + 1]);
+      }
+    }
+  }
+
+  // ---- Cholesky (O9)
+  void cholesky(int t, Node acc) {
+    if (T.cl_nsons[t] == 0) {
+      flush(acc);
+      leaf_factor(t);
+      return;
+    }
+    std::vector<Node> ch = split(acc, true);   // (t1,t1), [upper], (t2,t1), (t2,t2)
+    const int t1 = son0(t), t2 = t1 + 1;
+    cholesky(t1, ch[0]);
+    solve_lt(t1, blk(t2, t1), ch[2]);
+    P.addproduct(ch[3], blk(t2, t1), blk(t1, t2));   // Y = L^T view: (t1,t2) of L^T = (t2,t1) of L
+    cholesky(t2, ch[3]);
+  }
+
+  void solve_lt(int s, int b, Node acc) {
+    const int kind = T.bl_kind[b];
+    if (kind == HM_BLOCK_ADM) {
+      flush(acc);
+      trsm(2, s, G->pB[b], T.cl_size[T.bl_col[b]], G->rank[b]);
+    } else if (kind == HM_BLOCK_DENSE) {
+      flush(acc);
+      trsm_right_dense(2, s, b);
+    } else {
+      std::vector<Node> ch = split(acc, false);
+      const int s1 = son0(s), s2 = s1 + 1;
+      for (int i = 0; i < T.cl_nsons[T.bl_row[b]]; i++) {
+        const int b1 = T.son(b, i, 0), b2 = T.son(b, i, 1);
+        solve_lt(s1, b1, ch[2 * i]);
+        P.addproduct(ch[2 * i + 1], b1, blk(s1, s2));
+        solve_lt(s2, b2, ch[2 * i + 1]);
+      }
+    }
+  }
+
+  // compact G's admissible factors into one pool; check pivots
+  void finish(double* min_pivot_out) {
+    HM_CUDA(cudaStreamSynchronize(c->stream));
+    int fail = 0;
+    HM_CUDA(cudaMemcpy(&fail, d_fail, sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<double> mp(T.nclusters());
+    HM_CUDA(cudaMemcpy(mp.data(), d_minpiv, sizeof(double) * mp.size(), cudaMemcpyDeviceToHost));
+    double mn = 1e300;
+    for (int t = 0; t < T.nclusters(); t++)
+      if (T.cl_nsons[t] == 0) mn = std::min(mn, mp[t]);
+    if (min_pivot_out) *min_pivot_out = mn;
+    const int nb = T.nblocks();
+    size_t total = 0;
+    for (int b = 0; b < nb; b++)
+      if (T.bl_kind[b] == HM_BLOCK_ADM)
+        total += (size_t)(T.cl_size[T.bl_row[b]] + T.cl_size[T.bl_col[b]]) * G->rank[b];
+    double* pool = static_cast<double*>(c->dmalloc((total + 1) * sizeof(double)));
+    size_t off = 0;
+    for (int b = 0; b < nb; b++) {
+      if (T.bl_kind[b] != HM_BLOCK_ADM) continue;
+      const size_t m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]], k = G->rank[b];
+      if (k) {
+        HM_CUDA(cudaMemcpyAsync(pool + off, G->pA[b], sizeof(double) * m * k, cudaMemcpyDeviceToDevice, c->stream));
+        HM_CUDA(cudaMemcpyAsync(pool + off + m * k, G->pB[b], sizeof(double) * n * k, cudaMemcpyDeviceToDevice,
+                                c->stream));
+      }
+      G->pA[b] = pool + off;
+      G->pB[b] = pool + off + m * k;
+      off += (m + n) * k;
+    }
+    HM_CUDA(cudaStreamSynchronize(c->stream));
+    c->dfree(G->fpool.first, G->fpool.second);
+    G->fpool = {pool, (total + 1) * sizeof(double)};
+    for (auto& o : own)
+      if (o.first) c->dfree(o.first, o.second);
+    own.clear();
+    if (fail) {
+      const int t = fail - 1;
+      throw Error(HM_EPIVOT, "pivot breakdown in leaf cluster " + std::to_string(t) + " [" +
+                                 std::to_string(T.cl_start[t]) + ":" +
+                                 std::to_string(T.cl_start[t] + T.cl_size[t]) + "]");
+    }
+  }
+};
+
 }  // namespace
+
+void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_pivot) {
+  if (!G) throw Error(HM_EINVAL, "hm_lr/hm_chol: null matrix");
+  if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_lr/hm_chol: eps must be >= 0");
+  const Tree& T = *G->tree;
+  if (T.bl_kind[0] != HM_BLOCK_SUB && T.bl_kind[0] != HM_BLOCK_DENSE)
+    throw Error(HM_ESTRUCT, "hm_lr/hm_chol: the root block must not be admissible");
+  if (shift != 0.0) {
+    Arena ar(c);
+    std::vector<CopyJob> cj;
+    int64_t tiles = 0;
+    for (int b = 0; b < T.nblocks(); b++) {
+      if (T.bl_kind[b] != HM_BLOCK_DENSE || T.bl_row[b] != T.bl_col[b]) continue;
+      const int m = T.cl_size[T.bl_row[b]];
+      cj.push_back(CopyJob{G->pA[b], nullptr, m, 0, m, m, 0, 1, 1, shift, tiles});
+      tiles += (int64_t)((m + 31) / 32) * ((m + 31) / 32);
+    }
+    launch_copy(ar.upload(cj), (int)cj.size(), tiles, c->stream);
+    HM_CHECK_LAUNCH();
+  }
+  Factorizer F(c, G, eps, chol);
+  Node root = F.acc_for(0);
+  const int t = T.bl_row[0];
+  if (chol) F.cholesky(t, root);
+  else F.lr(t, root);
+  F.finish(min_pivot);
+  hm_stats_t& s = c->last;
+  s.addproduct_calls = F.P.n_addproduct;
+  s.evaluated_terms = F.P.n_eval;
+  s.truncations = F.P.n_trunc;
+  s.trunc_cols = F.P.n_cols;
+  s.merges = F.P.n_merge;
+  s.dense_adds = F.P.n_dense;
+  s.levels = F.n_flush;
+  s.flops_trunc = F.P.fl_trunc;
+  s.bytes_trunc = F.P.by_trunc;
+  s.flops_eval = F.P.fl_eval;
+  s.bytes_eval = F.P.by_eval;
+  s.flops_dense = F.P.fl_dense;
+  s.bytes_dense = F.P.by_dense;
+  F.P.persist.release();
+  HM_CUDA(cudaStreamSynchronize(c->stream));
+}
 
 void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps) {
   if (!X || !Y || !Z) throw Error(HM_EINVAL, "hm_addmul: null matrix");

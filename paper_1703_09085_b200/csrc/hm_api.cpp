@@ -317,20 +317,25 @@ hm_status hm_build(hm_ctx ctx, const double* pts_host, const double* area_host, 
 }
 
 hm_status hm_lr(hm_ctx ctx, hm_mat G, double eps) {
-  (void)G;
-  (void)eps;
-  if (!ctx) return HM_EINVAL;
-  ctx->c.err = "hm_lr: not available in this build (round 1: product path only)";
-  return HM_EUNSUPPORTED;
+  if (!ctx || !G) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    double mp = 0;
+    ctx->c.last = hm_stats_t{};
+    factorize(&ctx->c, &G->m, eps, false, 0.0, &mp);
+    ctx->c.last.min_pivot = mp;
+  });
 }
 
 hm_status hm_chol(hm_ctx ctx, hm_mat G, double eps, double shift) {
-  (void)G;
-  (void)eps;
-  (void)shift;
-  if (!ctx) return HM_EINVAL;
-  ctx->c.err = "hm_chol: not available in this build (round 1: product path only)";
-  return HM_EUNSUPPORTED;
+  if (!ctx || !G) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    double mp = 0;
+    ctx->c.last = hm_stats_t{};
+    factorize(&ctx->c, &G->m, eps, true, shift, &mp);
+    ctx->c.last.min_pivot = mp;
+  });
 }
 
 hm_status hm_matvec_thin(hm_ctx ctx, hm_mat G, int op, double alpha, const double* x_dev, int64_t ldx,

@@ -170,6 +170,7 @@ double trunc_flops(double m, double n, double l, double k);
 double trunc_bytes(double m, double n, double l, double k);
 
 void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps);
+void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_pivot);
 Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int kernel,
                   int leaf_size, double eta, double eps, int64_t* perm_out);
 void matvec(Ctx* c, Mat* G, int op, double alpha, const double* x, int64_t ldx, double beta,

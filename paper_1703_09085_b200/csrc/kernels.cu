@@ -322,13 +322,12 @@ __device__ void cta_gemm_acc(double* out, int ldo, int M, int N, int K, double c
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_eval(const EvalJob* __restrict__ jobs) {
-  __shared__ double sA[32 * 33];
-  __shared__ double sB[32 * 33];
-  __shared__ double sT[32 * 33];
-  const EvalJob J = jobs[blockIdx.x];
+// out += coef * op(H) V over the leaves [lb, le) of J's table (Fig. 1 addeval /
+// addevaltrans flattened over a DFS leaf range); one CTA, results accumulate in
+// place (each CTA owns its output panel).
+__device__ void eval_leaves(const EvalJob& J, int lb, int le, double* sA, double* sB, double* sT) {
   const int tid = threadIdx.x;
-  for (int li = J.leaf_begin; li < J.leaf_end; li++) {
+  for (int li = lb; li < le; li++) {
     const LeafDesc L = J.leaves[li];
     const int ro = L.row0 - J.t0, co = L.col0 - J.s0;   // offsets inside block (t,s)
     // non-trans: out rows ro.., V rows co.. ; trans: out rows co.., V rows ro..
@@ -381,6 +380,145 @@ __global__ void __launch_bounds__(256) k_eval(const EvalJob* __restrict__ jobs) 
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_eval(const EvalJob* __restrict__ jobs) {
+  __shared__ double sA[32 * 33];
+  __shared__ double sB[32 * 33];
+  __shared__ double sT[32 * 33];
+  const EvalJob J = jobs[blockIdx.x];
+  eval_leaves(J, J.leaf_begin, J.leaf_end, sA, sB, sT);
+}
+
+// ------------------------------------------------------------------ TRSM
+// Triangular solve through the H-structure on one thin panel per CTA: a host
+// prepared step list of (a) dense triangular solves on leaf clusters and (b)
+// addeval / addevaltrans updates over leaf ranges (alpha = -1), e.g.
+// TRSM_L(t, V): TRSM_L(t1, V1); V2 -= L_(t2,t1) V1; TRSM_L(t2, V2).
+__global__ void __launch_bounds__(256) k_trsm(const TrsmJob* __restrict__ jobs,
+                                              const TrsmStep* __restrict__ steps,
+                                              const LeafDesc* __restrict__ leaves) {
+  __shared__ double tri[64 * 65];   // solve steps; eval steps reuse it as 3 tiles
+  double* sA = tri;
+  double* sB = tri + 32 * 33;
+  double* sT = tri + 2 * 32 * 33;
+  const TrsmJob J = jobs[blockIdx.x];
+  const int tid = threadIdx.x;
+  for (int si = J.step0; si < J.step1; si++) {
+    const TrsmStep S = steps[si];
+    if (S.kind == 0) {
+      // V[r0:r0+m, :] <- T^{-1} V, T lower triangular: T(i,j) = trans ? P[j + i ld] : P[i + j ld]
+      const int m = S.m;
+      double* v = J.V + S.r0;
+      if (m <= 64) {
+        for (int e = tid; e < m * m; e += 256) {
+          const int i = e % m, j = e / m;
+          tri[i + j * 65] = S.trans ? S.P[j + (int64_t)i * S.ld] : S.P[i + (int64_t)j * S.ld];
+        }
+        __syncthreads();
+      }
+      for (int col = tid; col < J.ncols; col += 256) {
+        double* x = v + (int64_t)col * J.ldv;
+        for (int i = 0; i < m; i++) {
+          double s = x[i];
+          for (int p = 0; p < i; p++) {
+            const double tip = (m <= 64) ? tri[i + p * 65]
+                                         : (S.trans ? S.P[p + (int64_t)i * S.ld] : S.P[i + (int64_t)p * S.ld]);
+            s = fma(-tip, x[p], s);
+          }
+          if (!S.unit) {
+            const double d = (m <= 64) ? tri[i + i * 65] : S.P[i + (int64_t)i * S.ld];
+            s /= d;
+          }
+          x[i] = s;
+        }
+      }
+      __syncthreads();
+    } else {
+      EvalJob E{};
+      E.leaves = leaves;
+      E.trans = S.trans;
+      E.t0 = J.panel0;
+      E.s0 = J.panel0;
+      E.coef = -1.0;
+      E.out = J.V;
+      E.ldo = J.ldv;
+      E.w = J.ncols;
+      E.V = J.V;
+      E.ldv = J.ldv;
+      eval_leaves(E, S.lb, S.le, sA, sB, sT);
+      __syncthreads();
+    }
+  }
+}
+
+void launch_trsm(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, const LeafDesc* leaves,
+                 cudaStream_t st) {
+  if (njobs <= 0) return;
+  count_launch();
+  k_trsm<<<njobs, 256, 0, st>>>(d_jobs, d_steps, leaves);
+}
+
+// ------------------------------------------------------------------ dense leaf factorizations
+// In-place LU without pivoting (unit L) or Cholesky (lower) of one diagonal
+// leaf per CTA (m <= 128 in shared memory).  Pivot breakdown (|p| <= 1e-300,
+// non-finite, or a non-positive Cholesky pivot) sets *fail = cluster id + 1
+// (first failure wins); minpiv[job] = min |pivot|.
+__global__ void __launch_bounds__(256) k_leaf_factor(const LeafFactorJob* __restrict__ jobs, int chol,
+                                                     int* fail, double* minpiv) {
+  extern __shared__ double a[];
+  __shared__ double s_piv;
+  const LeafFactorJob J = jobs[blockIdx.x];
+  const int m = J.m, tid = threadIdx.x;
+  for (int e = tid; e < m * m; e += blockDim.x) a[e] = J.N[(e % m) + (int64_t)(e / m) * J.ld];
+  __syncthreads();
+  double mp = 1e300;
+  bool bad = false;
+  for (int j = 0; j < m; j++) {
+    if (tid == 0) {
+      double p = a[j + j * m];
+      if (chol) {
+        p = (p > 0.0 && isfinite(p)) ? sqrt(p) : -1.0;
+        if (p > 0.0) a[j + j * m] = p;
+      }
+      s_piv = p;
+    }
+    __syncthreads();
+    const double p = s_piv;
+    if (!isfinite(p) || fabs(p) <= 1e-300 || (chol && p <= 0.0)) { bad = true; break; }
+    mp = fmin(mp, fabs(p));
+    for (int i = j + 1 + tid; i < m; i += blockDim.x) a[i + j * m] /= p;
+    __syncthreads();
+    // trailing update: lower-right block (Cholesky: lower triangle only)
+    const int r = m - j - 1;
+    for (int e = tid; e < r * r; e += blockDim.x) {
+      const int i = j + 1 + e % r, c = j + 1 + e / r;
+      if (chol && c > i) continue;
+      a[i + c * m] -= a[i + j * m] * (chol ? a[c + j * m] : a[j + c * m]);
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) atomicCAS(fail, 0, J.cluster + 1);
+    return;
+  }
+  for (int e = tid; e < m * m; e += blockDim.x) {
+    const int i = e % m, c = e / m;
+    J.N[i + (int64_t)c * J.ld] = (chol && c > i) ? 0.0 : a[e];
+  }
+  if (tid == 0 && minpiv) minpiv[blockIdx.x] = mp;
+}
+
+void launch_leaf_factor(const LeafFactorJob* d_jobs, int njobs, int chol, int* fail, double* minpiv,
+                        int maxm, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  count_launch();
+  k_leaf_factor<<<njobs, 256, (size_t)maxm * maxm * 8, st>>>(d_jobs, chol, fail, minpiv);
 }
 
 void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st) {

@@ -98,6 +98,31 @@ struct EvalJob {
   int64_t cost;        // for scheduling (largest first)
 };
 
+// Triangular solve through the H-structure on a thin panel (one CTA per job).
+// kind 0: V[r0:r0+m] <- T^{-1} V[r0:r0+m], T lower: T(i,j) = trans ? P[j+i ld] : P[i+j ld],
+//         unit diagonal if unit;
+// kind 1: V -= op(H) V over the leaves [lb, le) (eval semantics, t0 = s0 = panel0).
+struct TrsmStep {
+  int kind;
+  int r0, m;
+  const double* P;
+  int ld, trans, unit;
+  int lb, le;
+};
+struct TrsmJob {
+  double* V;
+  int ldv, ncols;
+  int panel0;          // absolute start (tree order) of the panel's first row
+  int step0, step1;
+};
+
+// In-place dense LU (no pivoting, unit L) or Cholesky of a diagonal leaf.
+struct LeafFactorJob {
+  double* N;
+  int m, ld;
+  int cluster;
+};
+
 // Kernel-matrix generation: dst[i,j] = G(perm[r0+i], perm[c0+j]).
 struct GenJob {
   double* dst;
@@ -119,6 +144,10 @@ void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st);
+void launch_trsm(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, const LeafDesc* leaves,
+                 cudaStream_t st);
+void launch_leaf_factor(const LeafFactorJob* d_jobs, int njobs, int chol, int* fail, double* minpiv,
+                        int maxm, cudaStream_t st);
 void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x,
                 const double* w, const int64_t* perm, int kernel, cudaStream_t st);
 void launch_norm(const NormJob* d_jobs, int njobs, double* out, cudaStream_t st);
