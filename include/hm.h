@@ -118,7 +118,7 @@ typedef struct {
 
 /* Per-kernel-class device timing (CUDA events on the context stream,
  * summed over launches since hm_profile_reset). */
-#define HM_NPROF 16
+#define HM_NPROF 32
 typedef struct {
   char name[HM_NPROF][24];
   double ms[HM_NPROF];

@@ -48,7 +48,7 @@ class Stats(C.Structure):
     ]
 
 
-HM_NPROF = 16
+HM_NPROF = 32
 
 
 class Prof(C.Structure):

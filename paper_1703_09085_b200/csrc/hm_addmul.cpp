@@ -102,8 +102,21 @@ struct Planner {
     } else {
       return false;
     }
+    if (narrow) {
+      // Any branch whose leaf condition holds factorizes the SAME exact product
+      // alpha X|ts Y|sr; pick the narrowest (reading R7b): the
+      // truncated matrix is unchanged, only the stack width shrinks.
+      auto cand = [&](int br, int w) {
+        if (w < out.w) { out.br = br; out.w = w; }
+      };
+      if (kx == HM_BLOCK_DENSE) cand(csize(t) <= csize(s) ? 0 : 1, std::min(csize(t), csize(s)));
+      if (ky == HM_BLOCK_DENSE) cand(csize(r) <= csize(s) ? 2 : 3, std::min(csize(r), csize(s)));
+      if (kx == HM_BLOCK_ADM) cand(4, X->rank[bx]);
+      if (ky == HM_BLOCK_ADM) cand(5, Y->rank[yb(by)]);
+    }
     return true;
   }
+  bool narrow = true;
 
   void addproduct(Node& nd, int bx, int by) {
     n_addproduct++;

@@ -56,8 +56,11 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
   size_t tau_total = 0, m_total = 0;
   for (int i = 0; i < nj; i++) {
     const TruncReq& r = reqs[i];
-    qa[i] = r.l < r.m;
-    qb[i] = r.l < r.n;
+    // one-sided route (the paper's: QR of one factor, SVD of A R_B^*): QR the
+    // factor with more rows if the stack is thin there; the column-pivoted QR
+    // inside the SVD kernel orthogonalises the other side.
+    if (r.n >= r.m) { qa[i] = 0; qb[i] = r.l < r.n; }
+    else { qa[i] = r.l < r.m; qb[i] = 0; }
     p[i] = qa[i] ? r.l : r.m;
     q[i] = qb[i] ? r.l : r.n;
     if (qa[i]) tau_total += r.l;
@@ -91,7 +94,10 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
   }
   {
     ProfScope ps(c, PC_QR, fl_qr, 0);
-    if (!qr_small.empty()) launch_qr(ar.upload(qr_small), (int)qr_small.size(), 4 * 1024, st);
+    if (!qr_small.empty()) {
+      ProfScope pb(c, PC_QR_SMALL, 0, (double)qr_small.size());
+      launch_qr(ar.upload(qr_small), (int)qr_small.size(), 4 * 1024, st);
+    }
     // blocked (compact-WY) QR, bucketed by panel height so that small panels
     // get several CTAs per SM: cap = 16 * rows doubles of shared memory
     std::vector<QrJob> qb[4], qr_huge;
@@ -103,26 +109,40 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
         qb[b].push_back(j);
       }
     for (int b = 0; b < 4; b++)
-      if (!qb[b].empty()) launch_qr_blocked(ar.upload(qb[b]), (int)qb[b].size(), qcap[b], st);
+      if (!qb[b].empty()) {
+        ProfScope pb(c, PC_QR_B0 + b, 0, (double)qb[b].size());
+        launch_qr_blocked(ar.upload(qb[b]), (int)qb[b].size(), qcap[b], st);
+      }
     if (!qr_huge.empty()) launch_qr(ar.upload(qr_huge), (int)qr_huge.size(), 0, st);
     HM_CHECK_LAUNCH();
   }
-  // --- M = R_A R_B^T
+  // --- M = op(A) op(B)^T, stored in its TALL orientation Mt (L x c): Mt = M if
+  // p >= q, else Mt = M^T (then the SVD's "left" side is the B side).
   std::vector<GemmJob> gj;
   gj.reserve(nj);
   int64_t tiles = 0;
   double fl_m = 0;
+  std::vector<char> tallM(nj);
   for (int i = 0; i < nj; i++) {
     const TruncReq& r = reqs[i];
+    tallM[i] = p[i] >= q[i];
     if (p[i] == 0 || q[i] == 0) continue;
     GemmJob g{};
-    g.A = r.A; g.lda = r.m; g.transA = 0; g.maskA = qa[i];
-    g.B = r.B; g.ldb = r.n; g.transB = 1; g.maskB = qb[i];
-    g.C = Mp[i]; g.ldc = p[i];
-    g.m = p[i]; g.n = q[i]; g.k = r.l;
+    if (tallM[i]) {
+      g.A = r.A; g.lda = r.m; g.maskA = qa[i];
+      g.B = r.B; g.ldb = r.n; g.maskB = qb[i];
+      g.m = p[i]; g.n = q[i]; g.ldc = p[i];
+    } else {
+      g.A = r.B; g.lda = r.n; g.maskA = qb[i];
+      g.B = r.A; g.ldb = r.m; g.maskB = qa[i];
+      g.m = q[i]; g.n = p[i]; g.ldc = q[i];
+    }
+    g.transA = 0; g.transB = 1;
+    g.C = Mp[i];
+    g.k = r.l;
     g.alpha = 1.0; g.beta = 0.0;
     g.tile0 = tiles;
-    tiles += (int64_t)((p[i] + 63) / 64) * ((q[i] + 63) / 64);
+    tiles += (int64_t)((g.m + 63) / 64) * ((g.n + 63) / 64);
     fl_m += 2.0 * p[i] * q[i] * r.l;
     gj.push_back(g);
   }
@@ -131,24 +151,56 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
     launch_gemm(ar.upload(gj), (int)gj.size(), tiles, st);
     HM_CHECK_LAUNCH();
   }
-  // --- Jacobi SVD + rank rule + U_k / V_k S_k, bucketed by smem need
+  // --- SVD jobs; matrices too large for shared memory are first reduced by an
+  // unpivoted blocked QR (Mt = Q1 R1) and the SVD kernel works on R1 (c x c).
   std::vector<SvdJob> sj[4];
   int caps[4] = {3 * 1024, 8 * 1024, 26 * 1024, 0};
   double fl_svd = 0, fl_b[4] = {0, 0, 0, 0};
   const char* dump = std::getenv("HM_DUMP_JOBS");
   int* d_sw = dump ? static_cast<int*>(ar.alloc_bytes(sizeof(int) * (nj + 1))) : nullptr;
   std::vector<int> bucket_of(nj);
+  std::vector<char> preqr(nj, 0);
+  std::vector<double*> tauM(nj, nullptr);
+  std::vector<QrJob> pq[4];
+  const int pqcap[4] = {6 * 1024, 12 * 1024, 24 * 1024, 24 * 1024};
   for (int i = 0; i < nj; i++) {
     const TruncReq& r = reqs[i];
+    const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
+    const int64_t full = (int64_t)L * cc + 2 * (int64_t)cc * cc + 6 * (int64_t)cc;
+    if (full > caps[2] && L > cc && L <= 24 * 1024) {
+      preqr[i] = 1;
+      tauM[i] = ar.alloc(cc + 1);
+      const int b = L <= 384 ? 0 : (L <= 768 ? 1 : (L <= 1536 ? 2 : 3));
+      pq[b].push_back(QrJob{Mp[i], L, cc, L, tauM[i], nullptr});
+    }
+  }
+  {
+    ProfScope ps(c, PC_PREQR, 0, 0);
+    for (int b = 0; b < 4; b++)
+      if (!pq[b].empty()) launch_qr_blocked(ar.upload(pq[b]), (int)pq[b].size(), pqcap[b], st);
+    HM_CHECK_LAUNCH();
+  }
+  for (int i = 0; i < nj; i++) {
+    const TruncReq& r = reqs[i];
+    const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
     SvdJob s{};
     s.nsweep = d_sw ? d_sw + i : nullptr;
-    s.M = Mp[i]; s.p = p[i]; s.q = q[i]; s.ldm = std::max(p[i], 1);
-    s.Aout = r.Aout; s.lda = r.m; s.ma = r.m;
-    s.Bout = r.Bout; s.ldb = r.n; s.nb = r.n;
+    s.M = Mp[i];
+    s.ldm = std::max(L, 1);
+    s.p = preqr[i] ? cc : L;
+    s.q = cc;
+    s.maskM = preqr[i];
+    s.flip = tallM[i] ? 0 : 1;   // keep Fig. 2's convention: the A-side factor is orthonormal
+    // left (orthonormal U_k) / right (V_k S_k) outputs of the tall matrix
+    double* lo = tallM[i] ? r.Aout : r.Bout;
+    double* ro = tallM[i] ? r.Bout : r.Aout;
+    const int lrows = tallM[i] ? r.m : r.n, rrows = tallM[i] ? r.n : r.m;
+    s.Aout = lo; s.lda = lrows; s.ma = lrows;
+    s.Bout = ro; s.ldb = rrows; s.nb = rrows;
     s.rank = r.d_rank;
     s.sigma = r.d_sigma;
-    const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
-    const int64_t need = (int64_t)L * cc + 2 * (int64_t)cc * cc + 6 * (int64_t)cc;
+    const int Ls = s.p;
+    const int64_t need = (int64_t)Ls * cc + 2 * (int64_t)cc * cc + 6 * (int64_t)cc;
     const int cap = bucket_cap(need);
     fl_svd += 22.0 * (double)cc * cc * cc;
     int b = 3;
@@ -181,16 +233,23 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
       std::fclose(f);
     }
   }
-  // --- apply Q_A, Q_B
-  std::vector<ApplyQJob> aq;
+  // --- apply Q1 (pre-QR of Mt) to the left output, then the stack's Q_A / Q_B
+  std::vector<ApplyQJob> aq1, aq;
   for (int i = 0; i < nj; i++) {
     const TruncReq& r = reqs[i];
+    if (preqr[i]) {
+      const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
+      double* lo = tallM[i] ? r.Aout : r.Bout;
+      const int lrows = tallM[i] ? r.m : r.n;
+      aq1.push_back(ApplyQJob{Mp[i], tauM[i], L, cc, L, lo, lrows, 0, r.d_rank});
+    }
     if (qa[i]) aq.push_back(ApplyQJob{r.A, tauA[i], r.m, r.l, r.m, r.Aout, r.m, 0, r.d_rank});
     if (qb[i]) aq.push_back(ApplyQJob{r.B, tauB[i], r.n, r.l, r.n, r.Bout, r.n, 0, r.d_rank});
   }
   {
     ProfScope ps(c, PC_APPLYQ, 0, 0);
-    launch_applyq(ar.upload(aq), (int)aq.size(), st);
+    if (!aq1.empty()) launch_applyq(ar.upload(aq1), (int)aq1.size(), st);
+    if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), st);
     HM_CHECK_LAUNCH();
   }
 }

@@ -60,6 +60,8 @@ struct SvdJob {
   double* sigma;
   double* work;        // global work (L x c doubles) when it does not fit smem
   int* nsweep;         // optional: number of Jacobi sweeps used (diagnostics)
+  int maskM;           // M is upper triangular (entries below the diagonal read as 0)
+  int flip;            // put Sigma on the Aout side instead (Bout orthonormal)
 };
 
 // dst[0:rows, 0:cols] (+)= coef * op(src); identity: dst[d,d] = coef.

@@ -120,7 +120,8 @@ __global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
   int* order = perm + c;                        // c
   for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
     const int i = (int)(e % L), j = (int)(e / L);
-    C[e] = tr ? J.M[j + (int64_t)i * J.ldm] : J.M[i + (int64_t)j * J.ldm];
+    const int mi = tr ? j : i, mj = tr ? i : j;   // entry (mi, mj) of M
+    C[e] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
   }
   for (int j = tid; j < c; j += NT) perm[j] = j;
   __syncthreads();
@@ -215,34 +216,47 @@ __global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
   int sweep = 0;
   for (; sweep < 60 && rt > 1; sweep++) {
     int rot = 0;
+    // one group of G lanes per column pair (G = 8/16/32 by column length):
+    // shorter shuffle reductions and several pairs per warp in flight
+    const int G = c <= 64 ? 8 : (c <= 128 ? 16 : 32);
+    const int gl = lane & (G - 1), gpw = 32 / G;
     for (int r = 0; r < cp - 1; r++) {
-      for (int pr = warp; pr < (cp >> 1); pr += NW) {
-        const int a = rr_pos(pr, r, cp), b = rr_pos(cp - 1 - pr, r, cp);
-        if (a >= rt || b >= rt) continue;
+      for (int base = warp * gpw; base < (cp >> 1); base += NW * gpw) {
+        const int pr = base + lane / G;
+        int a = 0, b = 0;
+        bool act = pr < (cp >> 1);
+        if (act) {
+          a = rr_pos(pr, r, cp);
+          b = rr_pos(cp - 1 - pr, r, cp);
+          act = a < rt && b < rt;
+        }
         double* x = X + (int64_t)a * c;
         double* y = X + (int64_t)b * c;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < c; i += 32) {
-          const double xv = x[i], yv = y[i];
-          al = fma(xv, xv, al);
-          be = fma(yv, yv, be);
-          ga = fma(xv, yv, ga);
+        if (act)
+          for (int i = gl; i < c; i += G) {
+            const double xv = x[i], yv = y[i];
+            al = fma(xv, xv, al);
+            be = fma(yv, yv, be);
+            ga = fma(xv, yv, ga);
+          }
+        for (int o = G >> 1; o > 0; o >>= 1) {   // all 32 lanes shuffle (uniform control flow)
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        al = wsum(al);
-        be = wsum(be);
-        ga = wsum(ga);
-        if (fabs(ga) > tol * sqrt(al) * sqrt(be) && fmin(al, be) > delta2) {
+        if (act && fabs(ga) > tol * sqrt(al) * sqrt(be) && fmin(al, be) > delta2) {
           const double zeta = (be - al) / (2.0 * ga);
           const double tt = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
           const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
-          for (int i = lane; i < c; i += 32) {
+          for (int i = gl; i < c; i += G) {
             const double xv = x[i], yv = y[i];
             x[i] = cs * xv - sn * yv;
             y[i] = sn * xv + cs * yv;
           }
           double* u = V + (int64_t)a * rt;
           double* w = V + (int64_t)b * rt;
-          for (int i = lane; i < rt; i += 32) {
+          for (int i = gl; i < rt; i += G) {
             const double uv = u[i], wv = w[i];
             u[i] = cs * uv - sn * wv;
             w[i] = sn * uv + cs * wv;
@@ -308,12 +322,12 @@ __global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
   for (int64_t e = tid; e < (int64_t)c * k; e += NT) {
     const int r = (int)(e % c), i = (int)(e / c);
     const int j = order[i];
-    const double f = tr ? 1.0 / sig[j] : 1.0;
+    const double f = (tr != (J.flip != 0)) ? 1.0 / sig[j] : 1.0;
     Pout[perm[r] + (int64_t)i * Pld] = X[r + (int64_t)j * c] * f;
   }
   for (int i = warp; i < k; i += NW) {
     const int j = order[i];
-    const double g = tr ? sig[j] : 1.0;
+    const double g = (tr != (J.flip != 0)) ? sig[j] : 1.0;
     double* y = Qout + (int64_t)i * Qld;
     for (int r = lane; r < Qrows; r += 32) y[r] = (r < rt) ? V[r + (int64_t)j * rt] * g : 0.0;
     __syncwarp();
