@@ -77,7 +77,7 @@ struct Planner {
   Arena* fp_arena = nullptr;   // where new_fp allocates (default: persist)
 
   Planner(Ctx* c_, const Tree& T_, Mat* X_, Mat* Y_, Mat* Z_, double a, double e)
-      : c(c_), persist(c_), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {}
+      : c(c_), persist(c_, true), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {}
 
   int csize(int cl) const { return T.cl_size[cl]; }
   int cstart(int cl) const { return T.cl_start[cl]; }
@@ -298,7 +298,7 @@ struct Planner {
     if (stacks.empty()) return;
     size_t total = 0;
     for (auto& s : stacks) total += (size_t)(s.m + s.n) * s.l;
-    double* buf = scratch.alloc(total + 1);
+    double* buf = c->stack_ws(total + 1);
     {
       ProfScope ps(c, PC_MEMSET, 0, 8.0 * total);
       HM_CUDA(cudaMemsetAsync(buf, 0, total * sizeof(double), c->stream));
@@ -492,7 +492,7 @@ struct Planner {
           }
         }
         for (auto& s : pre) total += (size_t)(s.m + s.n) * s.l;
-        double* buf = scratch.alloc(total + 1);
+        double* buf = c->stack_ws(total + 1);
         HM_CUDA(cudaMemsetAsync(buf, 0, total * sizeof(double), c->stream));
         size_t off = 0;
         for (auto& s : pre) {
@@ -764,7 +764,7 @@ struct Factorizer {
   // Fig. 7 flush of an accumulator into the leaf nd.zb of G (branches i, ii, v).
   void flush(const Node& nd) {
     n_flush++;
-    Arena local(c);
+    Arena local(c, true);
     P.fp_arena = &local;
     const int zb = nd.zb;
     P.zresult[zb] = -1;
@@ -1032,6 +1032,7 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
     launch_copy(ar.upload(cj), (int)cj.size(), tiles, c->stream);
     HM_CHECK_LAUNCH();
   }
+  c->sp_prepare();
   Factorizer F(c, G, eps, chol);
   Node root = F.acc_for(0);
   const int t = T.bl_row[0];
@@ -1063,6 +1064,7 @@ void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps) {
   const Tree& T = *Z->tree;
   if (!(X->tree->same_structure(T) && Y->tree->same_structure(T)))
     throw Error(HM_ESTRUCT, "hm_addmul: X, Y and Z must share one block tree");
+  c->sp_prepare();
   Planner P(c, T, X, Y, Z, alpha, eps);
   P.run();
   hm_stats_t& s = c->last;

@@ -37,6 +37,24 @@ void* Ctx::pinned(size_t bytes) {
 
 Ctx::~Ctx() {
   if (pin) cudaFreeHost(pin);
+  if (ws) cudaFree(ws);
+  if (sp) cudaFree(sp);
+}
+
+double* Ctx::stack_ws(size_t ndoubles) {
+  if (ndoubles > ws_cap) {
+    if (ws) cudaFreeAsync(ws, stream);
+    ws = nullptr;
+    const size_t cap = std::max(ndoubles + ndoubles / 8, (size_t)1 << 24);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), cap * sizeof(double), stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ws_cap = 0;
+      throw Error(HM_ENOMEM, "stack workspace (" + std::to_string(cap * 8) + " B): " + cudaGetErrorString(e));
+    }
+    ws_cap = cap;
+  }
+  return ws;
 }
 
 void* Ctx::dmalloc(size_t bytes) {
@@ -105,8 +123,34 @@ void Ctx::prof_collect() {
   pend.clear();
 }
 
+void Ctx::sp_prepare() {
+  if (sp_hwm > sp_cap) {
+    if (sp) cudaFreeAsync(sp, stream);
+    sp = nullptr;
+    sp_cap = 0;
+    const size_t cap = sp_hwm + sp_hwm / 8;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&sp), cap, stream) == cudaSuccess) sp_cap = cap;
+    else cudaGetLastError();
+  }
+  sp_top = 0;
+  sp_hwm = 0;
+}
+
 void* Arena::alloc_bytes(size_t bytes) {
   bytes = (bytes + 255) & ~size_t(255);
+  if (stack_mode) {
+    const size_t need = ctx->sp_top + bytes;
+    ctx->sp_hwm = std::max(ctx->sp_hwm, need);
+    if (need <= ctx->sp_cap) {
+      void* p = ctx->sp + ctx->sp_top;
+      ctx->sp_top = need;
+      return p;
+    }
+    ctx->sp_top = need;   // account the overflow so the next operation sizes the pool
+    void* p = ctx->dmalloc(bytes);
+    blocks.push_back({p, bytes});
+    return p;
+  }
   if (bytes > cur_left) {
     if (bytes >= chunk_min) {   // large request: its own block, keep the current chunk
       void* p = ctx->dmalloc(bytes);
@@ -130,6 +174,7 @@ void Arena::release() {
   blocks.clear();
   cur = nullptr;
   cur_left = 0;
+  if (stack_mode && ctx->sp_top > mark) ctx->sp_top = mark;
 }
 
 void Mat::free_all(Ctx* c) {

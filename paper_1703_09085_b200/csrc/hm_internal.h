@@ -40,7 +40,7 @@ bool debug_sync();   // HM_DEBUG_SYNC=1: synchronize and check after every launc
 
 enum ProfClass {
   PC_QR = 0, PC_GEMM_M, PC_SVD, PC_APPLYQ, PC_COPY, PC_EVAL, PC_DENSE, PC_MEMSET,
-  PC_GEN, PC_BUILD_GEMM, PC_NORM, PC_MATVEC, PC_SVD_B0, PC_SVD_B1, PC_SVD_B2, PC_SVD_B3, PC_QR_SMALL, PC_QR_B0, PC_QR_B1, PC_QR_B2, PC_QR_B3, PC_PREQR, PC_TRSM, PC_LEAF, PC_COUNT
+  PC_GEN, PC_BUILD_GEMM, PC_NORM, PC_MATVEC, PC_SVD_B0, PC_SVD_B1, PC_SVD_B2, PC_SVD_B3, PC_QR_SMALL, PC_QR_B0, PC_QR_B1, PC_QR_B2, PC_QR_B3, PC_PREQR, PC_TRSM, PC_LEAF, PC_FUSED, PC_COUNT
 };
 
 struct Ctx {
@@ -66,6 +66,17 @@ struct Ctx {
   size_t pin_cap = 0, pin_used = 0;
   void* pinned(size_t bytes);
   void pinned_reset() { pin_used = 0; }
+  // grow-only device workspace for the per-level stacks (one user at a time,
+  // stream ordered): avoids re-mapping tens of GB every level
+  double* ws = nullptr;
+  size_t ws_cap = 0;
+  double* stack_ws(size_t ndoubles);
+  // grow-only LIFO pool for arenas in stack mode (factor outputs of one
+  // operation); overflow falls back to cudaMallocAsync chunks and the pool is
+  // resized to the high-water mark at the next operation start
+  char* sp = nullptr;
+  size_t sp_cap = 0, sp_top = 0, sp_hwm = 0;
+  void sp_prepare();   // call when no stack-mode arena is live
   ~Ctx();
 
   void* dmalloc(size_t bytes);
@@ -84,7 +95,9 @@ struct Arena {
   char* cur = nullptr;
   size_t cur_left = 0;
   size_t chunk_min = (size_t)64 << 20;
-  explicit Arena(Ctx* c) : ctx(c) {}
+  bool stack_mode = false;   // bump-allocate from ctx->sp (LIFO), release to mark
+  size_t mark = 0;
+  explicit Arena(Ctx* c, bool stack = false) : ctx(c), stack_mode(stack), mark(stack ? c->sp_top : 0) {}
   ~Arena() { release(); }
   void* alloc_bytes(size_t bytes);
   double* alloc(size_t ndoubles) { return static_cast<double*>(alloc_bytes(ndoubles * sizeof(double))); }

@@ -47,7 +47,33 @@ int bucket_cap(int64_t need) {
 }
 }  // namespace
 
+static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double eps);
+
+// Stacks whose whole working set fits in shared memory go to the fused
+// single-kernel TRUNC (k_trunc_small); the others to the staged pipeline.
 void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double eps) {
+  if (reqs.empty()) return;
+  std::vector<TruncSmallJob> fb[3];
+  const int fcap[3] = {4 * 1024, 10 * 1024, 26 * 1024};
+  std::vector<TruncReq> rest;
+  for (const TruncReq& r : reqs) {
+    const int need = trunc_small_need(r.m, r.n, r.l);
+    int b = -1;
+    for (int k = 0; k < 3; k++)
+      if (need <= fcap[k]) { b = k; break; }
+    if (b < 0 || std::getenv("HM_NO_FUSED")) { rest.push_back(r); continue; }
+    fb[b].push_back(TruncSmallJob{r.A, r.B, r.m, r.n, r.l, r.Aout, r.Bout, r.d_rank, r.d_sigma});
+  }
+  {
+    ProfScope ps(c, PC_FUSED, 0, 0);
+    for (int b = 0; b < 3; b++)
+      if (!fb[b].empty()) launch_trunc_small(ar.upload(fb[b]), (int)fb[b].size(), eps, fcap[b], c->stream);
+    HM_CHECK_LAUNCH();
+  }
+  trunc_general(c, ar, rest, eps);
+}
+
+static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double eps) {
   if (reqs.empty()) return;
   cudaStream_t st = c->stream;
   const int nj = (int)reqs.size();

@@ -64,6 +64,19 @@ struct SvdJob {
   int flip;            // put Sigma on the Aout side instead (Bout orthonormal)
 };
 
+// Fused TRUNC_eps of a small stack (everything in shared memory).
+struct TruncSmallJob {
+  const double* A;     // m x l (ld m)
+  const double* B;     // n x l (ld n)
+  int m, n, l;
+  double* Aout;        // m x k (ld m), orthonormal
+  double* Bout;        // n x k (ld n)
+  int* rank;
+  double* sigma;
+};
+int trunc_small_need(int m, int n, int l);   // doubles of shared memory
+void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
+
 // dst[0:rows, 0:cols] (+)= coef * op(src); identity: dst[d,d] = coef.
 struct CopyJob {
   double* dst;

@@ -92,37 +92,18 @@ int svd_smem_need(int p, int q) {
   return (int)(L * c + 2 * c * c + 6 * c);
 }
 
-__global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
-  extern __shared__ double sm[];
+// SVD + rank rule + factor output of the matrix already loaded in C (L x c,
+// the tall orientation of M; tr: C = M^T).  Workspace: X (c x c), V (c x c),
+// tau, nrm, sig (c each), perm, order (c ints each).  Outputs per J.
+__device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, double* C, double* X,
+                         double* V, double* tau, double* nrm, double* sig, int* perm, int* order) {
   __shared__ double red[32], redv[32], reds[32];
   __shared__ int redi[32];
   __shared__ int s_rank;
   __shared__ double s_tau, s_scale;
-  const SvdJob J = jobs[blockIdx.x];
-  const int p = J.p, q = J.q;
-  const bool tr = p < q;
-  const int L = tr ? q : p, c = tr ? p : q;
+  const int p = tr ? c : L, q = tr ? L : c;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = blockDim.x, NW = NT >> 5;
-  if (c == 0) {
-    if (tid == 0) *J.rank = 0;
-    if (J.nsweep && tid == 0) *J.nsweep = 0;
-    return;
-  }
-  const int64_t need = (int64_t)L * c + 2 * (int64_t)c * c + 6 * (int64_t)c;
-  double* C = (need <= cap) ? sm : J.work;      // L x c, QRCP in place
-  double* X = C + (int64_t)L * c;               // c x rt   (R^T, then W = X V)
-  double* V = X + (int64_t)c * c;               // rt x rt  (rotations)
-  double* tau = V + (int64_t)c * c;             // c
-  double* nrm = tau + c;                        // c
-  double* sig = nrm + c;                        // c
-  int* perm = reinterpret_cast<int*>(sig + c);  // c
-  int* order = perm + c;                        // c
-  for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
-    const int i = (int)(e % L), j = (int)(e / L);
-    const int mi = tr ? j : i, mj = tr ? i : j;   // entry (mi, mj) of M
-    C[e] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
-  }
   for (int j = tid; j < c; j += NT) perm[j] = j;
   __syncthreads();
   for (int j = warp; j < c; j += NW) {
@@ -343,6 +324,178 @@ __global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
       __syncwarp();
     }
   }
+}
+
+__global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
+  extern __shared__ double sm[];
+  const SvdJob J = jobs[blockIdx.x];
+  const int p = J.p, q = J.q;
+  const bool tr = p < q;
+  const int L = tr ? q : p, c = tr ? p : q;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  if (c == 0) {
+    if (tid == 0) *J.rank = 0;
+    if (J.nsweep && tid == 0) *J.nsweep = 0;
+    return;
+  }
+  const int64_t need = (int64_t)L * c + 2 * (int64_t)c * c + 6 * (int64_t)c;
+  double* C = (need <= cap) ? sm : J.work;      // L x c, QRCP in place
+  double* X = C + (int64_t)L * c;               // c x rt   (R^T, then W = X V)
+  double* V = X + (int64_t)c * c;               // rt x rt  (rotations)
+  double* tau = V + (int64_t)c * c;             // c
+  double* nrm = tau + c;                        // c
+  double* sig = nrm + c;                        // c
+  int* perm = reinterpret_cast<int*>(sig + c);  // c
+  int* order = perm + c;                        // c
+  for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
+    const int i = (int)(e % L), j = (int)(e / L);
+    const int mi = tr ? j : i, mj = tr ? i : j;   // entry (mi, mj) of M
+    C[e] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
+  }
+  svd_core(J, eps, tr, L, c, C, X, V, tau, nrm, sig, perm, order);
+}
+
+// In-place Householder QR (dgeqr2) of a rows x cols panel in shared memory.
+__device__ void house_qr_smem(double* A, int rows, int cols, double* tau) {
+  __shared__ double red[32];
+  __shared__ double s_tau, s_scale;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
+  for (int j = 0; j < cols && j < rows; j++) {
+    double* x = A + (int64_t)j * rows;
+    double pp = 0.0;
+    for (int i = j + 1 + tid; i < rows; i += NT) pp = fma(x[i], x[i], pp);
+    const double xn2 = bsum(pp, red);
+    if (tid == 0) {
+      const double alpha = x[j];
+      double t = 0.0, sc = 0.0, beta = alpha;
+      if (xn2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        t = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+      x[j] = beta;
+      tau[j] = t;
+      s_tau = t;
+      s_scale = sc;
+    }
+    __syncthreads();
+    const double t = s_tau, sc = s_scale;
+    if (t != 0.0) {
+      for (int i = j + 1 + tid; i < rows; i += NT) x[i] *= sc;
+      __syncthreads();
+      for (int c2 = j + 1 + warp; c2 < cols; c2 += NW) {
+        double* y = A + (int64_t)c2 * rows;
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < rows; i += 32) d = fma(x[i], y[i], d);
+        d = (wsum(d) + y[j]) * t;
+        if (lane == 0) y[j] -= d;
+        for (int i = j + 1 + lane; i < rows; i += 32) y[i] -= d * x[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// X (rows x k, ld ldx, global) <- H_0 ... H_{r-1} X, reflectors in shared memory.
+__device__ void apply_q_smem(const double* Vr, const double* tau, int rows, int r, double* X, int ldx, int k) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  for (int col = warp; col < k; col += NW) {
+    double* x = X + (int64_t)col * ldx;
+    for (int j = r - 1; j >= 0; j--) {
+      const double t = tau[j];
+      if (t == 0.0) continue;
+      const double* v = Vr + (int64_t)j * rows;
+      double d = 0.0;
+      for (int i = j + 1 + lane; i < rows; i += 32) d = fma(v[i], x[i], d);
+      d = (wsum(d) + x[j]) * t;
+      if (lane == 0) x[j] -= d;
+      for (int i = j + 1 + lane; i < rows; i += 32) x[i] -= d * v[i];
+      __syncwarp();
+    }
+  }
+}
+
+int trunc_small_need(int m, int n, int l) {
+  int qa = 0, qb = 0;
+  if (n >= m) qb = l < n; else qa = l < m;
+  const int p = qa ? l : m, q = qb ? l : n;
+  const int64_t L = p > q ? p : q, c = p < q ? p : q;
+  const int64_t need = (int64_t)(m + n) * l + 2 * (int64_t)l + L * c + 2 * c * c + 6 * c;
+  return need > (1 << 30) ? (1 << 30) : (int)need;
+}
+
+// Fused TRUNC_eps of one small stack per CTA, everything in shared memory:
+// one-sided Householder QR, M = op(A) op(B)^T in its tall orientation, the
+// QRCP + Jacobi SVD of svd_core, then Q of the stack applied to the output.
+__global__ void k_trunc_small(const TruncSmallJob* __restrict__ jobs, double eps) {
+  extern __shared__ double sm[];
+  const TruncSmallJob J = jobs[blockIdx.x];
+  const int m = J.m, n = J.n, l = J.l, tid = threadIdx.x, NT = blockDim.x;
+  int qa = 0, qb = 0;
+  if (n >= m) qb = l < n; else qa = l < m;
+  const int p = qa ? l : m, q = qb ? l : n;
+  const bool tall = p >= q;
+  const int L = tall ? p : q, c = tall ? q : p;
+  if (c == 0 || l == 0) {
+    if (tid == 0) *J.rank = 0;
+    return;
+  }
+  double* sA = sm;
+  double* sB = sA + (int64_t)m * l;
+  double* tA = sB + (int64_t)n * l;
+  double* tB = tA + l;
+  double* C = tB + l;
+  double* X = C + (int64_t)L * c;
+  double* V = X + (int64_t)c * c;
+  double* tau = V + (int64_t)c * c;
+  double* nrm = tau + c;
+  double* sig = nrm + c;
+  int* perm = reinterpret_cast<int*>(sig + c);
+  int* order = perm + c;
+  for (int64_t e = tid; e < (int64_t)m * l; e += NT) sA[e] = J.A[e];
+  for (int64_t e = tid; e < (int64_t)n * l; e += NT) sB[e] = J.B[e];
+  __syncthreads();
+  if (qa) house_qr_smem(sA, m, l, tA);
+  if (qb) house_qr_smem(sB, n, l, tB);
+  // Mt = op(A) op(B)^T (tall) or op(B) op(A)^T
+  for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
+    const int i = (int)(e % L), j = (int)(e / L);
+    const int ia = tall ? i : j, ib = tall ? j : i;   // row of op(A), row of op(B)
+    double s = 0.0;
+    for (int k = 0; k < l; k++) {
+      const double a = (qa && ia > k) ? 0.0 : sA[ia + (int64_t)k * m];
+      const double b = (qb && ib > k) ? 0.0 : sB[ib + (int64_t)k * n];
+      s = fma(a, b, s);
+    }
+    C[e] = s;
+  }
+  __syncthreads();
+  SvdJob S{};
+  S.rank = J.rank;
+  S.sigma = J.sigma;
+  S.flip = tall ? 0 : 1;
+  S.Aout = tall ? J.Aout : J.Bout;
+  S.lda = tall ? m : n;
+  S.ma = S.lda;
+  S.Bout = tall ? J.Bout : J.Aout;
+  S.ldb = tall ? n : m;
+  S.nb = S.ldb;
+  svd_core(S, eps, false, L, c, C, X, V, tau, nrm, sig, perm, order);
+  __syncthreads();
+  const int k = *J.rank;
+  if (qa) apply_q_smem(sA, tA, m, l, J.Aout, m, k);
+  if (qb) apply_q_smem(sB, tB, n, l, J.Bout, n, k);
+}
+
+void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_trunc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 26 * 1024 * 8);
+    attr = true;
+  }
+  count_launch();
+  k_trunc_small<<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, eps);
 }
 
 int svd_smem_capacity() { return 26 * 1024; }
