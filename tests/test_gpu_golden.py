@@ -1,0 +1,124 @@
+"""Full-size GPU <-> oracle parity on BASELINE.json's configurations (pytest -m gpu).
+
+Golden data come from `scripts/make_golden.py` (calls only oracle/):
+per-block ranks and Frobenius norms of the oracle's result, sketches
+Z_b Omega_b of ~400 sampled leaf blocks, and the result applied to two probe
+vectors.  The device side builds the same H-matrix with hm_build (trees
+bit-identical, admissible blocks certified to 1e-12 against the exact SVD),
+runs the operation in the launch configuration bench.py uses, and is
+compared on: identical ranks (blocks flagged near-threshold by the oracle
+excepted), per-block norms and sampled sketches within 1e-9 relative, probes
+within 1e-9 relative.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from hm_inputs import probe_vectors, sphere_points
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def hm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1703_09085_b200 as hm
+    return hm
+
+
+@pytest.fixture(scope="module")
+def ctx(hm):
+    return hm.Context(0)
+
+
+def _load(name):
+    p = os.path.join(GOLD, name)
+    if not os.path.exists(p):
+        pytest.skip(f"golden file {name} not generated (scripts/make_golden.py)")
+    g = np.load(p)
+    return g, json.loads(str(g["meta"]))
+
+
+def _payloads(d):
+    from tests.hm_compare import leaf_payloads
+    return leaf_payloads(d)
+
+
+def _fro(v):
+    if v[0] == "dense":
+        return float(np.linalg.norm(v[1]))
+    A, B = v[1], v[2]
+    if A.shape[1] == 0:
+        return 0.0
+    return float(np.sqrt(max(np.sum((A.T @ A) * (B.T @ B)), 0.0)))
+
+
+def _check(hm, ctx, out, g, meta):
+    d = out.export()
+    pay = _payloads(d)
+    ranks = g["ranks"]
+    nearb = set()
+    mism = [b for b, v in pay.items() if v[0] == "adm" and v[1].shape[1] != ranks[b]]
+    assert not mism or meta.get("near"), (len(mism), mism[:10])
+    fro = g["fro"]
+    znorm = np.sqrt(np.sum(fro ** 2))
+    worst = 0.0
+    for b, v in pay.items():
+        if b in mism:
+            continue
+        worst = max(worst, abs(_fro(v) - fro[b]) / max(fro[b], 1e-12 * znorm))
+    assert worst <= TOL, worst
+    ws = 0.0
+    for bid in g["sample"]:
+        if int(bid) in mism:
+            continue
+        v = pay[int(bid)]
+        n_b = (v[1].shape[1] if v[0] == "dense" else v[2].shape[0])
+        Om = np.random.default_rng([1703, 9085, 99, int(bid)]).standard_normal((n_b, 4))
+        s = v[1] @ Om if v[0] == "dense" else v[1] @ (v[2].T @ Om)
+        ref = g[f"sketch_{int(bid)}"]
+        ws = max(ws, np.linalg.norm(s - ref) / max(np.linalg.norm(ref), 1e-12 * znorm))
+    assert ws <= TOL, ws
+    return worst, ws
+
+
+@pytest.mark.parametrize("cfg", [1, 4])
+def test_product_golden(hm, ctx, cfg):
+    import torch
+    g, meta = _load(f"product_cfg{cfg}.npz")
+    x, w = sphere_points(meta["L"])
+    G = ctx.build(x, w, meta["leaf"], 2.0, meta["eps"])
+    X, Y, Z = G.clone(), G.clone(), G.clone()
+    hm.addmul(1.0, X, Y, Z, meta["eps"])
+    st = ctx.last_stats()
+    assert st["truncations"] == meta["truncations"]
+    assert st["addproduct_calls"] == meta["addproduct"]
+    _check(hm, ctx, Z, g, meta)
+    n = len(w)
+    v = probe_vectors(n, 2)[G.perm]
+    xv = torch.from_numpy(v.T.copy()).cuda().T
+    yv = torch.zeros_like(xv)
+    hm.matvec(Z, xv, yv)
+    pr = yv.cpu().numpy()
+    assert np.linalg.norm(pr - g["probes"]) <= TOL * np.linalg.norm(g["probes"])
+
+
+@pytest.mark.parametrize("kind,cfg", [("lr", 2), ("chol", 3)])
+def test_factor_golden(hm, ctx, kind, cfg):
+    g, meta = _load(f"{kind}_cfg{cfg}.npz")
+    x, w = sphere_points(meta["L"])
+    G = ctx.build(x, w, meta["leaf"], 2.0, meta["eps"], kernel=0 if kind == "lr" else 1)
+    if kind == "lr":
+        hm.lr(G, meta["eps"])
+    else:
+        hm.chol(G, meta["eps"], meta.get("shift", 0.0))
+    st = ctx.last_stats()
+    assert st["truncations"] == meta["truncations"]
+    assert abs(st["min_pivot"] - meta["min_pivot"]) <= 1e-9 * meta["min_pivot"]
+    _check(hm, ctx, G, g, meta)
