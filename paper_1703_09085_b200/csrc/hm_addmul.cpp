@@ -761,16 +761,23 @@ struct Factorizer {
     return nd;
   }
 
-  // Fig. 7 flush of an accumulator into the leaf nd.zb of G (branches i, ii, v).
-  void flush(const Node& nd) {
-    n_flush++;
+  // Fig. 7 flush of accumulators into distinct leaves nd.zb of G (branches i,
+  // ii, v) -- all of them in ONE level-synchronous batch.
+  void flush(const Node& nd) { flush_many(std::vector<Node>{nd}); }
+
+  void flush_many(std::vector<Node> roots) {
+    if (roots.empty()) return;
+    n_flush += (int64_t)roots.size();
     Arena local(c, true);
     P.fp_arena = &local;
-    const int zb = nd.zb;
-    P.zresult[zb] = -1;
-    std::vector<Node> roots{nd};
+    std::vector<int> zbs;
+    for (auto& nd : roots) {
+      P.zresult[nd.zb] = -1;
+      zbs.push_back(nd.zb);
+    }
     P.run_from(std::move(roots));
-    if (T.bl_kind[zb] == HM_BLOCK_ADM) {
+    for (int zb : zbs) {
+      if (T.bl_kind[zb] != HM_BLOCK_ADM) continue;
       const int f = P.zresult[zb];
       if (f < 0) throw Error(HM_ESTRUCT, "internal: flush produced no result");
       const FP& fp = P.fps[f];
@@ -795,14 +802,25 @@ struct Factorizer {
 
   // T1 reduce of an accumulator that is split (Fig. 6); result persists.
   void reduce(Node& nd) {
-    if (nd.terms.empty()) {
-      nd.red = nd.base;
-      return;
+    std::vector<Node*> v{&nd};
+    reduce_many(v);
+  }
+
+  void reduce_many(std::vector<Node*>& nds) {
+    std::vector<Node> batch;
+    std::vector<Node*> who;
+    for (Node* nd : nds) {
+      if (nd->terms.empty()) {
+        nd->red = nd->base;
+        continue;
+      }
+      batch.push_back(*nd);
+      batch.back().force_split = true;
+      who.push_back(nd);
     }
-    std::vector<Node> one{nd};
-    one[0].force_split = true;
-    P.run_level(one);
-    nd.red = one[0].red;
+    if (batch.empty()) return;
+    P.run_level(batch);
+    for (size_t i = 0; i < who.size(); i++) who[i]->red = batch[i].red;
   }
 
   std::vector<Node> split(Node& nd, bool lower_only) {
@@ -875,6 +893,107 @@ struct Factorizer {
     HM_CHECK_LAUNCH();
   }
 
+  // ---- batched solves: every target of one set shares the cluster t (row
+  // cluster of SOLVE_L targets, column cluster of SOLVE_R / SOLVE_LT
+  // targets), so the recursions over sons(t) run in lock step and each step
+  // is ONE batch of flushes / reduces / triangular solves.  Each accumulator
+  // still receives exactly the addproducts of the serial recursion before it
+  // is split or flushed (same truncation inputs as oracle/factor.py).
+  struct Item { int b; Node acc; };
+
+  void trsm_set(int t, const std::vector<std::pair<int, int>>& targets) {   // (block, mode)
+    if (targets.empty()) return;
+    Arena ar(c);
+    std::vector<TrsmStep> st;
+    int rng[3][2] = {{-1, -1}, {-1, -1}, {-1, -1}};
+    for (auto& tg : targets) {
+      const int mode = tg.second;
+      if (rng[mode][0] >= 0) continue;
+      rng[mode][0] = (int)st.size();
+      if (mode == 1) steps_rt(t, T.cl_start[t], st);
+      else steps_lower(t, mode == 0, T.cl_start[t], st);
+      rng[mode][1] = (int)st.size();
+    }
+    std::vector<TrsmJob> jobs;
+    std::vector<CopyJob> pre, post;
+    int64_t pt = 0, qt = 0;
+    for (auto& tg : targets) {
+      const int b = tg.first, mode = tg.second;
+      const int m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
+      if (T.bl_kind[b] == HM_BLOCK_ADM) {
+        if (G->rank[b] <= 0) continue;
+        if (mode == 0) jobs.push_back(TrsmJob{G->pA[b], m, G->rank[b], T.cl_start[t], rng[0][0], rng[0][1]});
+        else jobs.push_back(TrsmJob{G->pB[b], n, G->rank[b], T.cl_start[t], rng[mode][0], rng[mode][1]});
+      } else if (mode == 0) {
+        jobs.push_back(TrsmJob{G->pA[b], m, n, T.cl_start[t], rng[0][0], rng[0][1]});
+      } else {
+        // N <- N op^{-1}: solve on the transpose panel (n x m) and copy back
+        double* tmp = ar.alloc((size_t)m * n);
+        pre.push_back(CopyJob{tmp, G->pA[b], n, m, n, m, 1, 0, 0, 1.0, pt});
+        pt += (int64_t)((n + 31) / 32) * ((m + 31) / 32);
+        post.push_back(CopyJob{G->pA[b], tmp, m, n, m, n, 1, 0, 0, 1.0, qt});
+        qt += (int64_t)((m + 31) / 32) * ((n + 31) / 32);
+        jobs.push_back(TrsmJob{tmp, n, m, T.cl_start[t], rng[mode][0], rng[mode][1]});
+      }
+    }
+    n_trsm += (int64_t)jobs.size();
+    ProfScope ps(c, PC_TRSM, 0, 0);
+    if (!pre.empty()) launch_copy(ar.upload(pre), (int)pre.size(), pt, c->stream);
+    if (!jobs.empty()) launch_trsm(ar.upload(jobs), (int)jobs.size(), ar.upload(st), dlt, c->stream);
+    if (!post.empty()) launch_copy(ar.upload(post), (int)post.size(), qt, c->stream);
+    HM_CHECK_LAUNCH();
+  }
+
+  // L: SOLVE_L targets (t, r); R: SOLVE_R targets (t', t) (mode 1) or, for
+  // Cholesky, SOLVE_LT targets (mode 2).
+  void solve_set(int t, std::vector<Item> L, std::vector<Item> R) {
+    const int rmode = chol ? 2 : 1;
+    std::vector<Node> leaf_accs;
+    std::vector<std::pair<int, int>> leaf_targets;
+    std::vector<Item*> subL, subR;
+    for (auto& it : L) {
+      if (T.bl_kind[it.b] == HM_BLOCK_SUB) subL.push_back(&it);
+      else { leaf_accs.push_back(it.acc); leaf_targets.push_back({it.b, 0}); }
+    }
+    for (auto& it : R) {
+      if (T.bl_kind[it.b] == HM_BLOCK_SUB) subR.push_back(&it);
+      else { leaf_accs.push_back(it.acc); leaf_targets.push_back({it.b, rmode}); }
+    }
+    flush_many(std::move(leaf_accs));
+    trsm_set(t, leaf_targets);
+    if (subL.empty() && subR.empty()) return;
+    std::vector<Node*> red;
+    for (auto* it : subL) red.push_back(&it->acc);
+    for (auto* it : subR) red.push_back(&it->acc);
+    reduce_many(red);
+    const int t1 = son0(t), t2 = t1 + 1;
+    std::vector<Item> L1, L2, R1, R2;
+    for (auto* it : subL) {            // b = (t, r): sons (t_i, r_j), row-major
+      std::vector<Node> ch;
+      P.expand(it->acc, false, ch);
+      const int nr = T.cl_nsons[T.bl_col[it->b]];
+      for (int j = 0; j < nr; j++) {
+        L1.push_back(Item{T.son(it->b, 0, j), ch[j]});
+        L2.push_back(Item{T.son(it->b, 1, j), ch[nr + j]});
+      }
+    }
+    for (auto* it : subR) {            // b = (t', t): sons (t'_i, t_j)
+      std::vector<Node> ch;
+      P.expand(it->acc, false, ch);
+      const int nt = T.cl_nsons[T.bl_row[it->b]];
+      for (int i = 0; i < nt; i++) {
+        R1.push_back(Item{T.son(it->b, i, 0), ch[2 * i]});
+        R2.push_back(Item{T.son(it->b, i, 1), ch[2 * i + 1]});
+      }
+    }
+    solve_set(t1, L1, R1);
+    for (size_t j = 0; j < L2.size(); j++)          // acc_(t2,r') += -L_(t2,t1) R_(t1,r')
+      P.addproduct(L2[j].acc, blk(t2, t1), L1[j].b);
+    for (size_t i = 0; i < R2.size(); i++)          // acc_(t',t2) += -L_(t',t1) R_(t1,t2)  [chol: L_(t2,t1)^T]
+      P.addproduct(R2[i].acc, R1[i].b, blk(t1, t2));
+    solve_set(t2, L2, R2);
+  }
+
   // ---- LR (O8)
   void lr(int t, Node acc) {
     if (T.cl_nsons[t] == 0) {
@@ -885,8 +1004,7 @@ struct Factorizer {
     std::vector<Node> ch = split(acc, false);
     const int t1 = son0(t), t2 = t1 + 1;
     lr(t1, ch[0]);
-    solve_l(t1, blk(t1, t2), ch[1]);
-    solve_r(t1, blk(t2, t1), ch[2]);
+    solve_set(t1, {Item{blk(t1, t2), ch[1]}}, {Item{blk(t2, t1), ch[2]}});
     P.addproduct(ch[3], blk(t2, t1), blk(t1, t2));
     lr(t2, ch[3]);
   }
@@ -941,7 +1059,7 @@ struct Factorizer {
     std::vector<Node> ch = split(acc, true);   // (t1,t1), [upper], (t2,t1), (t2,t2)
     const int t1 = son0(t), t2 = t1 + 1;
     cholesky(t1, ch[0]);
-    solve_lt(t1, blk(t2, t1), ch[2]);
+    solve_set(t1, {}, {Item{blk(t2, t1), ch[2]}});
     P.addproduct(ch[3], blk(t2, t1), blk(t1, t2));   // Y = L^T view: (t1,t2) of L^T = (t2,t1) of L
     cholesky(t2, ch[3]);
   }

@@ -495,7 +495,12 @@ void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int 
     attr = true;
   }
   count_launch();
-  k_trunc_small<<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, eps);
+  // small stacks: one warp per stack (barriers of a 1-warp CTA are nearly
+  // free, and many stacks share an SM); larger: 128 / 256 threads
+  // (measured on B200: 32 or 128 threads for the small buckets is slower --
+  // the L x c loops lose more than the cheaper barriers gain)
+  const int threads = 256;
+  k_trunc_small<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps);
 }
 
 int svd_smem_capacity() { return 26 * 1024; }
