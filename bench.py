@@ -40,6 +40,12 @@ CONFIGS = {
     1: dict(level=3, leaf=32, eta=2.0, eps=1e-4, name="cfg1 hm_addmul Z<-Z+XY n=1280 (icosphere L3) leaf32 eta2 eps1e-4"),
 }
 METRIC = "batched low-rank update FP64 GFLOP/s (hm_addmul, accumulated updates)"
+# (key, icosphere level, leaf, eps, kernel 0=G 1=(G+G^T)/2, op, repetitions)
+FACTOR_RUNS = [
+    ("cfg2_hlr_n5120", 4, 32, 1e-4, 0, "lr", 2),
+    ("cfg3_hchol_n20480", 5, 32, 1e-5, 1, "chol", 1),
+    ("cfg4p_hlr_n81920", 6, 64, 1e-6, 0, "lr", 1),
+]
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA: SMs x FMA/clk x 2 x max clock
 
 
@@ -255,7 +261,8 @@ def run_ours(args, cfg):
     # ---- roofline of the dominant kernel class
     peaks = load_peaks()
     dgemm = measure_dgemm_tflops(torch, dev) if rank == 0 else None
-    top = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    # dominant single kernel class ("qr" / "jacobi_svd" are aggregates of the bucketed launches)
+    top = max(((k, v) for k, v in prof.items() if k not in ("qr", "jacobi_svd")), key=lambda kv: kv[1]["ms"])
     name, p = top
     hbm = peaks.get("hbm_gbs", 6553.6)
     if name in ("eval", "copy", "memset", "apply_q"):
@@ -275,6 +282,30 @@ def run_ours(args, cfg):
             "classes": {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                             "gflop": round(v["flops"] / 1e9, 3), "gb": round(v["bytes"] / 1e9, 3)}
                         for k, v in prof.items() if v["launches"]}}
+
+    # ---- H-LR / H-Cholesky setup seconds (BASELINE configs[1], [2] and the
+    # metric's n = 81920 H-LR, "config 4'"), device time with CUDA events
+    factor = {}
+    if rank == 0 and not args.no_factor:
+        for key, L, leaf, eps, kern, op, reps in FACTOR_RUNS:
+            xf, wf = sphere_points(L)
+            G0 = ctx.build(xf, wf, leaf, 2.0, eps, kernel=kern)
+            times = []
+            for r in range(reps):
+                Gf = G0.clone()
+                torch.cuda.synchronize(dev)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                (hm.lr if op == "lr" else hm.chol)(Gf, eps)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                times.append(e0.elapsed_time(e1) / 1e3)
+                fst = ctx.last_stats()
+                Gf.free()
+            G0.free()
+            factor[key] = {"setup_s": min(times), "runs": len(times), "n": len(wf), "leaf": leaf, "eps": eps,
+                           "truncations": fst["truncations"], "min_pivot": fst["min_pivot"]}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -296,6 +327,7 @@ def run_ours(args, cfg):
             "hmatrix": {"blocks": gstats["nblocks"], "adm": gstats["nadm"], "dense": gstats["ndense"],
                         "mean_rank": gstats["mean_rank"], "max_rank": gstats["max_rank"], "build_s": build_s},
             "roofline": roof,
+            "hlr_hchol_setup": factor,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -317,6 +349,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-factor", action="store_true", help="skip the H-LR / H-Cholesky setup timings")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

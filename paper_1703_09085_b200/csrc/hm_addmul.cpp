@@ -1157,6 +1157,12 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
   if (chol) F.cholesky(t, root);
   else F.lr(t, root);
   F.finish(min_pivot);
+  if (std::getenv("HM_DEBUG_TIMING"))
+    std::fprintf(stderr,
+                 "[hm_factor] flushes %lld trsm %lld leaf %lld | planner: levels %.3fs (sync wait %.3fs; host "
+                 "layout %.3f jobs %.3f launch %.3f trunc %.3f) split %.3fs merges %.3fs\n",
+                 (long long)F.n_flush, (long long)F.n_trsm, (long long)F.n_leaf, F.P.t_level, F.P.t_wait,
+                 F.P.t_a, F.P.t_b, F.P.t_c, F.P.t_d, F.P.t_split, F.P.t_merge);
   hm_stats_t& s = c->last;
   s.addproduct_calls = F.P.n_addproduct;
   s.evaluated_terms = F.P.n_eval;

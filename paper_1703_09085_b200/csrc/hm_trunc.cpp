@@ -56,16 +56,20 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
   std::vector<TruncSmallJob> fb[3];
   const int fcap[3] = {4 * 1024, 10 * 1024, 26 * 1024};
   std::vector<TruncReq> rest;
+  static const bool no_fused = std::getenv("HM_NO_FUSED") != nullptr;
+  double fl = 0, by = 0;
   for (const TruncReq& r : reqs) {
     const int need = trunc_small_need(r.m, r.n, r.l);
     int b = -1;
     for (int k = 0; k < 3; k++)
       if (need <= fcap[k]) { b = k; break; }
-    if (b < 0 || std::getenv("HM_NO_FUSED")) { rest.push_back(r); continue; }
+    if (b < 0 || no_fused) { rest.push_back(r); continue; }
     fb[b].push_back(TruncSmallJob{r.A, r.B, r.m, r.n, r.l, r.Aout, r.Bout, r.d_rank, r.d_sigma});
+    fl += trunc_flops(r.m, r.n, r.l, 0.0);   // convention flops (reform term k unknown here)
+    by += trunc_bytes(r.m, r.n, r.l, 0.0);
   }
   {
-    ProfScope ps(c, PC_FUSED, 0, 0);
+    ProfScope ps(c, PC_FUSED, fl, by);
     for (int b = 0; b < 3; b++)
       if (!fb[b].empty()) launch_trunc_small(ar.upload(fb[b]), (int)fb[b].size(), eps, fcap[b], c->stream);
     HM_CHECK_LAUNCH();
