@@ -50,7 +50,9 @@ typedef enum {
 } hm_status;
 
 enum { HM_KERNEL_SLP = 0, HM_KERNEL_SLP_SYM = 1 };   /* G, (G + G^T)/2 */
-enum { HM_OP_G = 0, HM_OP_GT = 1 };
+/* hm_matvec_thin operators: G, G^T, and (after hm_lr / hm_chol, in place)
+ * the unit lower factor L, the upper factor R, the Cholesky factor L and L^T. */
+enum { HM_OP_G = 0, HM_OP_GT = 1, HM_OP_L = 2, HM_OP_R = 3, HM_OP_LC = 4, HM_OP_LCT = 5 };
 
 /* Block kinds (Def 2.2 / Def 2.4). */
 enum { HM_BLOCK_SUB = 0, HM_BLOCK_ADM = 1, HM_BLOCK_DENSE = 2 };

@@ -343,7 +343,7 @@ hm_status hm_matvec_thin(hm_ctx ctx, hm_mat G, int op, double alpha, const doubl
   if (!ctx || !G || !x_dev || !y_dev) return HM_EINVAL;
   return guard(ctx, [&] {
     set_device(ctx->c);
-    if (op != HM_OP_G && op != HM_OP_GT) throw Error(HM_EINVAL, "hm_matvec_thin: bad op");
+    if (op < HM_OP_G || op > HM_OP_LCT) throw Error(HM_EINVAL, "hm_matvec_thin: bad op");
     if (ncols < 0 || ldx < G->m.tree->n || ldy < G->m.tree->n)
       throw Error(HM_EINVAL, "hm_matvec_thin: bad leading dimension");
     matvec(&ctx->c, &G->m, op, alpha, x_dev, ldx, beta, y_dev, ldy, ncols);

@@ -344,10 +344,13 @@ void matvec(Ctx* c, Mat* G, int op, double alpha, const double* x, int64_t ldx, 
   Arena ar(c);
   LeafDesc* d = ar.upload(lt);
   ProfScope ps(c, PC_MATVEC, 0, 0);
+  // op -> (transpose, part): G, G^T, unit-lower L, upper R, Cholesky L, L^T
+  static const int tr_of[6] = {0, 1, 0, 0, 0, 1};
+  static const int part_of[6] = {0, 0, 1, 2, 3, 4};
   for (int j0 = 0; j0 < ncols; j0 += chunk) {
     const int nc = std::min(chunk, ncols - j0);
-    launch_matvec_leaves(d, (int)lt.size(), op == HM_OP_GT ? 1 : 0, alpha, x + j0 * ldx, ldx,
-                         y + j0 * ldy, ldy, nc, c->stream);
+    launch_matvec_leaves(d, (int)lt.size(), tr_of[op], alpha, x + j0 * ldx, ldx, y + j0 * ldy, ldy, nc,
+                         part_of[op], c->stream);
   }
   HM_CHECK_LAUNCH();
   HM_CUDA(cudaStreamSynchronize(c->stream));

@@ -612,11 +612,20 @@ void launch_randn(double* dst, int64_t count, uint64_t seed, cudaStream_t st) {
 
 // ------------------------------------------------------------------ matvec
 // y += alpha op(G) x over all leaves (one CTA per leaf, FP64 atomics).
+// part (factor views of an in-place H-LR / H-Cholesky, SURVEY O10 probes):
+//   0 all of G; 1 L (strict lower + unit diagonal); 2 R (upper incl. diagonal);
+//   3 L of Cholesky (lower incl. diagonal); 4 its transpose (call with trans=1).
 __global__ void __launch_bounds__(256) k_matvec(const LeafDesc* __restrict__ leaves, int trans,
                                                 double alpha, const double* __restrict__ x,
-                                                int64_t ldx, double* y, int64_t ldy, int ncols) {
+                                                int64_t ldx, double* y, int64_t ldy, int ncols,
+                                                int part) {
   __shared__ double tmp[4096];  // k x ncols (host guarantees k*ncols <= 4096)
   const LeafDesc L = leaves[blockIdx.x];
+  const bool diag = L.row0 == L.col0 && L.m == L.n;
+  if (part != 0 && !diag) {
+    const bool lower = L.row0 > L.col0;
+    if ((part == 2) == lower) return;   // R: upper blocks only; L parts: lower blocks only
+  }
   const int orow = trans ? L.col0 : L.row0, vrow = trans ? L.row0 : L.col0;
   const int mo = trans ? L.n : L.m, ko = trans ? L.m : L.n;
   if (L.kind == 2) {
@@ -624,7 +633,14 @@ __global__ void __launch_bounds__(256) k_matvec(const LeafDesc* __restrict__ lea
       const int i = (int)(e % mo), j = (int)(e / mo);
       double s = 0.0;
       for (int p = 0; p < ko; p++) {
-        const double a = trans ? L.A[p + (int64_t)i * L.m] : L.A[i + (int64_t)p * L.m];
+        // stored entry (r, c) of the leaf
+        const int r = trans ? p : i, cc = trans ? i : p;
+        double a = L.A[r + (int64_t)cc * L.m];
+        if (part != 0 && diag) {
+          if (part == 1) a = (r > cc) ? a : (r == cc ? 1.0 : 0.0);
+          else if (part == 2) a = (r <= cc) ? a : 0.0;
+          else a = (r >= cc) ? a : 0.0;
+        }
         s = fma(a, x[vrow + p + (int64_t)j * ldx], s);
       }
       atomicAdd(&y[orow + i + (int64_t)j * ldy], alpha * s);
@@ -652,10 +668,10 @@ __global__ void __launch_bounds__(256) k_matvec(const LeafDesc* __restrict__ lea
 
 void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double alpha,
                           const double* x, int64_t ldx, double* y, int64_t ldy, int ncols,
-                          cudaStream_t st) {
+                          int part, cudaStream_t st) {
   if (nleaves <= 0) return;
   count_launch();
-  k_matvec<<<nleaves, 256, 0, st>>>(leaves, trans, alpha, x, ldx, y, ldy, ncols);
+  k_matvec<<<nleaves, 256, 0, st>>>(leaves, trans, alpha, x, ldx, y, ldy, ncols, part);
 }
 
 __global__ void k_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta) {

@@ -169,7 +169,7 @@ void launch_norm(const NormJob* d_jobs, int njobs, double* out, cudaStream_t st)
 void launch_randn(double* dst, int64_t count, uint64_t seed, cudaStream_t st);
 void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double alpha,
                           const double* x, int64_t ldx, double* y, int64_t ldy, int ncols,
-                          cudaStream_t st);
+                          int part, cudaStream_t st);
 void launch_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta, cudaStream_t st);
 
 int64_t launch_count();     // process-wide number of kernel launches

@@ -122,3 +122,41 @@ def test_factor_golden(hm, ctx, kind, cfg):
     assert st["truncations"] == meta["truncations"]
     assert abs(st["min_pivot"] - meta["min_pivot"]) <= 1e-9 * meta["min_pivot"]
     _check(hm, ctx, G, g, meta)
+
+
+def _probe_residual_gpu(hm, G0, F, n, perm, kind):
+    """||G v - L(R v)|| / ||G v|| (LR) or ||G v - L(L^T v)|| / ||G v|| with the
+    device matvec on 8 probes."""
+    import torch
+    v = probe_vectors(n)[perm]
+    x = torch.from_numpy(v.T.copy()).cuda().T
+    gv = torch.zeros_like(x)
+    hm.matvec(G0, x, gv)
+    t = torch.zeros_like(x)
+    y = torch.zeros_like(x)
+    if kind == "lr":
+        hm.matvec(F, x, t, op=3)      # R v
+        hm.matvec(F, t, y, op=2)      # L (R v)
+    else:
+        hm.matvec(F, x, t, op=5)      # L^T v
+        hm.matvec(F, t, y, op=4)      # L (L^T v)
+    return float(torch.linalg.norm(gv - y) / torch.linalg.norm(gv))
+
+
+@pytest.mark.parametrize("kind,L,leaf,eps", [
+    ("lr", 4, 32, 1e-4),     # configs[1]
+    ("chol", 5, 32, 1e-5),   # configs[2]
+    ("lr", 6, 64, 1e-6),     # the metric's n = 81920 H-LR
+    ("lr", 7, 64, 1e-4),     # configs[4]: n = 327680, fully HBM resident
+])
+def test_factor_probe_residual(hm, ctx, kind, L, leaf, eps):
+    """Property valid at any size (north star check 4): probe residual of the
+    device factors <= 50 eps (SURVEY #21), min pivot positive (no shift)."""
+    x, w = sphere_points(L)
+    G0 = ctx.build(x, w, leaf, 2.0, eps, kernel=0 if kind == "lr" else 1)
+    F = G0.clone()
+    (hm.lr if kind == "lr" else hm.chol)(F, eps)
+    assert ctx.last_stats()["min_pivot"] > 0
+    res = _probe_residual_gpu(hm, G0, F, len(w), G0.perm, kind)
+    assert res <= 50 * eps, res
+    print(f"{kind} n={len(w)} probe residual {res:.3e}")
