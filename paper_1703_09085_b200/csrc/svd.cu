@@ -25,6 +25,9 @@
 namespace hm {
 
 static constexpr double kUs = 1.1102230246251565e-16;  // 2^-53
+// fused TRUNC: no stack QR when m, n <= this (0 = always QR the thin side;
+// measured: skipping it does not shorten the H-LR critical path)
+static constexpr int kNoQrRows = 0;
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -104,14 +107,22 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
   const int p = tr ? c : L, q = tr ? L : c;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = blockDim.x, NW = NT >> 5;
+  // nrm[col]: squared norm of the trailing part (rows >= j) of column col;
+  // nrm2[col]: the same without row j (rows > j), both maintained exactly by
+  // the update pass, so the Householder step needs no extra reduction.
+  double* nrm2 = sig + 2 * (int64_t)c;
   for (int j = tid; j < c; j += NT) perm[j] = j;
   __syncthreads();
   for (int j = warp; j < c; j += NW) {
     const double* x = C + (int64_t)j * L;
-    double s = 0.0;
-    for (int i = lane; i < L; i += 32) s = fma(x[i], x[i], s);
+    double s = 0.0, s2 = 0.0;
+    for (int i = lane; i < L; i += 32) {
+      s = fma(x[i], x[i], s);
+      if (i > 0) s2 = fma(x[i], x[i], s2);
+    }
     s = wsum(s);
-    if (lane == 0) nrm[j] = s;
+    s2 = wsum(s2);
+    if (lane == 0) { nrm[j] = s; nrm2[j] = s2; }
   }
   __syncthreads();
   double part = 0.0;
@@ -138,16 +149,15 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
       for (int i = tid; i < L; i += NT) { const double t = a[i]; a[i] = b[i]; b[i] = t; }
       if (tid == 0) {
         const double t = nrm[j]; nrm[j] = nrm[piv]; nrm[piv] = t;
+        const double t2 = nrm2[j]; nrm2[j] = nrm2[piv]; nrm2[piv] = t2;
         const int pt = perm[j]; perm[j] = perm[piv]; perm[piv] = pt;
       }
       __syncthreads();
     }
     double* x = C + (int64_t)j * L;
-    double pp = 0.0;
-    for (int i = j + 1 + tid; i < L; i += NT) pp = fma(x[i], x[i], pp);
-    const double xn2 = bsum(pp, red);
     if (tid == 0) {
       const double alpha = x[j];
+      const double xn2 = nrm2[j];   // ||x[j+1:]||^2, summed directly (no cancellation)
       double t = 0.0, sc = 0.0, beta = alpha;
       if (xn2 > 0.0) {
         beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
@@ -172,14 +182,16 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
         d = (wsum(d) + y[j]) * t;
         if (lane == 0) y[j] -= d;
       }
-      double nn = 0.0;
+      double nn = 0.0, nn2 = 0.0;
       for (int i = j + 1 + lane; i < L; i += 32) {
         const double yi = y[i] - d * x[i];
         y[i] = yi;
         nn = fma(yi, yi, nn);
+        if (i > j + 1) nn2 = fma(yi, yi, nn2);
       }
       nn = wsum(nn);
-      if (lane == 0) nrm[col] = nn;
+      nn2 = wsum(nn2);
+      if (lane == 0) { nrm[col] = nn; nrm2[col] = nn2; }
     }
     __syncthreads();
     rt = j + 1;
@@ -418,6 +430,7 @@ __device__ void apply_q_smem(const double* Vr, const double* tau, int rows, int 
 int trunc_small_need(int m, int n, int l) {
   int qa = 0, qb = 0;
   if (n >= m) qb = l < n; else qa = l < m;
+  if (m <= kNoQrRows && n <= kNoQrRows) qa = qb = 0;
   const int p = qa ? l : m, q = qb ? l : n;
   const int64_t L = p > q ? p : q, c = p < q ? p : q;
   const int64_t need = (int64_t)(m + n) * l + 2 * (int64_t)l + L * c + 2 * c * c + 6 * c;
@@ -433,6 +446,10 @@ __global__ void k_trunc_small(const TruncSmallJob* __restrict__ jobs, double eps
   const int m = J.m, n = J.n, l = J.l, tid = threadIdx.x, NT = blockDim.x;
   int qa = 0, qb = 0;
   if (n >= m) qb = l < n; else qa = l < m;
+  // small factors: no QR of the stack -- the column-pivoted QR of M = A B^T
+  // stops at the numerical rank anyway, and the stack QR only adds
+  // sequential Householder steps (latency) for these sizes
+  if (m <= kNoQrRows && n <= kNoQrRows) qa = qb = 0;
   const int p = qa ? l : m, q = qb ? l : n;
   const bool tall = p >= q;
   const int L = tall ? p : q, c = tall ? q : p;
