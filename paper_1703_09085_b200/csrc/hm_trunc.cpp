@@ -91,6 +91,10 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     // inside the SVD kernel orthogonalises the other side.
     if (r.n >= r.m) { qa[i] = 0; qb[i] = r.l < r.n; }
     else { qa[i] = r.l < r.m; qb[i] = 0; }
+    // both factors tall and the one-sided M (min(m,n) x l) too large for shared
+    // memory: QR both (two independent CTAs) so M = R_A R_B^T is only l x l --
+    // avoids a third, sequential QR of M on the critical path
+    if (r.l < r.m && r.l < r.n && (int64_t)std::min(r.m, r.n) * r.l > 12 * 1024) qa[i] = qb[i] = 1;
     p[i] = qa[i] ? r.l : r.m;
     q[i] = qb[i] ? r.l : r.n;
     if (qa[i]) tau_total += r.l;
