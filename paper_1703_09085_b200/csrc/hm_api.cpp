@@ -408,7 +408,8 @@ hm_status hm_profile_get(hm_ctx ctx, hm_prof_t* out) {
     static const char* names[PC_COUNT] = {"qr", "gemm_M", "jacobi_svd", "apply_q", "copy", "eval",
                                           "dense_add", "memset", "gen", "build_gemm", "norm", "matvec",
                                           "svd_smem3k", "svd_smem8k", "svd_smem26k", "svd_global", "qr_smem4k", "qr_blk384",
-                                          "qr_blk768", "qr_blk1536", "qr_blk_big", "pre_qr_M", "trsm", "leaf_lu_chol", "trunc_fused"};
+                                          "qr_blk768", "qr_blk1536", "qr_blk_big", "pre_qr_M", "trsm", "leaf_lu_chol", "trunc_fused",
+                                          "tsqr_stack"};
     std::memset(out, 0, sizeof(*out));
     out->count = PC_COUNT;
     for (int i = 0; i < PC_COUNT; i++) {

@@ -40,7 +40,7 @@ bool debug_sync();   // HM_DEBUG_SYNC=1: synchronize and check after every launc
 
 enum ProfClass {
   PC_QR = 0, PC_GEMM_M, PC_SVD, PC_APPLYQ, PC_COPY, PC_EVAL, PC_DENSE, PC_MEMSET,
-  PC_GEN, PC_BUILD_GEMM, PC_NORM, PC_MATVEC, PC_SVD_B0, PC_SVD_B1, PC_SVD_B2, PC_SVD_B3, PC_QR_SMALL, PC_QR_B0, PC_QR_B1, PC_QR_B2, PC_QR_B3, PC_PREQR, PC_TRSM, PC_LEAF, PC_FUSED, PC_COUNT
+  PC_GEN, PC_BUILD_GEMM, PC_NORM, PC_MATVEC, PC_SVD_B0, PC_SVD_B1, PC_SVD_B2, PC_SVD_B3, PC_QR_SMALL, PC_QR_B0, PC_QR_B1, PC_QR_B2, PC_QR_B3, PC_PREQR, PC_TRSM, PC_LEAF, PC_FUSED, PC_TSQR, PC_COUNT
 };
 
 struct Ctx {

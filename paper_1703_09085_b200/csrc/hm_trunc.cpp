@@ -103,8 +103,75 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   }
   double* tau = ar.alloc(tau_total + 1);
   double* Mbuf = ar.alloc(m_total + 1);
+  // --- tall thin factors get a TSQR plan: the factor is cut into chunks of h
+  // rows, every chunk is QR'd by its own CTA, the chunk R's are stacked
+  // (upper triangles, zeros below) and the stack is QR'd the same way until one
+  // chunk remains.  Same factorisation A = Q R (Q = blockdiag(Q_chunks) Q_stack,
+  // R = the last level's R), but the single-CTA row sweep over thousands of
+  // rows becomes nch independent CTAs.
+  static const int ts_min = [] { const char* e = std::getenv("HM_TSQR_ROWS"); return e ? std::atoi(e) : 1536; }();
+  static const int ts_h = [] { const char* e = std::getenv("HM_TSQR_H"); return e ? std::atoi(e) : 768; }();
+  struct TsLevel { double* V; int rows, ld, h, nch; double* tau; size_t xoff; double* X; int ldx; };
+  struct TsPlan { int job, side, l, kcap; std::vector<TsLevel> lv; };
+  std::vector<TsPlan> ts;
+  std::vector<int> tsp[2] = {std::vector<int>(nj, -1), std::vector<int>(nj, -1)};
+  size_t xslab = 0;
+  for (int i = 0; i < nj; i++) {
+    const TruncReq& r = reqs[i];
+    for (int side = 0; side < 2; side++) {
+      const int rows0 = side == 0 ? r.m : r.n;
+      if (!(side == 0 ? qa[i] : qb[i]) || ts_min <= 0 || rows0 <= ts_min || 2 * r.l > ts_h) continue;
+      TsPlan P{i, side, r.l, trunc_kcap(r.m, r.n, r.l), {}};
+      TsLevel L{side == 0 ? r.A : r.B, rows0, rows0, 0, 1, nullptr, 0, side == 0 ? r.Aout : r.Bout, rows0};
+      for (;;) {
+        if (L.rows > ts_min) { L.h = ts_h; L.nch = L.rows / ts_h; }
+        else { L.h = L.rows; L.nch = 1; }
+        L.tau = ar.alloc((size_t)L.nch * r.l);
+        P.lv.push_back(L);
+        if (L.nch == 1) break;
+        const int rows = L.nch * r.l;
+        L = TsLevel{ar.alloc((size_t)rows * r.l), rows, rows, 0, 1, nullptr, xslab, nullptr, rows};
+        xslab += (size_t)rows * P.kcap;
+      }
+      tsp[side][i] = (int)ts.size();
+      ts.push_back(std::move(P));
+    }
+  }
+  double* xbuf = xslab ? ar.alloc(xslab) : nullptr;
+  size_t maxdepth = 0;
+  for (TsPlan& P : ts) {
+    for (size_t j = 1; j < P.lv.size(); j++) P.lv[j].X = xbuf + P.lv[j].xoff;
+    maxdepth = std::max(maxdepth, P.lv.size());
+  }
+  auto chunk = [](const TsLevel& L, int ch, int& r0, int& rows) {
+    r0 = ch * L.h;
+    rows = ch == L.nch - 1 ? L.rows - r0 : L.h;
+  };
   // --- QR jobs, bucketed by shared-memory need
-  std::vector<QrJob> qr_small, qr_big, qr_glob;
+  auto launch_qr_set = [&](const std::vector<QrJob>& jobs) {
+    std::vector<QrJob> qs, qbk[4], qr_huge;
+    for (const QrJob& j : jobs) {
+      const int64_t need = (int64_t)j.m * j.n;
+      if (need <= 4 * 1024) { qs.push_back(j); continue; }
+      if (j.m > 24 * 1024) { qr_huge.push_back(j); continue; }
+      const int b = j.m <= 384 ? 0 : (j.m <= 768 ? 1 : (j.m <= 1536 ? 2 : 3));
+      qbk[b].push_back(j);
+    }
+    if (!qs.empty()) {
+      ProfScope pb(c, PC_QR_SMALL, 0, (double)qs.size());
+      launch_qr(ar.upload(qs), (int)qs.size(), 4 * 1024, st);
+    }
+    // blocked (compact-WY) QR, bucketed by panel height so that small panels
+    // get several CTAs per SM: cap = 16 * rows doubles of shared memory
+    const int qcap[4] = {6 * 1024, 12 * 1024, 24 * 1024, 24 * 1024};
+    for (int b = 0; b < 4; b++)
+      if (!qbk[b].empty()) {
+        ProfScope pb(c, PC_QR_B0 + b, 0, (double)qbk[b].size());
+        launch_qr_blocked(ar.upload(qbk[b]), (int)qbk[b].size(), qcap[b], st);
+      }
+    if (!qr_huge.empty()) launch_qr(ar.upload(qr_huge), (int)qr_huge.size(), 0, st);
+  };
+  std::vector<QrJob> qjobs;
   std::vector<double*> tauA(nj, nullptr), tauB(nj, nullptr), Mp(nj, nullptr);
   size_t to = 0, mo = 0;
   double fl_qr = 0;
@@ -116,38 +183,55 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       const bool doit = side == 0 ? qa[i] : qb[i];
       if (!doit) continue;
       const int rows = side == 0 ? r.m : r.n;
-      QrJob j{side == 0 ? r.A : r.B, rows, r.l, rows, tau + to, nullptr};
+      fl_qr += 2.0 * rows * r.l * r.l;
+      if (tsp[side][i] >= 0) {
+        const TsLevel& L = ts[tsp[side][i]].lv[0];
+        for (int ch = 0; ch < L.nch; ch++) {
+          int r0, cr;
+          chunk(L, ch, r0, cr);
+          qjobs.push_back(QrJob{L.V + r0, cr, r.l, L.ld, L.tau + (size_t)ch * r.l, nullptr});
+        }
+        continue;
+      }
+      qjobs.push_back(QrJob{side == 0 ? r.A : r.B, rows, r.l, rows, tau + to, nullptr});
       (side == 0 ? tauA : tauB)[i] = tau + to;
       to += r.l;
-      const int64_t need = (int64_t)rows * r.l;
-      fl_qr += 2.0 * rows * r.l * r.l;
-      if (need <= 4 * 1024) qr_small.push_back(j);
-      else if (need <= qr_smem_capacity()) qr_big.push_back(j);
-      else qr_glob.push_back(j);
     }
   }
+  auto add_copy = [](std::vector<CopyJob>& v, int64_t& tiles, double* dst, int ldd, const double* src,
+                     int lds, int rows, int cols, int upper) {
+    CopyJob j{};
+    j.dst = dst; j.src = src; j.ldd = ldd; j.lds = lds; j.rows = rows; j.cols = cols;
+    j.coef = 1.0; j.upper = upper; j.tile0 = tiles;
+    tiles += (int64_t)((rows + 31) / 32) * ((cols + 31) / 32);
+    v.push_back(j);
+  };
   {
     ProfScope ps(c, PC_QR, fl_qr, 0);
-    if (!qr_small.empty()) {
-      ProfScope pb(c, PC_QR_SMALL, 0, (double)qr_small.size());
-      launch_qr(ar.upload(qr_small), (int)qr_small.size(), 4 * 1024, st);
+    launch_qr_set(qjobs);
+    // TSQR upper levels: stack the chunk R's, QR the stack
+    for (size_t lvl = 1; lvl < maxdepth; lvl++) {
+      ProfScope pt(c, PC_TSQR, 0, 0);
+      std::vector<CopyJob> cj;
+      std::vector<QrJob> qj;
+      int64_t tiles = 0;
+      for (const TsPlan& P : ts) {
+        if (P.lv.size() <= lvl) continue;
+        const TsLevel &D = P.lv[lvl - 1], &U = P.lv[lvl];
+        for (int ch = 0; ch < D.nch; ch++) {
+          int r0, cr;
+          chunk(D, ch, r0, cr);
+          add_copy(cj, tiles, U.V + (size_t)ch * P.l, U.ld, D.V + r0, D.ld, P.l, P.l, 1);
+        }
+        for (int ch = 0; ch < U.nch; ch++) {
+          int r0, cr;
+          chunk(U, ch, r0, cr);
+          qj.push_back(QrJob{U.V + r0, cr, P.l, U.ld, U.tau + (size_t)ch * P.l, nullptr});
+        }
+      }
+      launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
+      launch_qr_set(qj);
     }
-    // blocked (compact-WY) QR, bucketed by panel height so that small panels
-    // get several CTAs per SM: cap = 16 * rows doubles of shared memory
-    std::vector<QrJob> qb[4], qr_huge;
-    const int qcap[4] = {6 * 1024, 12 * 1024, 24 * 1024, 24 * 1024};
-    for (auto* v : {&qr_big, &qr_glob})
-      for (auto& j : *v) {
-        if (j.m > 24 * 1024) { qr_huge.push_back(j); continue; }
-        const int b = j.m <= 384 ? 0 : (j.m <= 768 ? 1 : (j.m <= 1536 ? 2 : 3));
-        qb[b].push_back(j);
-      }
-    for (int b = 0; b < 4; b++)
-      if (!qb[b].empty()) {
-        ProfScope pb(c, PC_QR_B0 + b, 0, (double)qb[b].size());
-        launch_qr_blocked(ar.upload(qb[b]), (int)qb[b].size(), qcap[b], st);
-      }
-    if (!qr_huge.empty()) launch_qr(ar.upload(qr_huge), (int)qr_huge.size(), 0, st);
     HM_CHECK_LAUNCH();
   }
   // --- M = op(A) op(B)^T, stored in its TALL orientation Mt (L x c): Mt = M if
@@ -162,13 +246,19 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     tallM[i] = p[i] >= q[i];
     if (p[i] == 0 || q[i] == 0) continue;
     GemmJob g{};
+    // R factor source of each side: the factor itself, or a TSQR plan's last level
+    const double* ra = r.A;
+    const double* rb = r.B;
+    int lda_ = r.m, ldb_ = r.n;
+    if (tsp[0][i] >= 0) { ra = ts[tsp[0][i]].lv.back().V; lda_ = ts[tsp[0][i]].lv.back().ld; }
+    if (tsp[1][i] >= 0) { rb = ts[tsp[1][i]].lv.back().V; ldb_ = ts[tsp[1][i]].lv.back().ld; }
     if (tallM[i]) {
-      g.A = r.A; g.lda = r.m; g.maskA = qa[i];
-      g.B = r.B; g.ldb = r.n; g.maskB = qb[i];
+      g.A = ra; g.lda = lda_; g.maskA = qa[i];
+      g.B = rb; g.ldb = ldb_; g.maskB = qb[i];
       g.m = p[i]; g.n = q[i]; g.ldc = p[i];
     } else {
-      g.A = r.B; g.lda = r.n; g.maskA = qb[i];
-      g.B = r.A; g.ldb = r.m; g.maskB = qa[i];
+      g.A = rb; g.lda = ldb_; g.maskA = qb[i];
+      g.B = ra; g.ldb = lda_; g.maskB = qa[i];
       g.m = q[i]; g.n = p[i]; g.ldc = q[i];
     }
     g.transA = 0; g.transB = 1;
@@ -277,12 +367,61 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       const int lrows = tallM[i] ? r.m : r.n;
       aq1.push_back(ApplyQJob{Mp[i], tauM[i], L, cc, L, lo, lrows, 0, r.d_rank});
     }
-    if (qa[i]) aq.push_back(ApplyQJob{r.A, tauA[i], r.m, r.l, r.m, r.Aout, r.m, 0, r.d_rank});
-    if (qb[i]) aq.push_back(ApplyQJob{r.B, tauB[i], r.n, r.l, r.n, r.Bout, r.n, 0, r.d_rank});
+    for (int side = 0; side < 2; side++) {
+      if (!(side == 0 ? qa[i] : qb[i])) continue;
+      if (tsp[side][i] >= 0) {   // level 0 of a TSQR plan: one job per chunk
+        const TsLevel& L = ts[tsp[side][i]].lv[0];
+        for (int ch = 0; ch < L.nch; ch++) {
+          int r0, cr;
+          chunk(L, ch, r0, cr);
+          aq.push_back(ApplyQJob{L.V + r0, L.tau + (size_t)ch * r.l, cr, r.l, L.ld, L.X + r0, L.ldx, 0,
+                                 r.d_rank});
+        }
+      } else if (side == 0) {
+        aq.push_back(ApplyQJob{r.A, tauA[i], r.m, r.l, r.m, r.Aout, r.m, 0, r.d_rank});
+      } else {
+        aq.push_back(ApplyQJob{r.B, tauB[i], r.n, r.l, r.n, r.Bout, r.n, 0, r.d_rank});
+      }
+    }
   }
   {
     ProfScope ps(c, PC_APPLYQ, 0, 0);
     if (!aq1.empty()) launch_applyq(ar.upload(aq1), (int)aq1.size(), st);
+    if (!ts.empty()) {
+      // TSQR: X_top[0:l] = output[0:l] (the SVD's factor), zeros below; then per
+      // level (top down) X_j <- blockdiag(Q_j) X_j and scatter its l-row blocks
+      // to the chunk heads of X_{j-1} (X_0 = the output itself, whose rows
+      // below each chunk head are already zero).
+      ProfScope pt(c, PC_TSQR, 0, 0);
+      HM_CUDA(cudaMemsetAsync(xbuf, 0, xslab * sizeof(double), st));
+      std::vector<CopyJob> cj;
+      int64_t tiles = 0;
+      for (const TsPlan& P : ts)
+        add_copy(cj, tiles, P.lv.back().X, P.lv.back().ldx, P.lv[0].X, P.lv[0].ldx, P.l, P.kcap, 0);
+      launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
+      for (size_t lvl = maxdepth - 1; lvl >= 1; lvl--) {
+        std::vector<ApplyQJob> tq;
+        cj.clear();
+        tiles = 0;
+        for (const TsPlan& P : ts) {
+          if (P.lv.size() <= lvl) continue;
+          const TsLevel &U = P.lv[lvl], &D = P.lv[lvl - 1];
+          const int* rk = reqs[P.job].d_rank;
+          for (int ch = 0; ch < U.nch; ch++) {
+            int r0, cr;
+            chunk(U, ch, r0, cr);
+            tq.push_back(ApplyQJob{U.V + r0, U.tau + (size_t)ch * P.l, cr, P.l, U.ld, U.X + r0, U.ldx, 0, rk});
+          }
+          for (int ch = 0; ch < D.nch; ch++) {
+            int r0, cr;
+            chunk(D, ch, r0, cr);
+            add_copy(cj, tiles, D.X + r0, D.ldx, U.X + (size_t)ch * P.l, U.ldx, P.l, P.kcap, 0);
+          }
+        }
+        launch_applyq(ar.upload(tq), (int)tq.size(), st);
+        launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
+      }
+    }
     if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), st);
     HM_CHECK_LAUNCH();
   }

@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(256) k_copy(const CopyJob* __restrict__ jobs, 
     if (J.identity) {
       if (i != j) continue;
       v = J.coef;
+    } else if (J.upper && i > j) {
+      v = 0.0;
     } else {
       v = J.coef * (J.trans ? J.src[j + (int64_t)i * J.lds] : J.src[i + (int64_t)j * J.lds]);
     }

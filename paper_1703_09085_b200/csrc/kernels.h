@@ -85,6 +85,7 @@ struct CopyJob {
   int trans, identity, accumulate;
   double coef;
   int64_t tile0;
+  int upper;           // copy only the upper triangle of op(src), zeros below
 };
 
 // A leaf of an H-matrix in DFS order (for addeval / addevaltrans).

@@ -24,30 +24,15 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-__device__ double bsum(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  v = wsum(v);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double s = (lane < nw) ? red[lane] : 0.0;
-    s = wsum(s);
-    if (lane == 0) red[0] = s;
-  }
-  __syncthreads();
-  const double s = red[0];
-  __syncthreads();
-  return s;
-}
 }  // namespace
 
-__global__ void k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
+__global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
   extern __shared__ double Vs[];            // panel / V (rows x nb), column-major
-  __shared__ double red[32];
   __shared__ double T[kNbMax * kNbMax];     // upper triangular, column-major
   __shared__ double G[kNbMax * kNbMax];     // V^T V
-  __shared__ double s_tau, s_scale;
+  __shared__ double red2[2 * 16 * kNbMax];  // per-warp partial sums (<= 16 warps), double-buffered
+  __shared__ double piv[2 * kNbMax];        // pivot row of the current column, double-buffered
+  __shared__ double stau[kNbMax];
   const QrJob J = jobs[blockIdx.x];
   const int m = J.m, n = J.n, lda = J.lda;
   double* A = J.A;
@@ -63,42 +48,71 @@ __global__ void k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
       Vs[e] = A[(k0 + i) + (int64_t)(k0 + j) * lda];
     }
     __syncthreads();
-    // 2. unblocked Householder on the panel (in shared memory)
+    // 2. unblocked Householder on the panel (in shared memory), ONE barrier per
+    //    column: thread tid owns rows i = tid (mod NT) for the whole panel; one
+    //    pass gives x.x and x.y_c for every later column c (x = column j below
+    //    the diagonal); the pivot row j is published through piv[] by its
+    //    owner; every thread then derives beta, tau and the column updates
+    //    itself.  red / piv are double-buffered by the parity of j.
     for (int j = 0; j < kb; j++) {
-      double* x = Vs + (int64_t)j * rows;
-      double pp = 0.0;
-      for (int i = j + 1 + tid; i < rows; i += NT) pp = fma(x[i], x[i], pp);
-      const double xn2 = bsum(pp, red);
-      if (tid == 0) {
-        const double alpha = x[j];
-        double t = 0.0, sc = 0.0, beta = alpha;
-        if (xn2 > 0.0) {
-          beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-          t = (beta - alpha) / beta;
-          sc = 1.0 / (alpha - beta);
-        }
-        x[j] = beta;
-        J.tau[k0 + j] = t;
-        s_tau = t;
-        s_scale = sc;
+      const int nc = kb - j;               // slot 0: x.x ; slot q: x.y_{j+q}
+      const double* x = Vs + (int64_t)j * rows;
+      double part[kNbMax];
+#pragma unroll
+      for (int q = 0; q < kNbMax; q++) part[q] = 0.0;
+      const int i0 = tid > j ? tid : tid + ((j - tid) / NT + 1) * NT;   // first owned row below j
+      for (int i = i0; i < rows; i += NT) {
+        const double xi = x[i];
+#pragma unroll
+        for (int q = 0; q < kNbMax; q++)
+          if (q < nc) part[q] = fma(xi, Vs[i + (int64_t)(j + q) * rows], part[q]);
       }
+      double* rb = red2 + (j & 1) * (16 * kNbMax);
+      double* pv = piv + (j & 1) * kNbMax;
+#pragma unroll
+      for (int q = 0; q < kNbMax; q++)
+        if (q < nc) {
+          const double s = wsum(part[q]);
+          if (lane == 0) rb[warp * kNbMax + q] = s;
+        }
+      if (tid == j % NT)
+        for (int q = 0; q < nc; q++) pv[q] = Vs[j + (int64_t)(j + q) * rows];
       __syncthreads();
-      const double t = s_tau, sc = s_scale;
+      // lane q of every warp totals slot q over the warps
+      double tq = 0.0;
+      if (lane < nc)
+        for (int w = 0; w < NW; w++) tq += rb[w * kNbMax + lane];
+      const double xn2 = __shfl_sync(0xffffffffu, tq, 0);
+      const double alpha = pv[0];
+      double t = 0.0, sc = 0.0, beta = alpha;
+      if (xn2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        t = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+      // d_q = tau (y_q[j] + v.y_q below), v = sc x below the pivot
+      double dq = 0.0;
+      if (lane >= 1 && lane < nc) dq = (pv[lane] + sc * tq) * t;
+      double d[kNbMax];
+#pragma unroll
+      for (int q = 1; q < kNbMax; q++) d[q] = __shfl_sync(0xffffffffu, dq, q);
+      if (tid == 0) { J.tau[k0 + j] = t; stau[j] = t; }
+      if (tid == j % NT) {
+        Vs[j + (int64_t)j * rows] = beta;
+#pragma unroll
+        for (int q = 1; q < kNbMax; q++)
+          if (q < nc) Vs[j + (int64_t)(j + q) * rows] = pv[q] - d[q];
+      }
       if (t != 0.0)
-        for (int i = j + 1 + tid; i < rows; i += NT) x[i] *= sc;
-      __syncthreads();
-      if (t != 0.0) {
-        for (int c = j + 1 + warp; c < kb; c += NW) {
-          double* y = Vs + (int64_t)c * rows;
-          double d = 0.0;
-          for (int i = j + 1 + lane; i < rows; i += 32) d = fma(x[i], y[i], d);
-          d = (wsum(d) + y[j]) * t;
-          if (lane == 0) y[j] -= d;
-          for (int i = j + 1 + lane; i < rows; i += 32) y[i] -= d * x[i];
+        for (int i = i0; i < rows; i += NT) {
+          const double vi = Vs[i + (int64_t)j * rows] * sc;
+          Vs[i + (int64_t)j * rows] = vi;
+#pragma unroll
+          for (int q = 1; q < kNbMax; q++)
+            if (q < nc) Vs[i + (int64_t)(j + q) * rows] -= d[q] * vi;
         }
-      }
-      __syncthreads();
     }
+    __syncthreads();
     // 3. write the panel (R + reflectors) back; make V explicit (unit diagonal, zero above)
     for (int64_t e = tid; e < (int64_t)rows * kb; e += NT) {
       const int i = (int)(e % rows), j = (int)(e / rows);
@@ -126,47 +140,63 @@ __global__ void k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
       if (lane == 0) G[a + b * kNbMax] = d;
     }
     __syncthreads();
-    if (tid == 0) {
-      for (int i = 0; i < kb; i++) {
-        const double ti = J.tau[k0 + i];
-        for (int r = 0; r < i; r++) {
-          double s = 0.0;
-          for (int q = r; q < i; q++) s += T[r + q * kNbMax] * G[q + i * kNbMax];
-          T[r + i * kNbMax] = -ti * s;
-        }
-        T[i + i * kNbMax] = ti;
+    // lane r of warp 0 computes row r of T (it only needs its own row and G)
+    if (warp == 0 && lane < kb) {
+      const int r = lane;
+      for (int i = r; i < kb; i++) {
+        if (i == r) { T[r + r * kNbMax] = stau[r]; continue; }
+        double s = 0.0;
+        for (int q = r; q < i; q++) s = fma(T[r + q * kNbMax], G[q + i * kNbMax], s);
+        T[r + i * kNbMax] = -stau[i] * s;
       }
     }
     __syncthreads();
-    // 5. trailing update, one warp per column: a <- a - V (T^T (V^T a))
-    for (int cc = warp; cc < ncol; cc += NW) {
-      double* a = A + k0 + (int64_t)(k0 + kb + cc) * lda;
-      double w[kNbMax];
+    // 5. trailing update, one warp per PAIR of columns (each V element read
+    //    from shared memory feeds two FMAs): a <- a - V (T^T (V^T a))
+    for (int c2 = 2 * warp; c2 < ncol; c2 += 2 * NW) {
+      double* a0 = A + k0 + (int64_t)(k0 + kb + c2) * lda;
+      const bool two = c2 + 1 < ncol;
+      double* a1 = two ? a0 + lda : a0;
+      double w0[kNbMax], w1[kNbMax];
 #pragma unroll
-      for (int q = 0; q < kNbMax; q++) w[q] = 0.0;
+      for (int q = 0; q < kNbMax; q++) w0[q] = w1[q] = 0.0;
       for (int i = lane; i < rows; i += 32) {
-        const double ai = a[i];
+        const double x0 = a0[i], x1 = a1[i];
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
-          if (q < kb) w[q] = fma(Vs[i + (int64_t)q * rows], ai, w[q]);
+          if (q < kb) {
+            const double v = Vs[i + (int64_t)q * rows];
+            w0[q] = fma(v, x0, w0[q]);
+            w1[q] = fma(v, x1, w1[q]);
+          }
       }
 #pragma unroll
-      for (int q = 0; q < kNbMax; q++) w[q] = wsum(w[q]);
-      double z[kNbMax];
+      for (int q = 0; q < kNbMax; q++) { w0[q] = wsum(w0[q]); w1[q] = wsum(w1[q]); }
+      // z = T^T w in place, from the last row up ((T^T w)_q = sum_{r<=q} T(r,q) w_r)
 #pragma unroll
-      for (int q = 0; q < kNbMax; q++) {
-        double s = 0.0;
+      for (int q = kNbMax - 1; q >= 0; q--) {
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int r = 0; r < kNbMax; r++)
-          if (r <= q && q < kb) s = fma(T[r + q * kNbMax], w[r], s);   // (T^T w)_q = sum_{r<=q} T(r,q) w_r
-        z[q] = s;
+        for (int r = 0; r <= q; r++)
+          if (q < kb) {
+            const double tr = T[r + q * kNbMax];
+            s0 = fma(tr, w0[r], s0);
+            s1 = fma(tr, w1[r], s1);
+          }
+        w0[q] = s0;
+        w1[q] = s1;
       }
       for (int i = lane; i < rows; i += 32) {
-        double s = 0.0;
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
-          if (q < kb) s = fma(Vs[i + (int64_t)q * rows], z[q], s);
-        a[i] -= s;
+          if (q < kb) {
+            const double v = Vs[i + (int64_t)q * rows];
+            s0 = fma(v, w0[q], s0);
+            s1 = fma(v, w1[q], s1);
+          }
+        a0[i] -= s0;
+        if (two) a1[i] -= s1;
       }
     }
     __syncthreads();

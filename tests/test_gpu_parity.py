@@ -74,6 +74,33 @@ def test_trunc_kernel_prescribed_sigma(hm, ctx, eps):
         assert lowrank_diff(U, V, Uo, Vo) <= TOL * lowrank_norm(Uo, Vo) + 1e-14
 
 
+def test_trunc_kernel_tall(hm, ctx):
+    """Tall stacks taking the TSQR route (factor rows > 1536: chunked QR, stacked
+    R's, up to five levels, ragged last chunks) -- same closed-form checks."""
+    eps = 1e-6
+    rng = np.random.default_rng(21)
+    shapes = [(5000, 3000, 40, 2), (40000, 200, 150, 1), (1700, 1600, 376, 1), (2000, 30, 10, 0),
+              (60000, 400, 300, 2), (3100, 2900, 500, 0)]
+    stacks, svals = [], []
+    for m, n, q, junk in shapes:
+        s = 10.0 ** (-0.13 * np.arange(q))
+        A, B = _prescribed(rng, m, n, s, junk)
+        stacks.append((A, B))
+        svals.append(s)
+    out, ranks, _ = hm.test_trunc_batched(ctx, stacks, eps)
+    for (A, B), (U, V), k, s in zip(stacks, out, ranks, svals):
+        kk = next(j for j in range(len(s) + 1) if np.sum(s[j:] ** 2) <= eps ** 2 * np.sum(s ** 2))
+        assert k == kk
+        # ||A B^T - U V^T||_F = ||R1 R2^T|| with [A, -U] = Q1 R1, [B, V] = Q2 R2
+        R1 = np.linalg.qr(np.hstack([A, -U]), mode="r")
+        R2 = np.linalg.qr(np.hstack([B, V]), mode="r")
+        err = np.linalg.norm(R1 @ R2.T)
+        tail = np.sqrt(np.sum(s[k:] ** 2))
+        scale = np.linalg.norm(A) * np.linalg.norm(B)   # rounding level of the stack itself
+        assert abs(err - tail) <= 1e-6 * tail + 1e-13 * scale, (err, tail, scale)
+        np.testing.assert_allclose(U.T @ U, np.eye(k), atol=1e-12)
+
+
 def test_trunc_kernel_degenerate(hm, ctx):
     rng = np.random.default_rng(3)
     R = (rng.standard_normal((30, 4)), rng.standard_normal((25, 4)))
