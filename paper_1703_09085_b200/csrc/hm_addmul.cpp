@@ -64,6 +64,7 @@ struct Planner {
   std::vector<LeafDesc> lx, ly;
   std::vector<double> lx_mat, lx_mn, ly_mat, ly_mn;   // DFS prefix sums (convention counts)
   double t_wait = 0;
+  int64_t n_sync = 0;
   LeafDesc *dlx = nullptr, *dly = nullptr;
   // stats
   int64_t n_addproduct = 0, n_eval = 0, n_trunc = 0, n_cols = 0, n_merge = 0, n_dense = 0;
@@ -255,6 +256,7 @@ struct Planner {
 
   void sync_ranks(int* d_ranks, const std::vector<int>& fp_ids) {
     if (fp_ids.empty()) return;
+    n_sync++;
     std::vector<int> h(fp_ids.size());
     auto a = std::chrono::steady_clock::now();
     HM_CUDA(cudaStreamSynchronize(c->stream));
@@ -1159,9 +1161,9 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
   F.finish(min_pivot);
   if (std::getenv("HM_DEBUG_TIMING"))
     std::fprintf(stderr,
-                 "[hm_factor] flushes %lld trsm %lld leaf %lld | planner: levels %.3fs (sync wait %.3fs; host "
+                 "[hm_factor] flushes %lld trsm %lld leaf %lld syncs %lld | planner: levels %.3fs (sync wait %.3fs; host "
                  "layout %.3f jobs %.3f launch %.3f trunc %.3f) split %.3fs merges %.3fs\n",
-                 (long long)F.n_flush, (long long)F.n_trsm, (long long)F.n_leaf, F.P.t_level, F.P.t_wait,
+                 (long long)F.n_flush, (long long)F.n_trsm, (long long)F.n_leaf, (long long)F.P.n_sync, F.P.t_level, F.P.t_wait,
                  F.P.t_a, F.P.t_b, F.P.t_c, F.P.t_d, F.P.t_split, F.P.t_merge);
   hm_stats_t& s = c->last;
   s.addproduct_calls = F.P.n_addproduct;

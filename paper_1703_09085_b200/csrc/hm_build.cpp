@@ -233,10 +233,10 @@ Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int 
             HM_CUDA(cudaMemsetAsync(X[a], 0, sizeof(double) * rows * r, st));
             cj.push_back(CopyJob{X[a], nullptr, rows, 0, rows, r, 0, 1, 0, 1.0, ct});
             ct += gen_tiles(rows, r);
-            aq.push_back(ApplyQJob{V[a], tau[a], rows, r, rows, X[a], rows, r, nullptr});
+            aq.push_back(ApplyQJob{V[a], tau[a], rows, r, rows, X[a], rows, r, nullptr, nullptr});
           }
           launch_copy(ar.upload(cj), (int)cj.size(), ct, st);
-          launch_applyq(ar.upload(aq), (int)aq.size(), st);
+          launch_applyq(ar.upload(aq), (int)aq.size(), r, st);
           HM_CHECK_LAUNCH();
         };
         gemm_all(0);

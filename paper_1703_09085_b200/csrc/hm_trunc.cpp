@@ -53,6 +53,13 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
 // single-kernel TRUNC (k_trunc_small); the others to the staged pipeline.
 void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double eps) {
   if (reqs.empty()) return;
+  if (const char* dump = std::getenv("HM_DUMP_TRUNC")) {   // diagnostics: shapes of every batch
+    if (FILE* f = std::fopen(dump, "a")) {
+      for (const TruncReq& r : reqs) std::fprintf(f, "%d %d %d\n", r.m, r.n, r.l);
+      std::fprintf(f, "#\n");
+      std::fclose(f);
+    }
+  }
   std::vector<TruncSmallJob> fb[3];
   const int fcap[3] = {4 * 1024, 10 * 1024, 26 * 1024};
   std::vector<TruncReq> rest;
@@ -111,7 +118,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   // rows becomes nch independent CTAs.
   static const int ts_min = [] { const char* e = std::getenv("HM_TSQR_ROWS"); return e ? std::atoi(e) : 1536; }();
   static const int ts_h = [] { const char* e = std::getenv("HM_TSQR_H"); return e ? std::atoi(e) : 768; }();
-  struct TsLevel { double* V; int rows, ld, h, nch; double* tau; size_t xoff; double* X; int ldx; };
+  struct TsLevel { double* V; int rows, ld, h, nch; double* tau; size_t xoff; double* X; int ldx; double* T; };
   struct TsPlan { int job, side, l, kcap; std::vector<TsLevel> lv; };
   std::vector<TsPlan> ts;
   std::vector<int> tsp[2] = {std::vector<int>(nj, -1), std::vector<int>(nj, -1)};
@@ -122,15 +129,16 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       const int rows0 = side == 0 ? r.m : r.n;
       if (!(side == 0 ? qa[i] : qb[i]) || ts_min <= 0 || rows0 <= ts_min || 2 * r.l > ts_h) continue;
       TsPlan P{i, side, r.l, trunc_kcap(r.m, r.n, r.l), {}};
-      TsLevel L{side == 0 ? r.A : r.B, rows0, rows0, 0, 1, nullptr, 0, side == 0 ? r.Aout : r.Bout, rows0};
+      TsLevel L{side == 0 ? r.A : r.B, rows0, rows0, 0, 1, nullptr, 0, side == 0 ? r.Aout : r.Bout, rows0, nullptr};
       for (;;) {
         if (L.rows > ts_min) { L.h = ts_h; L.nch = L.rows / ts_h; }
         else { L.h = L.rows; L.nch = 1; }
         L.tau = ar.alloc((size_t)L.nch * r.l);
+        L.T = ar.alloc((size_t)L.nch * ((r.l + 15) / 16) * 256);
         P.lv.push_back(L);
         if (L.nch == 1) break;
         const int rows = L.nch * r.l;
-        L = TsLevel{ar.alloc((size_t)rows * r.l), rows, rows, 0, 1, nullptr, xslab, nullptr, rows};
+        L = TsLevel{ar.alloc((size_t)rows * r.l), rows, rows, 0, 1, nullptr, xslab, nullptr, rows, nullptr};
         xslab += (size_t)rows * P.kcap;
       }
       tsp[side][i] = (int)ts.size();
@@ -146,6 +154,9 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   auto chunk = [](const TsLevel& L, int ch, int& r0, int& rows) {
     r0 = ch * L.h;
     rows = ch == L.nch - 1 ? L.rows - r0 : L.h;
+  };
+  auto chunkT = [](const TsLevel& L, int ch, int rows, int l) -> double* {
+    return qr_has_T(rows, l) ? L.T + (size_t)ch * ((l + 15) / 16) * 256 : nullptr;
   };
   // --- QR jobs, bucketed by shared-memory need
   auto launch_qr_set = [&](const std::vector<QrJob>& jobs) {
@@ -172,7 +183,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     if (!qr_huge.empty()) launch_qr(ar.upload(qr_huge), (int)qr_huge.size(), 0, st);
   };
   std::vector<QrJob> qjobs;
-  std::vector<double*> tauA(nj, nullptr), tauB(nj, nullptr), Mp(nj, nullptr);
+  std::vector<double*> tauA(nj, nullptr), tauB(nj, nullptr), Mp(nj, nullptr), TA(nj, nullptr), TB(nj, nullptr);
   size_t to = 0, mo = 0;
   double fl_qr = 0;
   for (int i = 0; i < nj; i++) {
@@ -189,12 +200,14 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
         for (int ch = 0; ch < L.nch; ch++) {
           int r0, cr;
           chunk(L, ch, r0, cr);
-          qjobs.push_back(QrJob{L.V + r0, cr, r.l, L.ld, L.tau + (size_t)ch * r.l, nullptr});
+          qjobs.push_back(QrJob{L.V + r0, cr, r.l, L.ld, L.tau + (size_t)ch * r.l, chunkT(L, ch, cr, r.l)});
         }
         continue;
       }
-      qjobs.push_back(QrJob{side == 0 ? r.A : r.B, rows, r.l, rows, tau + to, nullptr});
+      double* Tf = qr_has_T(rows, r.l) ? ar.alloc((size_t)((r.l + 15) / 16) * 256) : nullptr;
+      qjobs.push_back(QrJob{side == 0 ? r.A : r.B, rows, r.l, rows, tau + to, Tf});
       (side == 0 ? tauA : tauB)[i] = tau + to;
+      (side == 0 ? TA : TB)[i] = Tf;
       to += r.l;
     }
   }
@@ -226,7 +239,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
         for (int ch = 0; ch < U.nch; ch++) {
           int r0, cr;
           chunk(U, ch, r0, cr);
-          qj.push_back(QrJob{U.V + r0, cr, P.l, U.ld, U.tau + (size_t)ch * P.l, nullptr});
+          qj.push_back(QrJob{U.V + r0, cr, P.l, U.ld, U.tau + (size_t)ch * P.l, chunkT(U, ch, cr, P.l)});
         }
       }
       launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
@@ -275,6 +288,16 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     launch_gemm(ar.upload(gj), (int)gj.size(), tiles, st);
     HM_CHECK_LAUNCH();
   }
+  if (const char* dm = std::getenv("HM_DUMP_M")) {   // diagnostics: first job's M (tall orientation)
+    const size_t cnt = (size_t)std::max(p[0], q[0]) * std::min(p[0], q[0]);
+    std::vector<double> h(cnt);
+    HM_CUDA(cudaStreamSynchronize(st));
+    HM_CUDA(cudaMemcpy(h.data(), Mp[0], cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    if (FILE* f = std::fopen(dm, "wb")) {
+      std::fwrite(h.data(), sizeof(double), cnt, f);
+      std::fclose(f);
+    }
+  }
   // --- SVD jobs; matrices too large for shared memory are first reduced by an
   // unpivoted blocked QR (Mt = Q1 R1) and the SVD kernel works on R1 (c x c).
   std::vector<SvdJob> sj[4];
@@ -284,18 +307,19 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   int* d_sw = dump ? static_cast<int*>(ar.alloc_bytes(sizeof(int) * (nj + 1))) : nullptr;
   std::vector<int> bucket_of(nj);
   std::vector<char> preqr(nj, 0);
-  std::vector<double*> tauM(nj, nullptr);
+  std::vector<double*> tauM(nj, nullptr), TM(nj, nullptr);
   std::vector<QrJob> pq[4];
   const int pqcap[4] = {6 * 1024, 12 * 1024, 24 * 1024, 24 * 1024};
   for (int i = 0; i < nj; i++) {
     const TruncReq& r = reqs[i];
     const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
-    const int64_t full = (int64_t)L * cc + 2 * (int64_t)cc * cc + 6 * (int64_t)cc;
+    const int64_t full = svd_smem_need(L, cc);
     if (full > caps[2] && L > cc && L <= 24 * 1024) {
       preqr[i] = 1;
       tauM[i] = ar.alloc(cc + 1);
       const int b = L <= 384 ? 0 : (L <= 768 ? 1 : (L <= 1536 ? 2 : 3));
-      pq[b].push_back(QrJob{Mp[i], L, cc, L, tauM[i], nullptr});
+      if (L <= 1536) TM[i] = ar.alloc((size_t)((cc + 15) / 16) * 256);
+      pq[b].push_back(QrJob{Mp[i], L, cc, L, tauM[i], TM[i]});
     }
   }
   {
@@ -314,7 +338,6 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     s.p = preqr[i] ? cc : L;
     s.q = cc;
     s.maskM = preqr[i];
-    s.flip = tallM[i] ? 0 : 1;   // keep Fig. 2's convention: the A-side factor is orthonormal
     // left (orthonormal U_k) / right (V_k S_k) outputs of the tall matrix
     double* lo = tallM[i] ? r.Aout : r.Bout;
     double* ro = tallM[i] ? r.Bout : r.Aout;
@@ -324,7 +347,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     s.rank = r.d_rank;
     s.sigma = r.d_sigma;
     const int Ls = s.p;
-    const int64_t need = (int64_t)Ls * cc + 2 * (int64_t)cc * cc + 6 * (int64_t)cc;
+    const int64_t need = svd_smem_need(Ls, cc);
     const int cap = bucket_cap(need);
     fl_svd += 22.0 * (double)cc * cc * cc;
     int b = 3;
@@ -365,7 +388,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
       double* lo = tallM[i] ? r.Aout : r.Bout;
       const int lrows = tallM[i] ? r.m : r.n;
-      aq1.push_back(ApplyQJob{Mp[i], tauM[i], L, cc, L, lo, lrows, 0, r.d_rank});
+      aq1.push_back(ApplyQJob{Mp[i], tauM[i], L, cc, L, lo, lrows, cc, r.d_rank, TM[i]});
     }
     for (int side = 0; side < 2; side++) {
       if (!(side == 0 ? qa[i] : qb[i])) continue;
@@ -374,19 +397,24 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
         for (int ch = 0; ch < L.nch; ch++) {
           int r0, cr;
           chunk(L, ch, r0, cr);
-          aq.push_back(ApplyQJob{L.V + r0, L.tau + (size_t)ch * r.l, cr, r.l, L.ld, L.X + r0, L.ldx, 0,
-                                 r.d_rank});
+          aq.push_back(ApplyQJob{L.V + r0, L.tau + (size_t)ch * r.l, cr, r.l, L.ld, L.X + r0, L.ldx,
+                                 trunc_kcap(r.m, r.n, r.l), r.d_rank, chunkT(L, ch, cr, r.l)});
         }
       } else if (side == 0) {
-        aq.push_back(ApplyQJob{r.A, tauA[i], r.m, r.l, r.m, r.Aout, r.m, 0, r.d_rank});
+        aq.push_back(ApplyQJob{r.A, tauA[i], r.m, r.l, r.m, r.Aout, r.m, trunc_kcap(r.m, r.n, r.l), r.d_rank, TA[i]});
       } else {
-        aq.push_back(ApplyQJob{r.B, tauB[i], r.n, r.l, r.n, r.Bout, r.n, 0, r.d_rank});
+        aq.push_back(ApplyQJob{r.B, tauB[i], r.n, r.l, r.n, r.Bout, r.n, trunc_kcap(r.m, r.n, r.l), r.d_rank, TB[i]});
       }
     }
   }
   {
     ProfScope ps(c, PC_APPLYQ, 0, 0);
-    if (!aq1.empty()) launch_applyq(ar.upload(aq1), (int)aq1.size(), st);
+    auto cmax = [](const std::vector<ApplyQJob>& v) {
+      int m = 0;
+      for (const ApplyQJob& j : v) m = std::max(m, j.c);
+      return m;
+    };
+    if (!aq1.empty()) launch_applyq(ar.upload(aq1), (int)aq1.size(), cmax(aq1), st);
     if (!ts.empty()) {
       // TSQR: X_top[0:l] = output[0:l] (the SVD's factor), zeros below; then per
       // level (top down) X_j <- blockdiag(Q_j) X_j and scatter its l-row blocks
@@ -410,7 +438,8 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
           for (int ch = 0; ch < U.nch; ch++) {
             int r0, cr;
             chunk(U, ch, r0, cr);
-            tq.push_back(ApplyQJob{U.V + r0, U.tau + (size_t)ch * P.l, cr, P.l, U.ld, U.X + r0, U.ldx, 0, rk});
+            tq.push_back(ApplyQJob{U.V + r0, U.tau + (size_t)ch * P.l, cr, P.l, U.ld, U.X + r0, U.ldx, P.kcap, rk,
+                                   chunkT(U, ch, cr, P.l)});
           }
           for (int ch = 0; ch < D.nch; ch++) {
             int r0, cr;
@@ -418,11 +447,11 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
             add_copy(cj, tiles, D.X + r0, D.ldx, U.X + (size_t)ch * P.l, U.ldx, P.l, P.kcap, 0);
           }
         }
-        launch_applyq(ar.upload(tq), (int)tq.size(), st);
+        launch_applyq(ar.upload(tq), (int)tq.size(), cmax(tq), st);
         launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
       }
     }
-    if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), st);
+    if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), cmax(aq), st);
     HM_CHECK_LAUNCH();
   }
 }

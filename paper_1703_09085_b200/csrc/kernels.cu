@@ -214,31 +214,77 @@ void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ apply Q
-// X <- H_0 ... H_{r-1} X ; one warp per column of X, reflectors from L2.
+// X <- H_0 ... H_{r-1} X ; one warp per column of X (grid.y spreads the
+// columns over CTAs), reflectors read from L2.  With the QR's compact-WY T
+// factors the reflectors are applied 16 at a time (Q_p = I - Y_p T_p Y_p^T,
+// last panel first): two passes over the rows per panel instead of two per
+// reflector.
 __global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jobs) {
   const ApplyQJob J = jobs[blockIdx.x];
   const int c = J.cdyn ? *J.cdyn : J.c;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int col = warp; col < c; col += 8) {
-    double* x = J.X + (int64_t)col * J.ldx;
-    for (int j = J.r - 1; j >= 0; j--) {
-      const double tau = J.tau[j];
-      if (tau == 0.0) continue;
-      const double* v = J.V + (int64_t)j * J.ldv;
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < J.m; i += 32) s += v[i] * x[i];
-      s = (warp_sum(s) + x[j]) * tau;
-      if (lane == 0) x[j] -= s;
-      for (int i = j + 1 + lane; i < J.m; i += 32) x[i] -= s * v[i];
+  const int col = blockIdx.y * 8 + warp;
+  if (col >= c) return;
+  double* x = J.X + (int64_t)col * J.ldx;
+  if (J.T) {
+    for (int p = (J.r + 15) / 16 - 1; p >= 0; p--) {
+      const int j0 = p * 16, kb = min(16, J.r - j0);
+      const double* Vp = J.V + (int64_t)j0 * J.ldv;
+      double w[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) w[q] = 0.0;
+      for (int i = j0 + lane; i < J.m; i += 32) {
+        const double xi = x[i];
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+          if (q < kb) {
+            const double y = i > j0 + q ? Vp[i + (int64_t)q * J.ldv] : (i == j0 + q ? 1.0 : 0.0);
+            w[q] = fma(y, xi, w[q]);
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; q++) w[q] = warp_sum(w[q]);
+      const double* Tp = J.T + 256 * p;
+      double z[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = q; r < 16; r++)
+          if (r < kb) s = fma(Tp[q + r * 16], w[r], s);
+        z[q] = s;
+      }
+      for (int i = j0 + lane; i < J.m; i += 32) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+          if (q < kb) {
+            const double y = i > j0 + q ? Vp[i + (int64_t)q * J.ldv] : (i == j0 + q ? 1.0 : 0.0);
+            s = fma(y, z[q], s);
+          }
+        x[i] -= s;
+      }
       __syncwarp();
     }
+    return;
+  }
+  for (int j = J.r - 1; j >= 0; j--) {
+    const double tau = J.tau[j];
+    if (tau == 0.0) continue;
+    const double* v = J.V + (int64_t)j * J.ldv;
+    double s = 0.0;
+    for (int i = j + 1 + lane; i < J.m; i += 32) s += v[i] * x[i];
+    s = (warp_sum(s) + x[j]) * tau;
+    if (lane == 0) x[j] -= s;
+    for (int i = j + 1 + lane; i < J.m; i += 32) x[i] -= s * v[i];
+    __syncwarp();
   }
 }
 
-void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st) {
-  if (njobs <= 0) return;
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st) {
+  if (njobs <= 0 || cmax <= 0) return;
   count_launch();
-  k_applyq<<<njobs, 256, 0, st>>>(d_jobs);
+  k_applyq<<<dim3(njobs, (cmax + 7) / 8), 256, 0, st>>>(d_jobs);
 }
 
 // SVD kernels: see svd.cu

@@ -31,11 +31,16 @@ struct QrJob {
   double* A;
   int m, n, lda;
   double* tau;
-  double* work;        // unused by the smem path
+  double* T;           // optional (k_qr_blocked with 16-column panels, see qr_has_T):
+                       // compact-WY T factor of panel p at T + 256 p (16 x 16, upper)
 };
+// True iff the QR of an m x n panel runs k_qr_blocked with 16-column panels
+// (hm_trunc's routing) and can therefore emit the T factors for k_applyq.
+inline bool qr_has_T(int m, int n) { return (int64_t)m * n > 4 * 1024 && m <= 1536; }
 
-// X <- Q X with Q = H_0 H_1 ... H_{r-1} from a QrJob (X: m x c, ldx); c is
-// read from *cdyn (device) when cdyn != nullptr.
+// X <- Q X with Q = H_0 H_1 ... H_{r-1} from a QrJob (X: m x c, ldx); c is the
+// host-side column bound, the actual count is read from *cdyn (device) when
+// cdyn != nullptr.  T: the QR's compact-WY panel factors (nullable).
 struct ApplyQJob {
   const double* V;     // reflectors (m x r, ldv)
   const double* tau;
@@ -43,12 +48,15 @@ struct ApplyQJob {
   double* X;
   int ldx, c;
   const int* cdyn;
+  const double* T;
 };
 
-// One-sided Jacobi SVD of M (p x q, ldm) + eps rank rule + factor output:
-//   Aout[0:p, 0:k] = U_k (orthonormal), rows p..ma-1 zeroed  (ld lda)
-//   Bout[0:q, 0:k] = V_k Sigma_k,         rows q..nb-1 zeroed (ld ldb)
-//   *rank = k, sigma[0:min(p,q)] (descending) if sigma != nullptr
+// SVD of M (p x q, ldm; QRCP + one-sided Jacobi, svd.cu) + eps rank rule +
+// factor output with M ~= Aout Bout^T, *rank = k:
+//   the factor on the SHORT side of M (Bout if p >= q, else Aout) is
+//   orthonormal (right / left singular vectors), the other one carries the
+//   singular values; rows beyond p (Aout) / q (Bout) up to ma / nb are zeroed.
+//   sigma[0:min(p,q)] (descending) if sigma != nullptr.
 struct SvdJob {
   const double* M;
   int p, q, ldm;
@@ -58,18 +66,19 @@ struct SvdJob {
   int ldb, nb;
   int* rank;
   double* sigma;
-  double* work;        // global work (L x c doubles) when it does not fit smem
+  double* work;        // global work (svd_smem_need doubles) when it does not fit smem
   int* nsweep;         // optional: number of Jacobi sweeps used (diagnostics)
   int maskM;           // M is upper triangular (entries below the diagonal read as 0)
-  int flip;            // put Sigma on the Aout side instead (Bout orthonormal)
 };
+int svd_smem_need(int p, int q);   // doubles of workspace of one SvdJob
 
-// Fused TRUNC_eps of a small stack (everything in shared memory).
+// Fused TRUNC_eps of a small stack (everything in shared memory); one of the
+// two output factors is orthonormal (see SvdJob).
 struct TruncSmallJob {
   const double* A;     // m x l (ld m)
   const double* B;     // n x l (ld n)
   int m, n, l;
-  double* Aout;        // m x k (ld m), orthonormal
+  double* Aout;        // m x k (ld m)
   double* Bout;        // n x k (ld n)
   int* rank;
   double* sigma;
@@ -156,7 +165,7 @@ struct NormJob {
 void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
 void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);   // rows <= 24576
-void launch_applyq(const ApplyQJob* d_jobs, int njobs, cudaStream_t st);
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st);

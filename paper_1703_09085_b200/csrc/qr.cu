@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
     }
     __syncthreads();
     const int ncol = n - k0 - kb;
-    if (ncol <= 0) continue;
+    const bool wantT = J.T != nullptr && nb == kNbMax;   // panel factors for k_applyq
+    if (ncol <= 0 && !wantT) continue;
     // 4. T (dlarft, forward columnwise): G = V^T V, T(i,i) = tau_i,
     //    T(0:i, i) = -tau_i T(0:i,0:i) G(0:i, i)
     for (int pr = warp; pr < kb * kb; pr += NW) {
@@ -151,6 +152,9 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
       }
     }
     __syncthreads();
+    if (wantT)
+      for (int e = tid; e < kNbMax * kNbMax; e += NT) J.T[(int64_t)(k0 / kNbMax) * kNbMax * kNbMax + e] = T[e];
+    if (ncol <= 0) continue;
     // 5. trailing update, one warp per PAIR of columns (each V element read
     //    from shared memory feeds two FMAs): a <- a - V (T^T (V^T a))
     for (int c2 = 2 * warp; c2 < ncol; c2 += 2 * NW) {

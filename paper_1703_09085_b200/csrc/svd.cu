@@ -9,22 +9,43 @@
 //      also the classic preconditioner of one-sided Jacobi (Drmac-Veselic):
 //      kernel blocks need ~6 sweeps on R^T instead of ~25 on M.
 //   2. One-sided Jacobi (Hestenes) on X = R^T (c x r~), round-robin parallel
-//      ordering, one warp per column pair, rotations accumulated in V (r~ x r~).
-//   3. sigma_i = ||X V e_i||, descending order, smallest k with
-//      sum_{i>k} sigma_i^2 <= eps^2 sum_i sigma_i^2 (tails from the bottom).
-//   4. Factors: C = Q V Sigma (W/sigma)^T P^T with W = X V, so
-//        p >= q: U_k = Q [V_k; 0],        V_k S_k = P W_k
-//        p <  q: U_k = P W_k / sigma_k,   V_k S_k = Q [V_k S_k; 0]
-//      (Q applied from the stored reflectors).
+//      ordering, one group of 8/16/32 lanes per column pair.
+//   3. sigma_i = ||W e_i|| (W = X V, orthogonal columns), descending order,
+//      smallest k with sum_{i>k} sigma_i^2 <= eps^2 sum_i sigma_i^2 (tails
+//      from the bottom).
+//   4. Factors, without accumulating V: R^T = U_x S V^T with U_x = W S^-1, so
+//      C = (Q R U_x) (P U_x)^T -- the permuted (short) side gets the
+//      orthonormal P U_x,k = P W_k S_k^-1, the Q side gets Q [R U_x,k; 0] =
+//      Q [V_k S_k; 0] (one product with the R kept in C, then the stored
+//      reflectors).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "kernels.h"
 
 namespace hm {
 
 static constexpr double kUs = 1.1102230246251565e-16;  // 2^-53
+static constexpr int kE = 8;   // column elements per lane kept in registers
+
+// diagnostics: -DHM_PHASE_TIMING prints per-phase SM cycles of CTA 0
+#ifdef HM_PHASE_TIMING
+#define PHASE(name)                                                                        \
+  do {                                                                                     \
+    __syncthreads();                                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                             \
+      const long long t_ = clock64();                                                      \
+      printf("[phase] %-10s %8lld cycles\n", name, t_ - ph_t0);                            \
+      ph_t0 = t_;                                                                          \
+    }                                                                                      \
+  } while (0)
+#define PHASE_INIT long long ph_t0 = clock64()
+#else
+#define PHASE(name) do {} while (0)
+#define PHASE_INIT do {} while (0)
+#endif
 // fused TRUNC: no stack QR when m, n <= this (0 = always QR the thin side;
 // measured: skipping it does not shorten the H-LR critical path)
 static constexpr int kNoQrRows = 0;
@@ -51,6 +72,15 @@ __device__ double bsum(double v, double* red) {
   __syncthreads();
   return s;
 }
+
+// sum over aligned groups of G lanes (G = 8/16/32); all 32 lanes must call
+__device__ __forceinline__ double gsum(double v, int G) {
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// lanes per column for column-parallel passes over columns of length n
+__device__ __forceinline__ int col_group(int n) { return n <= 64 ? 8 : (n <= 128 ? 16 : 32); }
 
 // block argmax (value, lowest index on ties) and sum; results broadcast.
 __device__ void bargmax_sum(double v, int idx, double s, double* redv, int* redi, double* reds,
@@ -86,133 +116,60 @@ __device__ void bargmax_sum(double v, int idx, double s, double* redv, int* redi
   __syncthreads();
 }
 
+// round-robin position of slot k in round r (r < cp - 1): no integer division
 __device__ __forceinline__ int rr_pos(int k, int r, int cp) {
-  return k == 0 ? 0 : ((k - 1 + r) % (cp - 1)) + 1;
+  int x = k - 1 + r;
+  if (x >= cp - 1) x -= cp - 1;
+  return k == 0 ? 0 : x + 1;
+}
+
+// Leading dimension of a shared-memory column block: >= n and = 8 (mod 16), so
+// the 8-lane column groups of one warp (consecutive columns) fall into the two
+// 16-bank halves alternately (conflict-free LDS.64).
+__host__ __device__ __forceinline__ int pad_ld(int n) { return n + ((24 - (n & 15)) & 15); }
+
+// shared-memory doubles of svd_core on an L x c matrix: C (pad(L) x c),
+// X (pad(c) x c), tau / nrm / sig / perm+order / nrm2 (c each)
+__host__ __device__ __forceinline__ int64_t svd_ws(int L, int c) {
+  return (int64_t)pad_ld(L) * c + (int64_t)pad_ld(c) * c + 6 * (int64_t)c;
 }
 
 int svd_smem_need(int p, int q) {
-  const int64_t L = p > q ? p : q, c = p < q ? p : q;
-  return (int)(L * c + 2 * c * c + 6 * c);
+  const int L = p > q ? p : q, c = p < q ? p : q;
+  const int64_t need = svd_ws(L, c);
+  return need > (1 << 30) ? (1 << 30) : (int)need;
 }
 
-// SVD + rank rule + factor output of the matrix already loaded in C (L x c,
-// the tall orientation of M; tr: C = M^T).  Workspace: X (c x c), V (c x c),
-// tau, nrm, sig (c each), perm, order (c ints each).  Outputs per J.
-__device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, double* C, double* X,
-                         double* V, double* tau, double* nrm, double* sig, int* perm, int* order) {
-  __shared__ double red[32], redv[32], reds[32];
-  __shared__ int redi[32];
-  __shared__ int s_rank;
-  __shared__ double s_tau, s_scale;
-  const int p = tr ? c : L, q = tr ? L : c;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NT = blockDim.x, NW = NT >> 5;
-  // nrm[col]: squared norm of the trailing part (rows >= j) of column col;
-  // nrm2[col]: the same without row j (rows > j), both maintained exactly by
-  // the update pass, so the Householder step needs no extra reduction.
-  double* nrm2 = sig + 2 * (int64_t)c;
-  for (int j = tid; j < c; j += NT) perm[j] = j;
-  __syncthreads();
-  for (int j = warp; j < c; j += NW) {
-    const double* x = C + (int64_t)j * L;
-    double s = 0.0, s2 = 0.0;
-    for (int i = lane; i < L; i += 32) {
-      s = fma(x[i], x[i], s);
-      if (i > 0) s2 = fma(x[i], x[i], s2);
-    }
-    s = wsum(s);
-    s2 = wsum(s2);
-    if (lane == 0) { nrm[j] = s; nrm2[j] = s2; }
-  }
-  __syncthreads();
-  double part = 0.0;
-  for (int j = tid; j < c; j += NT) part += nrm[j];
-  const double fro2 = bsum(part, red);
-  const double delta2 = (16.0 * kUs * kUs) * (double)c * fro2;
-  // ---------------------------------------------------------------- 1. QRCP
-  int rt = 0;
-  for (int j = 0; j < c && j < L; j++) {
-    double v = -1.0, s = 0.0;
-    int idx = 0x7fffffff;
-    for (int col = j + tid; col < c; col += NT) {
-      const double w = nrm[col];
-      s += w;
-      if (w > v) { v = w; idx = col; }
-    }
-    double vmax, rem;
-    int piv;
-    bargmax_sum(v, idx, s, redv, redi, reds, vmax, piv, rem);
-    if (!(rem > delta2)) break;
-    if (piv != j) {
-      double* a = C + (int64_t)j * L;
-      double* b = C + (int64_t)piv * L;
-      for (int i = tid; i < L; i += NT) { const double t = a[i]; a[i] = b[i]; b[i] = t; }
-      if (tid == 0) {
-        const double t = nrm[j]; nrm[j] = nrm[piv]; nrm[piv] = t;
-        const double t2 = nrm2[j]; nrm2[j] = nrm2[piv]; nrm2[piv] = t2;
-        const int pt = perm[j]; perm[j] = perm[piv]; perm[piv] = pt;
-      }
-      __syncthreads();
-    }
-    double* x = C + (int64_t)j * L;
-    if (tid == 0) {
-      const double alpha = x[j];
-      const double xn2 = nrm2[j];   // ||x[j+1:]||^2, summed directly (no cancellation)
-      double t = 0.0, sc = 0.0, beta = alpha;
-      if (xn2 > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        t = (beta - alpha) / beta;
-        sc = 1.0 / (alpha - beta);
-      }
-      x[j] = beta;
-      tau[j] = t;
-      s_tau = t;
-      s_scale = sc;
-    }
-    __syncthreads();
-    const double t = s_tau, sc = s_scale;
-    if (t != 0.0)
-      for (int i = j + 1 + tid; i < L; i += NT) x[i] *= sc;
-    __syncthreads();
-    for (int col = j + 1 + warp; col < c; col += NW) {
-      double* y = C + (int64_t)col * L;
-      double d = 0.0;
-      if (t != 0.0) {
-        for (int i = j + 1 + lane; i < L; i += 32) d = fma(x[i], y[i], d);
-        d = (wsum(d) + y[j]) * t;
-        if (lane == 0) y[j] -= d;
-      }
-      double nn = 0.0, nn2 = 0.0;
-      for (int i = j + 1 + lane; i < L; i += 32) {
-        const double yi = y[i] - d * x[i];
-        y[i] = yi;
-        nn = fma(yi, yi, nn);
-        if (i > j + 1) nn2 = fma(yi, yi, nn2);
-      }
-      nn = wsum(nn);
-      nn2 = wsum(nn2);
-      if (lane == 0) { nrm[col] = nn; nrm2[col] = nn2; }
-    }
-    __syncthreads();
-    rt = j + 1;
-  }
-  // X = R^T (c x rt), V = I
-  for (int64_t e = tid; e < (int64_t)c * rt; e += NT) {
-    const int col = (int)(e % c), i = (int)(e / c);
-    X[e] = (col >= i) ? C[i + (int64_t)col * L] : 0.0;
-  }
-  for (int64_t e = tid; e < (int64_t)rt * rt; e += NT) V[e] = ((e % rt) == (e / rt)) ? 1.0 : 0.0;
-  __syncthreads();
-  // ---------------------------------------------------------------- 2. Jacobi
-  const double tol = kUs * sqrt((double)c);
+// Jacobi rotation (c, s) zeroing x.y for columns with x.x = al, y.y = be,
+// x.y = ga: tan(theta) = sign(d g) |g| / (|d| + sqrt(d^2 + g^2)), d = be - al,
+// g = 2 ga, |theta| <= pi/4, evaluated as cos 2theta = |d| / h, cos^2 theta =
+// (1 + cos 2theta) / 2, sin theta = sin 2theta / (2 cos theta) -- two rsqrt,
+// no division (d, g pre-scaled by a power of two against over/underflow).
+__device__ __forceinline__ void jacobi_rot(double al, double be, double ga, double& cs, double& sn) {
+  const double d0 = be - al, g0 = 2.0 * ga;
+  const int ex = max(__double2hiint(d0) & 0x7ff00000, __double2hiint(g0) & 0x7ff00000);
+  const double scl = __hiloint2double(0x7fe00000 - ex, 0);
+  const double d = d0 * scl, g = g0 * scl;
+  const double rh = rsqrt(fma(d, d, g * g));
+  const double hc = fma(0.5 * fabs(d), rh, 0.5);   // cos^2 theta
+  const double r2 = rsqrt(hc);
+  cs = hc * r2;
+  sn = copysign(0.5 * fabs(g) * rh * r2, d * g);
+}
+
+// One-sided Jacobi sweeps (round-robin parallel ordering) on the columns of
+// X (c x rt, ld ldx).  One group of G lanes per column pair; each lane keeps
+// its E elements of both columns in registers for the rotation (c <= E G).
+// Returns the number of sweeps.
+template <int G, int E>
+__device__ int jacobi_sweeps(double* X, int ldx, int c, int rt, double tol2, double delta2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  constexpr int gpw = 32 / G;
+  const int gl = lane & (G - 1);
   const int cp = rt + (rt & 1);
   int sweep = 0;
   for (; sweep < 60 && rt > 1; sweep++) {
     int rot = 0;
-    // one group of G lanes per column pair (G = 8/16/32 by column length):
-    // shorter shuffle reductions and several pairs per warp in flight
-    const int G = c <= 64 ? 8 : (c <= 128 ? 16 : 32);
-    const int gl = lane & (G - 1), gpw = 32 / G;
     for (int r = 0; r < cp - 1; r++) {
       for (int base = warp * gpw; base < (cp >> 1); base += NW * gpw) {
         const int pr = base + lane / G;
@@ -223,36 +180,77 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
           b = rr_pos(cp - 1 - pr, r, cp);
           act = a < rt && b < rt;
         }
-        double* x = X + (int64_t)a * c;
-        double* y = X + (int64_t)b * c;
+        double* x = X + a * ldx + gl;
+        double* y = X + b * ldx + gl;
+        double xr[E], yr[E];
         double al = 0.0, be = 0.0, ga = 0.0;
-        if (act)
-          for (int i = gl; i < c; i += G) {
-            const double xv = x[i], yv = y[i];
-            al = fma(xv, xv, al);
-            be = fma(yv, yv, be);
-            ga = fma(xv, yv, ga);
-          }
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+          const bool ok = act && gl + u * G < c;
+          xr[u] = ok ? x[u * G] : 0.0;
+          yr[u] = ok ? y[u * G] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+          al = fma(xr[u], xr[u], al);
+          be = fma(yr[u], yr[u], be);
+          ga = fma(xr[u], yr[u], ga);
+        }
+#pragma unroll
         for (int o = G >> 1; o > 0; o >>= 1) {   // all 32 lanes shuffle (uniform control flow)
           al += __shfl_xor_sync(0xffffffffu, al, o);
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (act && fabs(ga) > tol * sqrt(al) * sqrt(be) && fmin(al, be) > delta2) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double tt = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-          const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
-          for (int i = gl; i < c; i += G) {
+        if (act && ga * ga > tol2 * al * be && fmin(al, be) > delta2) {
+          double cs, sn;
+          jacobi_rot(al, be, ga, cs, sn);
+#pragma unroll
+          for (int u = 0; u < E; u++)
+            if (gl + u * G < c) {
+              x[u * G] = cs * xr[u] - sn * yr[u];
+              y[u * G] = sn * xr[u] + cs * yr[u];
+            }
+          rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rot)) break;
+  }
+  return sweep;
+}
+
+// Same, columns streamed from shared memory (c > 8 * 32).
+__device__ int jacobi_sweeps_stream(double* X, int ldx, int c, int rt, double tol2, double delta2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int cp = rt + (rt & 1);
+  int sweep = 0;
+  for (; sweep < 60 && rt > 1; sweep++) {
+    int rot = 0;
+    for (int r = 0; r < cp - 1; r++) {
+      for (int pr = warp; pr < (cp >> 1); pr += NW) {
+        const int a = rr_pos(pr, r, cp), b = rr_pos(cp - 1 - pr, r, cp);
+        if (a >= rt || b >= rt) continue;   // warp-uniform
+        double* x = X + (int64_t)a * ldx;
+        double* y = X + (int64_t)b * ldx;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < c; i += 32) {
+          const double xv = x[i], yv = y[i];
+          al = fma(xv, xv, al);
+          be = fma(yv, yv, be);
+          ga = fma(xv, yv, ga);
+        }
+        al = wsum(al);
+        be = wsum(be);
+        ga = wsum(ga);
+        if (ga * ga > tol2 * al * be && fmin(al, be) > delta2) {
+          double cs, sn;
+          jacobi_rot(al, be, ga, cs, sn);
+          for (int i = lane; i < c; i += 32) {
             const double xv = x[i], yv = y[i];
             x[i] = cs * xv - sn * yv;
             y[i] = sn * xv + cs * yv;
-          }
-          double* u = V + (int64_t)a * rt;
-          double* w = V + (int64_t)b * rt;
-          for (int i = gl; i < rt; i += G) {
-            const double uv = u[i], wv = w[i];
-            u[i] = cs * uv - sn * wv;
-            w[i] = sn * uv + cs * wv;
           }
           rot = 1;
         }
@@ -261,16 +259,190 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
     }
     if (!__syncthreads_or(rot)) break;
   }
-  if (tid == 0 && J.nsweep) *J.nsweep = sweep + 1000 * rt;
-  // ---------------------------------------------------------------- 3. rank
-  for (int j = warp; j < rt; j += NW) {
-    const double* x = X + (int64_t)j * c;
-    double s = 0.0;
-    for (int i = lane; i < c; i += 32) s = fma(x[i], x[i], s);
-    s = wsum(s);
-    if (lane == 0) sig[j] = sqrt(s);
+  return sweep;
+}
+
+// SVD + rank rule + factor output of the matrix already loaded in C (L x c,
+// ld ldc, the tall orientation of M; tr: C = M^T).  Workspace: X (c x c, ld
+// pad(c)), tau, nrm, sig, nrm2 (c each), perm, order (c ints each).
+//
+// Factors (no rotation accumulation): the one-sided Jacobi on X = R^T gives
+// W = X V with orthogonal columns, so R^T = U_x S V^T with U_x = W S^-1 and
+//   C = Q R P^T = (Q R U_x) (P U_x)^T,
+// i.e. the permuted (short) side gets the orthonormal P U_x,k and the Q side
+// gets Q (R U_x,k) = Q V_k S_k, formed by one product with the R left in C.
+__device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, double* C, int ldc, double* X,
+                         double* tau, double* nrm, double* sig, int* perm, int* order) {
+  __shared__ double red[32];
+  __shared__ int s_rank;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
+  // nrm[col]: squared norm of the trailing part (rows >= j) of column col;
+  // nrm2[col]: the same without row j (rows > j), both maintained exactly by
+  // the update pass, so the Householder step needs no extra reduction.
+  double* nrm2 = sig + 2 * (int64_t)c;
+  const int Gq = col_group(L);
+  const int gq = lane & (Gq - 1), gpwq = 32 / Gq;
+  PHASE_INIT;
+  for (int j = tid; j < c; j += NT) perm[j] = j;
+  __syncthreads();   // C was just written by the caller
+  for (int base = warp * gpwq; base < c; base += NW * gpwq) {
+    const int j = base + lane / Gq;
+    const bool act = j < c;
+    const double* x = C + (int64_t)(act ? j : 0) * ldc;
+    double s = 0.0, s2 = 0.0;
+    if (act)
+      for (int i = gq; i < L; i += Gq) {
+        s = fma(x[i], x[i], s);
+        if (i > 0) s2 = fma(x[i], x[i], s2);
+      }
+    s = gsum(s, Gq);
+    s2 = gsum(s2, Gq);
+    if (act && gq == 0) { nrm[j] = s; nrm2[j] = s2; }
   }
   __syncthreads();
+  double part = 0.0;
+  for (int j = tid; j < c; j += NT) part += nrm[j];
+  const double fro2 = bsum(part, red);
+  const double delta2 = (16.0 * kUs * kUs) * (double)c * fro2;
+  PHASE("norms");
+  // ---------------------------------------------------------------- 1. QRCP
+  // Two barriers per step at most: every warp finds the pivot itself (argmax of
+  // nrm, lowest index on ties, identical in all warps); every thread derives
+  // beta / tau itself; groups of Gq lanes update one column each; the scaling
+  // of the reflector x is deferred to the next step (x is read by all groups
+  // during its own step).
+  int rt = 0;
+  int pending = -1;
+  double pbeta = 0.0, psc = 0.0, pt = 0.0;
+  for (int j = 0; j < c && j < L; j++) {
+    if (pending >= 0) {
+      double* xp = C + (int64_t)pending * ldc;
+      if (pt != 0.0)
+        for (int i = pending + 1 + tid; i < L; i += NT) xp[i] *= psc;
+      if (tid == 0) xp[pending] = pbeta;
+      pending = -1;
+    }
+    double v = -1.0, s = 0.0;
+    int piv = 0x7fffffff;
+    for (int col = j + lane; col < c; col += 32) {
+      const double w = nrm[col];
+      s += w;
+      if (w > v) { v = w; piv = col; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, piv, o);
+      if (ov > v || (ov == v && oi < piv)) { v = ov; piv = oi; }
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if (!(s > delta2)) break;
+    __syncthreads();   // every warp has read nrm before it is swapped / updated
+    if (piv != j) {
+      double* a = C + (int64_t)j * ldc;
+      double* b = C + (int64_t)piv * ldc;
+      for (int i = tid; i < L; i += NT) { const double t = a[i]; a[i] = b[i]; b[i] = t; }
+      if (tid == 0) {
+        const double t = nrm[j]; nrm[j] = nrm[piv]; nrm[piv] = t;
+        const double t2 = nrm2[j]; nrm2[j] = nrm2[piv]; nrm2[piv] = t2;
+        const int pp = perm[j]; perm[j] = perm[piv]; perm[piv] = pp;
+      }
+      __syncthreads();
+    }
+    const double* x = C + (int64_t)j * ldc;
+    const double alpha = x[j];
+    const double xn2 = nrm2[j];   // ||x[j+1:]||^2, summed directly (no cancellation)
+    double t = 0.0, sc = 0.0, beta = alpha;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      t = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) tau[j] = t;
+    const double tsc = t * sc;
+    for (int base = j + 1 + warp * gpwq; base < c; base += NW * gpwq) {
+      const int col = base + lane / Gq;
+      const bool act = col < c;
+      double* y = C + (int64_t)(act ? col : j) * ldc;
+      double d = 0.0;
+      if (act && t != 0.0)
+        for (int i = j + 1 + gq; i < L; i += Gq) d = fma(x[i], y[i], d);
+      d = gsum(d, Gq);
+      const double yj = act ? y[j] : 0.0;
+      d = t != 0.0 ? fma(tsc, d, t * yj) : 0.0;   // tau (y_j + v.y), v = sc x below j
+      const double ds = d * sc;
+      double nn = 0.0, nn2 = 0.0;
+      if (act)
+        for (int i = j + 1 + gq; i < L; i += Gq) {
+          const double yi = fma(-ds, x[i], y[i]);
+          y[i] = yi;
+          nn = fma(yi, yi, nn);
+          if (i > j + 1) nn2 = fma(yi, yi, nn2);
+        }
+      nn = gsum(nn, Gq);
+      nn2 = gsum(nn2, Gq);
+      __syncwarp();
+      if (act && gq == 0) { y[j] = yj - d; nrm[col] = nn; nrm2[col] = nn2; }
+    }
+    __syncthreads();
+    pending = j; pbeta = beta; psc = sc; pt = t;
+    rt = j + 1;
+  }
+  if (pending >= 0) {
+    double* xp = C + (int64_t)pending * ldc;
+    if (pt != 0.0)
+      for (int i = pending + 1 + tid; i < L; i += NT) xp[i] *= psc;
+    if (tid == 0) xp[pending] = pbeta;
+  }
+  __syncthreads();
+  PHASE("qrcp");
+  // X = R^T (c x rt, ld ldx)
+  const int ldx = pad_ld(c);
+  for (int64_t e = tid; e < (int64_t)c * rt; e += NT) {
+    const int col = (int)(e % c), i = (int)(e / c);
+    X[col + (int64_t)i * ldx] = (col >= i) ? C[i + (int64_t)col * ldc] : 0.0;
+  }
+  __syncthreads();
+  // ---------------------------------------------------------------- 2. Jacobi
+  // convergence: |x.y| <= tol sqrt(x.x y.y).  tol sits 64x above the rounding
+  // noise of the computed dot products (~u sqrt(c)): at u sqrt(c) itself the
+  // test keeps firing on noise; 64 u sqrt(c) (<= 1e-13 for c <= 128) is far
+  // below the 1e-9 parity bar.
+  const double tol = 64.0 * kUs * sqrt((double)c);
+  const double tol2 = tol * tol;
+  const int cp = rt + (rt & 1);
+  // G lanes per pair: at least c / 8 (register slices), at most what keeps
+  // every pair of a round in flight at once (NT / G >= cp / 2), within 8..32
+  int G = 8;
+  while (G < 32 && 8 * G < c) G <<= 1;
+  while (G < 32 && (NT / (2 * G)) >= (cp >> 1)) G <<= 1;
+  int sweep;
+  if (c > 8 * 32) sweep = jacobi_sweeps_stream(X, ldx, c, rt, tol2, delta2);
+  else if (G == 8) sweep = jacobi_sweeps<8, 8>(X, ldx, c, rt, tol2, delta2);
+  else if (G == 16) sweep = c <= 64 ? jacobi_sweeps<16, 4>(X, ldx, c, rt, tol2, delta2)
+                                    : jacobi_sweeps<16, 8>(X, ldx, c, rt, tol2, delta2);
+  else sweep = c <= 64 ? jacobi_sweeps<32, 2>(X, ldx, c, rt, tol2, delta2)
+                       : (c <= 128 ? jacobi_sweeps<32, 4>(X, ldx, c, rt, tol2, delta2)
+                                   : jacobi_sweeps<32, 8>(X, ldx, c, rt, tol2, delta2));
+  PHASE("jacobi");
+#ifdef HM_PHASE_TIMING
+  if (blockIdx.x == 0 && tid == 0) printf("[phase] L=%d c=%d rt=%d sweeps=%d G=%d\n", L, c, rt, sweep, G);
+#endif
+  if (tid == 0 && J.nsweep) *J.nsweep = sweep + 1000 * rt;
+  // ---------------------------------------------------------------- 3. rank
+  for (int base = warp * gpwq; base < rt; base += NW * gpwq) {
+    const int j = base + lane / Gq;
+    const bool act = j < rt;
+    const double* x = X + (int64_t)(act ? j : 0) * ldx;
+    double s = 0.0;
+    if (act)
+      for (int i = gq; i < c; i += Gq) s = fma(x[i], x[i], s);
+    s = gsum(s, Gq);
+    if (act && gq == 0) sig[j] = sqrt(s);
+  }
+  __syncthreads();
+  double* ss = nrm;   // sorted sigma_i^2, then 1 / sigma_i of the kept ones
   for (int j = tid; j < rt; j += NT) {
     const double sj = sig[j];
     int pos = 0;
@@ -279,31 +451,41 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
       pos += (si > sj) || (si == sj && i < j);
     }
     order[pos] = j;
+    ss[pos] = sj * sj;
   }
   __syncthreads();
   if (tid == 0) {
     double acc = 0.0;
-    for (int i = rt - 1; i >= 0; i--) { const double s = sig[order[i]]; acc += s * s; }
+#pragma unroll 8
+    for (int i = rt - 1; i >= 0; i--) acc += ss[i];
     int k = 0;
     if (acc > 0.0) {
       const double thr = (eps * eps) * acc;
       double tail = 0.0;
       k = rt;
-      for (int kk = rt; kk >= 0; kk--) {
-        if (kk < rt) { const double s = sig[order[kk]]; tail += s * s; }
+#pragma unroll 8
+      for (int kk = rt - 1; kk >= 0; kk--) {
+        tail += ss[kk];
         if (tail <= thr) k = kk; else break;
       }
+      // never keep rounding-level singular values (sigma^2 <= delta^2): their
+      // Jacobi pairs are skipped, so their columns are not orthogonalised
+      // (binds only for eps below ~4 u sqrt(c); reading R7c)
+      while (k > 0 && !(ss[k - 1] > delta2)) k--;
     }
     s_rank = k;
     *J.rank = k;
   }
   __syncthreads();
   const int k = s_rank;
+  PHASE("rank");
   if (J.sigma)
     for (int i = tid; i < c; i += NT) J.sigma[i] = (i < rt) ? sig[order[i]] : 0.0;
+  for (int i = tid; i < k; i += NT) ss[i] = 1.0 / sig[order[i]];
+  __syncthreads();
   // ---------------------------------------------------------------- 4. factors
-  // permuted side:  out[perm[r], i] = W[r, order[i]] * f   (r < c), zero rows c..
-  // Q side:         out[:, i] = Q [V[:, order[i]] * g ; 0]   (L rows), zero rows L..
+  // permuted side (orthonormal): out[perm[r], i] = X[r, order[i]] / sigma_i  (r < c)
+  // Q side:  out[:, i] = Q [R X[:, order[i]] / sigma_i ; 0]  (= sigma_i u_i)
   double* Pout = tr ? J.Aout : J.Bout;
   const int Pld = tr ? J.lda : J.ldb, Prows = tr ? J.ma : J.nb;
   double* Qout = tr ? J.Bout : J.Aout;
@@ -314,31 +496,95 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
   }
   for (int64_t e = tid; e < (int64_t)c * k; e += NT) {
     const int r = (int)(e % c), i = (int)(e / c);
-    const int j = order[i];
-    const double f = (tr != (J.flip != 0)) ? 1.0 / sig[j] : 1.0;
-    Pout[perm[r] + (int64_t)i * Pld] = X[r + (int64_t)j * c] * f;
+    Pout[perm[r] + (int64_t)i * Pld] = X[r + (int64_t)order[i] * ldx] * ss[i];
   }
-  for (int i = warp; i < k; i += NW) {
-    const int j = order[i];
-    const double g = (tr != (J.flip != 0)) ? sig[j] : 1.0;
-    double* y = Qout + (int64_t)i * Qld;
-    for (int r = lane; r < Qrows; r += 32) y[r] = (r < rt) ? V[r + (int64_t)j * rt] * g : 0.0;
-    __syncwarp();
-    for (int jj = rt - 1; jj >= 0; jj--) {
-      const double t = tau[jj];
-      if (t == 0.0) continue;
-      const double* v = C + (int64_t)jj * L;
-      double d = 0.0;
-      for (int r = jj + 1 + lane; r < L; r += 32) d = fma(v[r], y[r], d);
-      d = (wsum(d) + y[jj]) * t;
-      if (lane == 0) y[jj] -= d;
-      for (int r = jj + 1 + lane; r < L; r += 32) y[r] -= d * v[r];
+  // Q side: one group of Gq lanes per output column; the column stays in
+  // registers (row gq + u Gq in slot u) while R u is formed and the rt
+  // reflectors are applied
+  const bool oreg = L <= kE * Gq;
+  for (int base = warp * gpwq; base < k; base += NW * gpwq) {
+    const int i = base + lane / Gq;
+    const bool act = i < k;
+    const int j = act ? order[i] : 0;
+    const double inv = act ? ss[i] : 0.0;
+    const double* w = X + (int64_t)j * ldx;
+    double* y = Qout + (int64_t)(act ? i : 0) * Qld;
+    if (oreg) {
+      double yr[kE];
+#pragma unroll
+      for (int u = 0; u < kE; u++) yr[u] = 0.0;
+      if (act)
+        for (int jj = 0; jj < c; jj++) {
+          const double xv = w[jj] * inv;
+          const double* rc = C + (int64_t)jj * ldc;
+#pragma unroll
+          for (int u = 0; u < kE; u++) {
+            const int r = gq + u * Gq;
+            if (r <= jj && r < rt) yr[u] = fma(rc[r], xv, yr[u]);
+          }
+        }
+      for (int jj = rt - 1; jj >= 0; jj--) {
+        const double t = tau[jj];
+        if (t == 0.0) continue;
+        const double* v = C + (int64_t)jj * ldc;
+        double d = 0.0, yj = 0.0;
+        const int uj = jj / Gq;
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int r = gq + u * Gq;
+          if (r > jj && r < L) d = fma(v[r], yr[u], d);
+          if (u == uj) yj = yr[u];
+        }
+        d = gsum(d, Gq);
+        yj = __shfl_sync(0xffffffffu, yj, (lane & ~(Gq - 1)) | (jj & (Gq - 1)));
+        d = (d + yj) * t;
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int r = gq + u * Gq;
+          if (r > jj && r < L) yr[u] = fma(-d, v[r], yr[u]);
+          else if (r == jj) yr[u] -= d;
+        }
+      }
+      if (act) {
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int r = gq + u * Gq;
+          if (r < L && r < Qrows) y[r] = yr[u];
+        }
+        for (int r = L + gq; r < Qrows; r += Gq) y[r] = 0.0;
+      }
+    } else {
+      if (act)
+        for (int r = gq; r < Qrows; r += Gq) {
+          double s = 0.0;
+          if (r < rt)
+            for (int jj = r; jj < c; jj++) s = fma(C[r + (int64_t)jj * ldc], w[jj] * inv, s);
+          y[r] = s;
+        }
       __syncwarp();
+      for (int jj = rt - 1; jj >= 0; jj--) {
+        const double t = tau[jj];
+        if (t == 0.0) continue;
+        const double* v = C + (int64_t)jj * ldc;
+        double d = 0.0;
+        if (act)
+          for (int r = jj + 1 + gq; r < L; r += Gq) d = fma(v[r], y[r], d);
+        d = gsum(d, Gq);
+        const double yj = act ? y[jj] : 0.0;
+        d = (d + yj) * t;
+        __syncwarp();
+        if (act) {
+          if (gq == 0) y[jj] = yj - d;
+          for (int r = jj + 1 + gq; r < L; r += Gq) y[r] -= d * v[r];
+        }
+        __syncwarp();
+      }
     }
   }
+  PHASE("output");
 }
 
-__global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
+__global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
   extern __shared__ double sm[];
   const SvdJob J = jobs[blockIdx.x];
   const int p = J.p, q = J.q;
@@ -350,11 +596,11 @@ __global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
     if (J.nsweep && tid == 0) *J.nsweep = 0;
     return;
   }
-  const int64_t need = (int64_t)L * c + 2 * (int64_t)c * c + 6 * (int64_t)c;
-  double* C = (need <= cap) ? sm : J.work;      // L x c, QRCP in place
-  double* X = C + (int64_t)L * c;               // c x rt   (R^T, then W = X V)
-  double* V = X + (int64_t)c * c;               // rt x rt  (rotations)
-  double* tau = V + (int64_t)c * c;             // c
+  const int ldc = pad_ld(L);
+  const int64_t need = svd_ws(L, c);
+  double* C = (need <= cap) ? sm : J.work;      // L x c (ld ldc), QRCP in place
+  double* X = C + (int64_t)ldc * c;             // c x rt  (R^T, then W)
+  double* tau = X + (int64_t)pad_ld(c) * c;     // c
   double* nrm = tau + c;                        // c
   double* sig = nrm + c;                        // c
   int* perm = reinterpret_cast<int*>(sig + c);  // c
@@ -362,67 +608,147 @@ __global__ void k_svd(const SvdJob* __restrict__ jobs, double eps, int cap) {
   for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
     const int i = (int)(e % L), j = (int)(e / L);
     const int mi = tr ? j : i, mj = tr ? i : j;   // entry (mi, mj) of M
-    C[e] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
+    C[i + (int64_t)j * ldc] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
   }
-  svd_core(J, eps, tr, L, c, C, X, V, tau, nrm, sig, perm, order);
+  svd_core(J, eps, tr, L, c, C, ldc, X, tau, nrm, sig, perm, order);
 }
 
-// In-place Householder QR (dgeqr2) of a rows x cols panel in shared memory.
-__device__ void house_qr_smem(double* A, int rows, int cols, double* tau) {
-  __shared__ double red[32];
-  __shared__ double s_tau, s_scale;
+// In-place Householder QR (dgeqr2 layout) of a rows x cols panel in shared
+// memory (ld lda), one barrier per column: nrm2[col] = ||A[j+1:, col]||^2 is
+// kept up to date by the update pass, every thread derives beta / tau itself,
+// groups of G lanes update one column each, and the scaling of the reflector
+// is deferred to the next step (all groups read it during its own step).
+__device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* tau, double* nrm2) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
-  for (int j = 0; j < cols && j < rows; j++) {
-    double* x = A + (int64_t)j * rows;
-    double pp = 0.0;
-    for (int i = j + 1 + tid; i < rows; i += NT) pp = fma(x[i], x[i], pp);
-    const double xn2 = bsum(pp, red);
-    if (tid == 0) {
-      const double alpha = x[j];
-      double t = 0.0, sc = 0.0, beta = alpha;
-      if (xn2 > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        t = (beta - alpha) / beta;
-        sc = 1.0 / (alpha - beta);
-      }
-      x[j] = beta;
-      tau[j] = t;
-      s_tau = t;
-      s_scale = sc;
-    }
-    __syncthreads();
-    const double t = s_tau, sc = s_scale;
-    if (t != 0.0) {
-      for (int i = j + 1 + tid; i < rows; i += NT) x[i] *= sc;
-      __syncthreads();
-      for (int c2 = j + 1 + warp; c2 < cols; c2 += NW) {
-        double* y = A + (int64_t)c2 * rows;
-        double d = 0.0;
-        for (int i = j + 1 + lane; i < rows; i += 32) d = fma(x[i], y[i], d);
-        d = (wsum(d) + y[j]) * t;
-        if (lane == 0) y[j] -= d;
-        for (int i = j + 1 + lane; i < rows; i += 32) y[i] -= d * x[i];
-      }
-    }
-    __syncthreads();
+  const int G = col_group(rows), gl = lane & (G - 1), gpw = 32 / G;
+  for (int base = warp * gpw; base < cols; base += NW * gpw) {
+    const int col = base + lane / G;
+    double s2 = 0.0;
+    if (col < cols)
+      for (int i = 1 + gl; i < rows; i += G) s2 = fma(A[i + (int64_t)col * lda], A[i + (int64_t)col * lda], s2);
+    s2 = gsum(s2, G);
+    if (col < cols && gl == 0) nrm2[col] = s2;
   }
+  __syncthreads();
+  int pending = -1;
+  double pbeta = 0.0, psc = 0.0, pt = 0.0;
+  const int steps = cols < rows ? cols : rows;
+  for (int j = 0; j < steps; j++) {
+    if (pending >= 0) {
+      double* xp = A + (int64_t)pending * lda;
+      if (pt != 0.0)
+        for (int i = pending + 1 + tid; i < rows; i += NT) xp[i] *= psc;
+      if (tid == 0) xp[pending] = pbeta;
+    }
+    const double* x = A + (int64_t)j * lda;
+    const double alpha = x[j], xn2 = nrm2[j];
+    double t = 0.0, sc = 0.0, beta = alpha;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      t = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) tau[j] = t;
+    const double tsc = t * sc;
+    for (int base = j + 1 + warp * gpw; base < cols; base += NW * gpw) {
+      const int col = base + lane / G;
+      const bool act = col < cols;
+      double* y = A + (int64_t)(act ? col : j) * lda;
+      double d = 0.0;
+      if (act && t != 0.0)
+        for (int i = j + 1 + gl; i < rows; i += G) d = fma(x[i], y[i], d);
+      d = gsum(d, G);
+      const double yj = act ? y[j] : 0.0;
+      d = t != 0.0 ? fma(tsc, d, t * yj) : 0.0;
+      const double ds = d * sc;
+      double nn2 = 0.0;
+      if (act)
+        for (int i = j + 1 + gl; i < rows; i += G) {
+          const double yi = fma(-ds, x[i], y[i]);
+          y[i] = yi;
+          if (i > j + 1) nn2 = fma(yi, yi, nn2);
+        }
+      nn2 = gsum(nn2, G);
+      __syncwarp();
+      if (act && gl == 0) { y[j] = yj - d; nrm2[col] = nn2; }
+    }
+    __syncthreads();
+    pending = j; pbeta = beta; psc = sc; pt = t;
+  }
+  if (pending >= 0) {
+    double* xp = A + (int64_t)pending * lda;
+    if (pt != 0.0)
+      for (int i = pending + 1 + tid; i < rows; i += NT) xp[i] *= psc;
+    if (tid == 0) xp[pending] = pbeta;
+  }
+  __syncthreads();
 }
 
-// X (rows x k, ld ldx, global) <- H_0 ... H_{r-1} X, reflectors in shared memory.
-__device__ void apply_q_smem(const double* Vr, const double* tau, int rows, int r, double* X, int ldx, int k) {
+// X (rows x k, ld ldx, global) <- H_0 ... H_{r-1} X, reflectors in shared
+// memory (ld ldv); one group of G lanes per column of X, the column held in
+// registers (row gl + u G in slot u) while the r reflectors are applied.
+__device__ void apply_q_smem(const double* Vr, int ldv, const double* tau, int rows, int r, double* X, int ldx,
+                             int k) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-  for (int col = warp; col < k; col += NW) {
-    double* x = X + (int64_t)col * ldx;
-    for (int j = r - 1; j >= 0; j--) {
-      const double t = tau[j];
-      if (t == 0.0) continue;
-      const double* v = Vr + (int64_t)j * rows;
-      double d = 0.0;
-      for (int i = j + 1 + lane; i < rows; i += 32) d = fma(v[i], x[i], d);
-      d = (wsum(d) + x[j]) * t;
-      if (lane == 0) x[j] -= d;
-      for (int i = j + 1 + lane; i < rows; i += 32) x[i] -= d * v[i];
-      __syncwarp();
+  const int G = col_group(rows), gl = lane & (G - 1), gpw = 32 / G;
+  const bool inreg = rows <= kE * G;
+  for (int base = warp * gpw; base < k; base += NW * gpw) {
+    const int col = base + lane / G;
+    const bool act = col < k;
+    double* x = X + (int64_t)(act ? col : 0) * ldx;
+    if (inreg) {
+      double xr[kE];
+#pragma unroll
+      for (int u = 0; u < kE; u++) {
+        const int i = gl + u * G;
+        xr[u] = (act && i < rows) ? x[i] : 0.0;
+      }
+      for (int j = r - 1; j >= 0; j--) {
+        const double t = tau[j];
+        if (t == 0.0) continue;
+        const double* v = Vr + (int64_t)j * ldv;
+        double d = 0.0, xj = 0.0;
+        const int uj = j / G;
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int i = gl + u * G;
+          if (i > j && i < rows) d = fma(v[i], xr[u], d);
+          if (u == uj) xj = xr[u];
+        }
+        d = gsum(d, G);
+        xj = __shfl_sync(0xffffffffu, xj, (lane & ~(G - 1)) | (j & (G - 1)));
+        d = (d + xj) * t;
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int i = gl + u * G;
+          if (i > j && i < rows) xr[u] = fma(-d, v[i], xr[u]);
+          else if (i == j) xr[u] -= d;
+        }
+      }
+      if (act)
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int i = gl + u * G;
+          if (i < rows) x[i] = xr[u];
+        }
+    } else {
+      for (int j = r - 1; j >= 0; j--) {
+        const double t = tau[j];
+        if (t == 0.0) continue;
+        const double* v = Vr + (int64_t)j * ldv;
+        double d = 0.0;
+        if (act)
+          for (int i = j + 1 + gl; i < rows; i += G) d = fma(v[i], x[i], d);
+        d = gsum(d, G);
+        const double xj = act ? x[j] : 0.0;
+        d = (d + xj) * t;
+        __syncwarp();
+        if (act) {
+          if (gl == 0) x[j] = xj - d;
+          for (int i = j + 1 + gl; i < rows; i += G) x[i] -= d * v[i];
+        }
+        __syncwarp();
+      }
     }
   }
 }
@@ -432,15 +758,15 @@ int trunc_small_need(int m, int n, int l) {
   if (n >= m) qb = l < n; else qa = l < m;
   if (m <= kNoQrRows && n <= kNoQrRows) qa = qb = 0;
   const int p = qa ? l : m, q = qb ? l : n;
-  const int64_t L = p > q ? p : q, c = p < q ? p : q;
-  const int64_t need = (int64_t)(m + n) * l + 2 * (int64_t)l + L * c + 2 * c * c + 6 * c;
+  const int L = p > q ? p : q, c = p < q ? p : q;
+  const int64_t need = (int64_t)(pad_ld(m) + pad_ld(n)) * l + 4 * (int64_t)l + svd_ws(L, c);
   return need > (1 << 30) ? (1 << 30) : (int)need;
 }
 
 // Fused TRUNC_eps of one small stack per CTA, everything in shared memory:
 // one-sided Householder QR, M = op(A) op(B)^T in its tall orientation, the
 // QRCP + Jacobi SVD of svd_core, then Q of the stack applied to the output.
-__global__ void k_trunc_small(const TruncSmallJob* __restrict__ jobs, double eps) {
+__global__ void __launch_bounds__(512) k_trunc_small(const TruncSmallJob* __restrict__ jobs, double eps) {
   extern __shared__ double sm[];
   const TruncSmallJob J = jobs[blockIdx.x];
   const int m = J.m, n = J.n, l = J.l, tid = threadIdx.x, NT = blockDim.x;
@@ -457,51 +783,80 @@ __global__ void k_trunc_small(const TruncSmallJob* __restrict__ jobs, double eps
     if (tid == 0) *J.rank = 0;
     return;
   }
+  const int lda = pad_ld(m), ldb = pad_ld(n), ldc = pad_ld(L);
   double* sA = sm;
-  double* sB = sA + (int64_t)m * l;
-  double* tA = sB + (int64_t)n * l;
+  double* sB = sA + (int64_t)lda * l;
+  double* tA = sB + (int64_t)ldb * l;
   double* tB = tA + l;
-  double* C = tB + l;
-  double* X = C + (int64_t)L * c;
-  double* V = X + (int64_t)c * c;
-  double* tau = V + (int64_t)c * c;
+  double* nA = tB + l;   // trailing column norms for the stack QRs
+  double* nB = nA + l;
+  double* C = nB + l;
+  double* X = C + (int64_t)ldc * c;
+  double* tau = X + (int64_t)pad_ld(c) * c;
   double* nrm = tau + c;
   double* sig = nrm + c;
   int* perm = reinterpret_cast<int*>(sig + c);
   int* order = perm + c;
-  for (int64_t e = tid; e < (int64_t)m * l; e += NT) sA[e] = J.A[e];
-  for (int64_t e = tid; e < (int64_t)n * l; e += NT) sB[e] = J.B[e];
+  PHASE_INIT;
+  for (int64_t e = tid; e < (int64_t)m * l; e += NT) sA[(e % m) + (e / m) * lda] = J.A[e];
+  for (int64_t e = tid; e < (int64_t)n * l; e += NT) sB[(e % n) + (e / n) * ldb] = J.B[e];
   __syncthreads();
-  if (qa) house_qr_smem(sA, m, l, tA);
-  if (qb) house_qr_smem(sB, n, l, tB);
-  // Mt = op(A) op(B)^T (tall) or op(B) op(A)^T
-  for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
-    const int i = (int)(e % L), j = (int)(e / L);
-    const int ia = tall ? i : j, ib = tall ? j : i;   // row of op(A), row of op(B)
-    double s = 0.0;
-    for (int k = 0; k < l; k++) {
-      const double a = (qa && ia > k) ? 0.0 : sA[ia + (int64_t)k * m];
-      const double b = (qb && ib > k) ? 0.0 : sB[ib + (int64_t)k * n];
-      s = fma(a, b, s);
+  PHASE("load");
+  if (qa) house_qr_smem(sA, m, lda, l, tA, nA);
+  if (qb) house_qr_smem(sB, n, ldb, l, tB, nB);
+  PHASE("stack_qr");
+  // Mt = F1 F2^T (L x c): F1 = op(A), F2 = op(B) if tall, else swapped; op() of
+  // a QR'd factor is its R (upper triangle, l rows).  4 x 4 register tiles.
+  {
+    const double* F1 = tall ? sA : sB;
+    const double* F2 = tall ? sB : sA;
+    const int ld1 = tall ? lda : ldb, ld2 = tall ? ldb : lda;
+    const bool mk1 = tall ? qa : qb, mk2 = tall ? qb : qa;
+    const int tl = (L + 3) >> 2, tc = (c + 3) >> 2;
+    for (int t = tid; t < tl * tc; t += NT) {
+      const int i0 = (t % tl) * 4, j0 = (t / tl) * 4;
+      double acc[4][4];
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int y = 0; y < 4; y++) acc[x][y] = 0.0;
+      for (int k = 0; k < l; k++) {
+        double a[4], b[4];
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+          const int i = i0 + x, j = j0 + x;
+          a[x] = (i < L && !(mk1 && i > k)) ? F1[i + (int64_t)k * ld1] : 0.0;
+          b[x] = (j < c && !(mk2 && j > k)) ? F2[j + (int64_t)k * ld2] : 0.0;
+        }
+#pragma unroll
+        for (int x = 0; x < 4; x++)
+#pragma unroll
+          for (int y = 0; y < 4; y++) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      }
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int y = 0; y < 4; y++)
+          if (i0 + x < L && j0 + y < c) C[(i0 + x) + (int64_t)(j0 + y) * ldc] = acc[x][y];
     }
-    C[e] = s;
   }
   __syncthreads();
+  PHASE("gemm_M");
   SvdJob S{};
   S.rank = J.rank;
   S.sigma = J.sigma;
-  S.flip = tall ? 0 : 1;
   S.Aout = tall ? J.Aout : J.Bout;
   S.lda = tall ? m : n;
   S.ma = S.lda;
   S.Bout = tall ? J.Bout : J.Aout;
   S.ldb = tall ? n : m;
   S.nb = S.ldb;
-  svd_core(S, eps, false, L, c, C, X, V, tau, nrm, sig, perm, order);
+  svd_core(S, eps, false, L, c, C, ldc, X, tau, nrm, sig, perm, order);
   __syncthreads();
   const int k = *J.rank;
-  if (qa) apply_q_smem(sA, tA, m, l, J.Aout, m, k);
-  if (qb) apply_q_smem(sB, tB, n, l, J.Bout, n, k);
+  if (qa) apply_q_smem(sA, lda, tA, m, l, J.Aout, m, k);
+  if (qb) apply_q_smem(sB, ldb, tB, n, l, J.Bout, n, k);
+  PHASE("apply_q");
 }
 
 void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
@@ -516,7 +871,9 @@ void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int 
   // free, and many stacks share an SM); larger: 128 / 256 threads
   // (measured on B200: 32 or 128 threads for the small buckets is slower --
   // the L x c loops lose more than the cheaper barriers gain)
-  const int threads = 256;
+  // few stacks (latency-bound, e.g. the H-LR critical path): 512 threads so
+  // every Jacobi pair of a round is in flight; many stacks: 256 (two CTAs/SM)
+  const int threads = njobs < 296 ? 512 : 256;
   k_trunc_small<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps);
 }
 
@@ -530,7 +887,7 @@ void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream
     attr = true;
   }
   if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
-  const int threads = (cap == 0 || cap > 8 * 1024) ? 512 : 256;
+  const int threads = (cap == 0 || cap > 8 * 1024 || njobs < 296) ? 512 : 256;
   count_launch();
   k_svd<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, cap);
 }
