@@ -233,7 +233,10 @@ __global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jo
       double w[16];
 #pragma unroll
       for (int q = 0; q < 16; q++) w[q] = 0.0;
-      for (int i = j0 + lane; i < J.m; i += 32) {
+      // the 16 reflector rows beyond the panel's unit triangle, 2 rows per
+      // lane per step (34 loads in flight)
+      int i = j0 + lane;
+      for (; i < j0 + 16 && i < J.m; i += 32) {
         const double xi = x[i];
 #pragma unroll
         for (int q = 0; q < 16; q++)
@@ -241,6 +244,22 @@ __global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jo
             const double y = i > j0 + q ? Vp[i + (int64_t)q * J.ldv] : (i == j0 + q ? 1.0 : 0.0);
             w[q] = fma(y, xi, w[q]);
           }
+      }
+      for (; i + 32 < J.m; i += 64) {
+        const double xa = x[i], xb = x[i + 32];
+        double va[16], vb[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+          if (q < kb) { va[q] = Vp[i + (int64_t)q * J.ldv]; vb[q] = Vp[i + 32 + (int64_t)q * J.ldv]; }
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+          if (q < kb) w[q] = fma(vb[q], xb, fma(va[q], xa, w[q]));
+      }
+      for (; i < J.m; i += 32) {
+        const double xi = x[i];
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+          if (q < kb) w[q] = fma(Vp[i + (int64_t)q * J.ldv], xi, w[q]);
       }
 #pragma unroll
       for (int q = 0; q < 16; q++) w[q] = warp_sum(w[q]);
@@ -254,7 +273,8 @@ __global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jo
           if (r < kb) s = fma(Tp[q + r * 16], w[r], s);
         z[q] = s;
       }
-      for (int i = j0 + lane; i < J.m; i += 32) {
+      i = j0 + lane;
+      for (; i < j0 + 16 && i < J.m; i += 32) {
         double s = 0.0;
 #pragma unroll
         for (int q = 0; q < 16; q++)
@@ -262,6 +282,25 @@ __global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jo
             const double y = i > j0 + q ? Vp[i + (int64_t)q * J.ldv] : (i == j0 + q ? 1.0 : 0.0);
             s = fma(y, z[q], s);
           }
+        x[i] -= s;
+      }
+      for (; i + 32 < J.m; i += 64) {
+        const double xa = x[i], xb = x[i + 32];
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+          if (q < kb) {
+            sa = fma(Vp[i + (int64_t)q * J.ldv], z[q], sa);
+            sb = fma(Vp[i + 32 + (int64_t)q * J.ldv], z[q], sb);
+          }
+        x[i] = xa - sa;
+        x[i + 32] = xb - sb;
+      }
+      for (; i < J.m; i += 32) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+          if (q < kb) s = fma(Vp[i + (int64_t)q * J.ldv], z[q], s);
         x[i] -= s;
       }
       __syncwarp();

@@ -164,12 +164,28 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
       double w0[kNbMax], w1[kNbMax];
 #pragma unroll
       for (int q = 0; q < kNbMax; q++) w0[q] = w1[q] = 0.0;
-      for (int i = lane; i < rows; i += 32) {
+      // rows in blocks of 4 per lane: 8 global loads in flight per lane
+      int i = lane;
+      for (; i + 96 < rows; i += 128) {
+        double x0[4], x1[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) { x0[u] = a0[i + 32 * u]; x1[u] = a1[i + 32 * u]; }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int q = 0; q < kNbMax; q++)
+            if (q < kb) {
+              const double v = Vs[i + 32 * u + q * rows];
+              w0[q] = fma(v, x0[u], w0[q]);
+              w1[q] = fma(v, x1[u], w1[q]);
+            }
+      }
+      for (; i < rows; i += 32) {
         const double x0 = a0[i], x1 = a1[i];
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
           if (q < kb) {
-            const double v = Vs[i + (int64_t)q * rows];
+            const double v = Vs[i + q * rows];
             w0[q] = fma(v, x0, w0[q]);
             w1[q] = fma(v, x1, w1[q]);
           }
@@ -190,12 +206,36 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
         w0[q] = s0;
         w1[q] = s1;
       }
-      for (int i = lane; i < rows; i += 32) {
+      i = lane;
+      for (; i + 96 < rows; i += 128) {
+        double x0[4], x1[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) { x0[u] = a0[i + 32 * u]; x1[u] = a1[i + 32 * u]; }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < kNbMax; q++)
+            if (q < kb) {
+              const double v = Vs[i + 32 * u + q * rows];
+              s0 = fma(v, w0[q], s0);
+              s1 = fma(v, w1[q], s1);
+            }
+          x0[u] -= s0;
+          x1[u] -= s1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          a0[i + 32 * u] = x0[u];
+          if (two) a1[i + 32 * u] = x1[u];
+        }
+      }
+      for (; i < rows; i += 32) {
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
           if (q < kb) {
-            const double v = Vs[i + (int64_t)q * rows];
+            const double v = Vs[i + q * rows];
             s0 = fma(v, w0[q], s0);
             s1 = fma(v, w1[q], s1);
           }
