@@ -10,10 +10,26 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 
 namespace hm {
+
+#ifdef HM_PHASE_TIMING
+#define QT_INIT long long qt0 = clock64(), qt_panel = 0, qt_t = 0, qt_trail = 0
+#define QT_MARK(acc)                        \
+  do {                                      \
+    __syncthreads();                        \
+    const long long t_ = clock64();         \
+    acc += t_ - qt0;                        \
+    qt0 = t_;                               \
+  } while (0)
+#else
+#define QT_INIT do {} while (0)
+#define QT_MARK(acc) do {} while (0)
+#endif
 
 namespace {
 constexpr int kNbMax = 16;
@@ -39,6 +55,7 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
   int nb = kNbMax;
   while (nb > 1 && (int64_t)m * nb > cap) nb >>= 1;
+  QT_INIT;
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int kb = min(nb, n - k0);
     const int rows = m - k0;
@@ -69,19 +86,48 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
       }
       double* rb = red2 + (j & 1) * (16 * kNbMax);
       double* pv = piv + (j & 1) * kNbMax;
+      // warp reduce-scatter of the 16 slots (16 shuffles instead of 80): after
+      // the xor-16/8/4/2 halvings lane L holds slot L >> 1 summed over its
+      // half-warp partners, the xor-1 step completes it
+      {
+        double h8[8], h4[4], h2[2];
+        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
 #pragma unroll
-      for (int q = 0; q < kNbMax; q++)
-        if (q < nc) {
-          const double s = wsum(part[q]);
-          if (lane == 0) rb[warp * kNbMax + q] = s;
+        for (int q = 0; q < 8; q++) {
+          const double send = b4 ? part[q] : part[q + 8];
+          h8[q] = (b4 ? part[q + 8] : part[q]) + __shfl_xor_sync(0xffffffffu, send, 16);
         }
-      if (tid == j % NT)
-        for (int q = 0; q < nc; q++) pv[q] = Vs[j + (int64_t)(j + q) * rows];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const double send = b3 ? h8[q] : h8[q + 4];
+          h4[q] = (b3 ? h8[q + 4] : h8[q]) + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const double send = b2 ? h4[q] : h4[q + 2];
+          h2[q] = (b2 ? h4[q + 2] : h4[q]) + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        const double send = b1 ? h2[0] : h2[1];
+        double h1 = (b1 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+        const int slot = (b4 ? 8 : 0) + (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+        if ((lane & 1) == 0 && slot < nc) rb[warp * kNbMax + slot] = h1;
+      }
+      if (tid == j % NT) {
+#pragma unroll
+        for (int q = 0; q < kNbMax; q++)
+          if (q < nc) pv[q] = Vs[j + (int64_t)(j + q) * rows];
+      }
       __syncthreads();
-      // lane q of every warp totals slot q over the warps
+      // lane q of every warp totals slot q over the warps (loads issued together)
       double tq = 0.0;
-      if (lane < nc)
-        for (int w = 0; w < NW; w++) tq += rb[w * kNbMax + lane];
+      if (lane < nc) {
+        double r16[16];
+#pragma unroll
+        for (int w = 0; w < 16; w++) r16[w] = w < NW ? rb[w * kNbMax + lane] : 0.0;
+#pragma unroll
+        for (int w = 0; w < 16; w++) tq += r16[w];
+      }
       const double xn2 = __shfl_sync(0xffffffffu, tq, 0);
       const double alpha = pv[0];
       double t = 0.0, sc = 0.0, beta = alpha;
@@ -125,6 +171,7 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
       else if (i == j) Vs[i + (int64_t)j * rows] = 1.0;
     }
     __syncthreads();
+    QT_MARK(qt_panel);
     const int ncol = n - k0 - kb;
     const bool wantT = J.T != nullptr && nb == kNbMax;   // panel factors for k_applyq
     if (ncol <= 0 && !wantT) continue;
@@ -154,6 +201,7 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
     __syncthreads();
     if (wantT)
       for (int e = tid; e < kNbMax * kNbMax; e += NT) J.T[(int64_t)(k0 / kNbMax) * kNbMax * kNbMax + e] = T[e];
+    QT_MARK(qt_t);
     if (ncol <= 0) continue;
     // 5. trailing update, one warp per PAIR of columns (each V element read
     //    from shared memory feeds two FMAs): a <- a - V (T^T (V^T a))
@@ -244,7 +292,12 @@ __global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__
       }
     }
     __syncthreads();
+    QT_MARK(qt_trail);
   }
+#ifdef HM_PHASE_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("[qr] m=%d n=%d nb=%d panel %lld T %lld trailing %lld cycles\n", m, n, nb, qt_panel, qt_t, qt_trail);
+#endif
 }
 
 void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
@@ -256,7 +309,9 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
   }
   if (cap > 24 * 1024) cap = 24 * 1024;
   count_launch();
-  k_qr_blocked<<<njobs, cap <= 6 * 1024 ? 256 : 512, (size_t)cap * 8, st>>>(d_jobs, cap);
+  static const int thr = [] { const char* e = std::getenv("HM_QR_THREADS"); return e ? std::atoi(e) : 0; }();
+  const int threads = thr > 0 ? thr : (cap <= 6 * 1024 ? 256 : 512);
+  k_qr_blocked<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, cap);
 }
 
 }  // namespace hm
