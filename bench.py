@@ -210,6 +210,7 @@ def run_ours(args, cfg):
 
     def step(i):
         hm.addmul(1.0, X, Y, Zs[i], cfg["eps"])
+        Zs[i].free()     # the product is consumed; its memory returns to the pool
 
     for i in range(args.warmup):
         step(i)
