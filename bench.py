@@ -243,6 +243,15 @@ def run_ours(args, cfg):
 
     # ---- end to end through the C-ABI with host buffers
     dX, dY, dZ = X.export(), Y.export(), G.export()
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    for d_ in (dX, dY, dZ):   # the step's inputs live in pinned host memory
+        d_["factors"] = pinned(d_["factors"])
+        d_["dense"] = pinned(d_["dense"])
     h2d = sum(int(d["factors"].nbytes + d["dense"].nbytes) for d in (dX, dY, dZ))
     e2e_steps = max(1, min(args.steps, 2))
     torch.cuda.synchronize(dev)

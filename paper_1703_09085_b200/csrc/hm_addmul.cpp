@@ -348,7 +348,9 @@ struct Planner {
       std::stable_sort(ej.begin(), ej.end(),
                        [](const EvalJob& a, const EvalJob& b) { return a.cost > b.cost; });
       ProfScope ps(c, PC_EVAL, fl_eval - fl_eval0, by_eval - by_eval0);
-      launch_eval(scratch.upload(ej), (int)ej.size(), c->stream);
+      static const bool old_eval = std::getenv("HM_EVAL_OLD") != nullptr;
+      if (old_eval) launch_eval(scratch.upload(ej), (int)ej.size(), c->stream);
+      else launch_eval2(scratch.upload(ej), (int)ej.size(), c->stream);
       HM_CHECK_LAUNCH();
     }
     // truncations and dense adds
@@ -691,6 +693,12 @@ struct Planner {
 // (reduce = T1, flush into a leaf incl. temporaries + rkmerge, addproduct)
 // goes through the Planner above, triangular solves through the H-structure
 // run as one k_trsm CTA per panel, dense diagonal leaves as k_leaf_factor.
+static void trsm_launch(const TrsmJob* j, int n, const TrsmStep* st, const LeafDesc* lv, cudaStream_t s) {
+  static const bool old_trsm = std::getenv("HM_TRSM_OLD") != nullptr;
+  if (old_trsm) launch_trsm(j, n, st, lv, s);
+  else launch_trsm2(j, n, st, lv, s);
+}
+
 struct Factorizer {
   Ctx* c;
   Mat* G;
@@ -704,7 +712,7 @@ struct Factorizer {
   std::unordered_map<int64_t, int> bmap;       // (row, col) -> block id
   int* d_fail = nullptr;
   double* d_minpiv = nullptr;
-  int64_t n_trsm = 0, n_leaf = 0, n_flush = 0;
+  int64_t n_trsm = 0, n_leaf = 0, n_flush = 0, n_flush_calls = 0, n_reduce_calls = 0;
 
   Factorizer(Ctx* c_, Mat* G_, double eps, bool ch)
       : c(c_), G(G_), T(*G_->tree), chol(ch), P(c_, *G_->tree, G_, G_, G_, -1.0, eps) {
@@ -770,6 +778,7 @@ struct Factorizer {
   void flush_many(std::vector<Node> roots) {
     if (roots.empty()) return;
     n_flush += (int64_t)roots.size();
+    n_flush_calls++;
     Arena local(c, true);
     P.fp_arena = &local;
     std::vector<int> zbs;
@@ -821,6 +830,7 @@ struct Factorizer {
       who.push_back(nd);
     }
     if (batch.empty()) return;
+    n_reduce_calls++;
     P.run_level(batch);
     for (size_t i = 0; i < who.size(); i++) who[i]->red = batch[i].red;
   }
@@ -868,7 +878,7 @@ struct Factorizer {
     else steps_lower(t, mode == 0, T.cl_start[t], st);
     Arena ar(c);
     std::vector<TrsmJob> jb{TrsmJob{V, ldv, ncols, T.cl_start[t], 0, (int)st.size()}};
-    launch_trsm(ar.upload(jb), 1, ar.upload(st), dlt, c->stream);
+    trsm_launch(ar.upload(jb), 1, ar.upload(st), dlt, c->stream);
     HM_CHECK_LAUNCH();
   }
 
@@ -941,7 +951,7 @@ struct Factorizer {
     n_trsm += (int64_t)jobs.size();
     ProfScope ps(c, PC_TRSM, 0, 0);
     if (!pre.empty()) launch_copy(ar.upload(pre), (int)pre.size(), pt, c->stream);
-    if (!jobs.empty()) launch_trsm(ar.upload(jobs), (int)jobs.size(), ar.upload(st), dlt, c->stream);
+    if (!jobs.empty()) trsm_launch(ar.upload(jobs), (int)jobs.size(), ar.upload(st), dlt, c->stream);
     if (!post.empty()) launch_copy(ar.upload(post), (int)post.size(), qt, c->stream);
     HM_CHECK_LAUNCH();
   }
@@ -1161,9 +1171,9 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
   F.finish(min_pivot);
   if (std::getenv("HM_DEBUG_TIMING"))
     std::fprintf(stderr,
-                 "[hm_factor] flushes %lld trsm %lld leaf %lld syncs %lld | planner: levels %.3fs (sync wait %.3fs; host "
+                 "[hm_factor] flushes %lld (calls %lld, reduce calls %lld) trsm %lld leaf %lld syncs %lld | planner: levels %.3fs (sync wait %.3fs; host "
                  "layout %.3f jobs %.3f launch %.3f trunc %.3f) split %.3fs merges %.3fs\n",
-                 (long long)F.n_flush, (long long)F.n_trsm, (long long)F.n_leaf, (long long)F.P.n_sync, F.P.t_level, F.P.t_wait,
+                 (long long)F.n_flush, (long long)F.n_flush_calls, (long long)F.n_reduce_calls, (long long)F.n_trsm, (long long)F.n_leaf, (long long)F.P.n_sync, F.P.t_level, F.P.t_wait,
                  F.P.t_a, F.P.t_b, F.P.t_c, F.P.t_d, F.P.t_split, F.P.t_merge);
   hm_stats_t& s = c->last;
   s.addproduct_calls = F.P.n_addproduct;

@@ -99,25 +99,44 @@ void upload_payload(Ctx& c, Mat& M, const hm_host_desc* d) {
   M.fpool = {fp, (nf + 1) * sizeof(double)};
   double* dp = static_cast<double*>(c.dmalloc((nd + 1) * sizeof(double)));
   M.dpool = {dp, (nd + 1) * sizeof(double)};
-  // repack in block order
-  std::vector<double> hf(nf), hd(nd);
+  // payload in block order and contiguous (what hm_export writes): one bulk
+  // copy per pool; otherwise repack on the host first
+  bool fcont = true, dcont = true;
+  {
+    int64_t of = 0, od = 0;
+    for (int b = 0; b < nb; b++) {
+      const int64_t m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
+      if (T.bl_kind[b] == HM_BLOCK_ADM) {
+        if (M.rank[b] > 0 && d->bl_off[b] != of) fcont = false;
+        of += (m + n) * M.rank[b];
+      } else if (T.bl_kind[b] == HM_BLOCK_DENSE) {
+        if (d->bl_off[b] != od) dcont = false;
+        od += m * n;
+      }
+    }
+  }
+  std::vector<double> hf, hd;
+  if (!fcont) hf.resize(nf);
+  if (!dcont) hd.resize(nd);
   size_t of = 0, od = 0;
   for (int b = 0; b < nb; b++) {
     const int64_t m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
     if (T.bl_kind[b] == HM_BLOCK_ADM) {
       const int k = M.rank[b];
-      std::memcpy(hf.data() + of, d->factors + d->bl_off[b], sizeof(double) * (m + n) * k);
+      if (!fcont) std::memcpy(hf.data() + of, d->factors + d->bl_off[b], sizeof(double) * (m + n) * k);
       M.pA[b] = fp + of;
       M.pB[b] = fp + of + m * k;
       of += (m + n) * k;
     } else if (T.bl_kind[b] == HM_BLOCK_DENSE) {
-      std::memcpy(hd.data() + od, d->dense + d->bl_off[b], sizeof(double) * m * n);
+      if (!dcont) std::memcpy(hd.data() + od, d->dense + d->bl_off[b], sizeof(double) * m * n);
       M.pA[b] = dp + od;
       od += m * n;
     }
   }
-  if (nf) HM_CUDA(cudaMemcpyAsync(fp, hf.data(), nf * sizeof(double), cudaMemcpyHostToDevice, c.stream));
-  if (nd) HM_CUDA(cudaMemcpyAsync(dp, hd.data(), nd * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  if (nf)
+    HM_CUDA(cudaMemcpyAsync(fp, fcont ? d->factors : hf.data(), nf * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  if (nd)
+    HM_CUDA(cudaMemcpyAsync(dp, dcont ? d->dense : hd.data(), nd * sizeof(double), cudaMemcpyHostToDevice, c.stream));
   HM_CUDA(cudaStreamSynchronize(c.stream));
 }
 }  // namespace
@@ -214,18 +233,53 @@ hm_status hm_export(hm_ctx ctx, hm_mat mat, hm_host_desc* d) {
         nd += (size_t)m * n;
       }
     }
-    M.ex_factors.assign(nf, 0.0);
-    M.ex_dense.assign(nd, 0.0);
-    HM_CUDA(cudaStreamSynchronize(ctx->c.stream));
-    for (int b = 0; b < nb; b++) {
-      const int64_t m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
-      if (T.bl_kind[b] == HM_BLOCK_ADM && M.rank[b] > 0) {
-        const int k = M.rank[b];
-        HM_CUDA(cudaMemcpy(M.ex_factors.data() + M.ex_off[b], M.pA[b], sizeof(double) * m * k, cudaMemcpyDeviceToHost));
-        HM_CUDA(cudaMemcpy(M.ex_factors.data() + M.ex_off[b] + m * k, M.pB[b], sizeof(double) * n * k, cudaMemcpyDeviceToHost));
-      } else if (T.bl_kind[b] == HM_BLOCK_DENSE) {
-        HM_CUDA(cudaMemcpy(M.ex_dense.data() + M.ex_off[b], M.pA[b], sizeof(double) * m * n, cudaMemcpyDeviceToHost));
+    M.ex_factors.reset(new double[nf + 1]);
+    M.ex_dense.reset(new double[nd + 1]);
+    // gather the blocks into export order on the device (one batched copy per
+    // pool), then one bulk D2H per pool
+    {
+      Arena ar(&ctx->c);
+      double* gf = nf ? ar.alloc(nf) : nullptr;
+      double* gd = nd ? ar.alloc(nd) : nullptr;
+      std::vector<CopyJob> cj;
+      int64_t tiles = 0;
+      auto add = [&](double* dst, const double* src, int64_t cnt) {
+        // a contiguous run of cnt doubles as a (1024 x ceil) column block
+        const int rows = 1024;
+        const int cols = (int)((cnt + rows - 1) / rows);
+        const int full = (int)(cnt / rows);
+        if (full > 0) {
+          CopyJob j{};
+          j.dst = dst; j.src = src; j.ldd = rows; j.lds = rows; j.rows = rows; j.cols = full;
+          j.coef = 1.0; j.tile0 = tiles;
+          tiles += (int64_t)(rows / 32) * ((full + 31) / 32);
+          cj.push_back(j);
+        }
+        if (cols > full) {
+          CopyJob j{};
+          const int64_t off = (int64_t)full * rows;
+          j.dst = dst + off; j.src = src + off; j.ldd = rows; j.lds = rows; j.rows = (int)(cnt - off); j.cols = 1;
+          j.coef = 1.0; j.tile0 = tiles;
+          tiles += (int64_t)((j.rows + 31) / 32);
+          cj.push_back(j);
+        }
+      };
+      for (int b = 0; b < nb; b++) {
+        const int64_t m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
+        if (T.bl_kind[b] == HM_BLOCK_ADM && M.rank[b] > 0) {
+          const int64_t k = M.rank[b];
+          add(gf + M.ex_off[b], M.pA[b], m * k);
+          add(gf + M.ex_off[b] + m * k, M.pB[b], n * k);
+        } else if (T.bl_kind[b] == HM_BLOCK_DENSE) {
+          add(gd + M.ex_off[b], M.pA[b], m * n);
+        }
       }
+      if (!cj.empty()) launch_copy(ar.upload(cj), (int)cj.size(), tiles, ctx->c.stream);
+      HM_CHECK_LAUNCH();
+      if (nf) HM_CUDA(cudaMemcpyAsync(M.ex_factors.get(), gf, nf * sizeof(double), cudaMemcpyDeviceToHost, ctx->c.stream));
+      if (nd) HM_CUDA(cudaMemcpyAsync(M.ex_dense.get(), gd, nd * sizeof(double), cudaMemcpyDeviceToHost, ctx->c.stream));
+      HM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+      ar.release();
     }
     std::memset(d, 0, sizeof(*d));
     d->n = T.n;
@@ -244,9 +298,9 @@ hm_status hm_export(hm_ctx ctx, hm_mat mat, hm_host_desc* d) {
     d->bl_nsons = T.bl_nsons.data();
     d->bl_rank = M.ex_rank.data();
     d->bl_off = M.ex_off.data();
-    d->factors = M.ex_factors.data();
+    d->factors = M.ex_factors.get();
     d->nfactors = (int64_t)nf;
-    d->dense = M.ex_dense.data();
+    d->dense = M.ex_dense.get();
     d->ndense = (int64_t)nd;
     d->perm = T.perm.empty() ? nullptr : T.perm.data();
   });

@@ -157,7 +157,7 @@ struct Mat {
   // export staging
   std::vector<int32_t> ex_rank;
   std::vector<int64_t> ex_off;
-  std::vector<double> ex_factors, ex_dense;
+  std::unique_ptr<double[]> ex_factors, ex_dense;   // export buffers (uninitialised, owned)
   // geometry kept by hm_build (for diagnostics)
   int kernel = 0;
   void free_all(Ctx* c);

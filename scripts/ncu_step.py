@@ -1,14 +1,31 @@
 """One hm_addmul step (config 4) bracketed by cudaProfilerStart/Stop, for
-`ncu --profile-from-start off` launch lists / full captures of the bench step."""
+`ncu --profile-from-start off` launch lists / full captures of the bench step.
+
+    python scripts/ncu_step.py save PATH     build config 4 and save its host description
+    python scripts/ncu_step.py load PATH     import it (no build kernels: ncu's per-launch
+                                             overhead would otherwise dominate), warm-up step,
+                                             then ONE profiled step
+"""
 import sys
 sys.path.insert(0, '.')
+import numpy as np
 import torch
 import paper_1703_09085_b200 as hm
 from hm_inputs import sphere_points
-L, leaf, eps = (int(sys.argv[1]), int(sys.argv[2]), float(sys.argv[3])) if len(sys.argv) > 3 else (6, 64, 1e-6)
+mode, path = sys.argv[1], sys.argv[2]
+L, leaf, eps = 6, 64, 1e-6
 ctx = hm.Context(0)
-x, w = sphere_points(L)
-G = ctx.build(x, w, leaf, 2.0, eps)
+if mode == "save":
+    x, w = sphere_points(L)
+    G = ctx.build(x, w, leaf, 2.0, eps)
+    d = G.export()
+    np.savez(path, **{k: v for k, v in d.items() if v is not None})
+    print("saved", path)
+    sys.exit(0)
+z = np.load(path)
+d = {k: z[k] for k in z.files}
+d["perm"] = d.get("perm")
+G = ctx.import_desc(d)
 X, Y = G.clone(), G.clone()
 Z = G.clone()
 hm.addmul(1.0, X, Y, Z, eps)          # warm-up (pools, caches)
@@ -20,4 +37,4 @@ torch.cuda.profiler.start()
 hm.addmul(1.0, X, Y, Z, eps)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("launches in step:", ctx.last_stats()["kernel_launches"])
+print("launches after step:", ctx.last_stats()["kernel_launches"], flush=True)
