@@ -166,6 +166,17 @@ hm_status hm_build(hm_ctx ctx, const double* pts_host, const double* area_host, 
 hm_status hm_import(hm_ctx ctx, const hm_host_desc* d, hm_mat* out);
 /* hm_export: download; pointers in *d owned by the matrix (see above). */
 hm_status hm_export(hm_ctx ctx, hm_mat m, hm_host_desc* d);
+
+/* hm_export_sizes: payload sizes (doubles) hm_export / hm_export_into produce. */
+hm_status hm_export_sizes(hm_ctx ctx, hm_mat m, int64_t* nfactors, int64_t* ndense);
+
+/* hm_export_into: as hm_export, but the factor / dense payloads are copied
+ * straight into CALLER-owned host buffers factors_out (nfactors doubles) and
+ * dense_out (ndense doubles) -- one bulk D2H per pool, no library-side host
+ * copy (pinned buffers give full DMA bandwidth).  d->factors / d->dense are
+ * set to those buffers; the other arrays of *d are owned by the matrix as for
+ * hm_export.  HM_EINVAL if a buffer is null while its size is non-zero. */
+hm_status hm_export_into(hm_ctx ctx, hm_mat m, hm_host_desc* d, double* factors_out, double* dense_out);
 hm_status hm_clone(hm_ctx ctx, hm_mat src, hm_mat* out);
 hm_status hm_free(hm_ctx ctx, hm_mat m);
 

@@ -177,9 +177,24 @@ class HMatrix:
         self.ctx.check(lib().hm_stats(self.ctx.h, self.h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in _lib.Stats._fields_}
 
-    def export(self):
+    def export(self, pinned=False):
+        """Host description (dict of numpy arrays).  The payloads are written by
+        the library straight into freshly allocated arrays (hm_export_into);
+        pinned=True allocates them in page-locked memory (full-bandwidth D2H)."""
+        import torch
+        nf, nd = C.c_int64(), C.c_int64()
+        self.ctx.check(lib().hm_export_sizes(self.ctx.h, self.h, C.byref(nf), C.byref(nd)))
+
+        def buf(cnt):
+            if pinned:
+                return torch.empty(max(cnt, 1), dtype=torch.float64, pin_memory=True).numpy()[:cnt]
+            return np.empty(cnt, np.float64)
+
+        fbuf, dbuf = buf(nf.value), buf(nd.value)
         hd = _lib.HostDesc()
-        self.ctx.check(lib().hm_export(self.ctx.h, self.h, C.byref(hd)))
+        self.ctx.check(lib().hm_export_into(self.ctx.h, self.h, C.byref(hd),
+                                            C.c_void_p(fbuf.ctypes.data) if nf.value else None,
+                                            C.c_void_p(dbuf.ctypes.data) if nd.value else None))
         nc, nb = hd.nclusters, hd.nblocks
 
         def cp(p, cnt, dt):
@@ -194,8 +209,8 @@ class HMatrix:
         for k in ("bl_row", "bl_col", "bl_kind", "bl_son0", "bl_nsons", "bl_rank"):
             d[k] = cp(getattr(hd, k), nb, np.int32)
         d["bl_off"] = cp(hd.bl_off, nb, np.int64)
-        d["factors"] = cp(hd.factors, hd.nfactors, np.float64)
-        d["dense"] = cp(hd.dense, hd.ndense, np.float64)
+        d["factors"] = fbuf
+        d["dense"] = dbuf
         d["perm"] = cp(hd.perm, hd.n, np.int64) if hd.perm else None
         return d
 

@@ -64,7 +64,7 @@ class Prof(C.Structure):
 
 EXPORTS = [
     "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_build",
-    "hm_import", "hm_export", "hm_clone", "hm_free", "hm_addmul", "hm_lr", "hm_chol",
+    "hm_import", "hm_export", "hm_export_sizes", "hm_export_into", "hm_clone", "hm_free", "hm_addmul", "hm_lr", "hm_chol",
     "hm_matvec_thin", "hm_stats", "hm_profile_enable", "hm_profile_reset", "hm_profile_get",
     "hm_test_trunc_batched",
 ]
@@ -87,6 +87,8 @@ def load(path: str = LIB_PATH):
                                C.POINTER(vp), P_i64]),
         "hm_import": (C.c_int, [vp, C.POINTER(HostDesc), C.POINTER(vp)]),
         "hm_export": (C.c_int, [vp, vp, C.POINTER(HostDesc)]),
+        "hm_export_sizes": (C.c_int, [vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "hm_export_into": (C.c_int, [vp, vp, C.POINTER(HostDesc), vp, vp]),
         "hm_clone": (C.c_int, [vp, vp, C.POINTER(vp)]),
         "hm_free": (C.c_int, [vp, vp]),
         "hm_addmul": (C.c_int, [vp, C.c_double, vp, vp, vp, C.c_double]),

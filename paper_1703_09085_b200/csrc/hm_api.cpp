@@ -212,9 +212,8 @@ hm_status hm_import(hm_ctx ctx, const hm_host_desc* d, hm_mat* out) {
   });
 }
 
-hm_status hm_export(hm_ctx ctx, hm_mat mat, hm_host_desc* d) {
-  if (!ctx || !mat || !d) return HM_EINVAL;
-  return guard(ctx, [&] {
+static void export_impl(hm_ctx ctx, hm_mat mat, hm_host_desc* d, double* fout, double* dout, bool user) {
+  {
     set_device(ctx->c);
     Mat& M = mat->m;
     const Tree& T = *M.tree;
@@ -233,8 +232,14 @@ hm_status hm_export(hm_ctx ctx, hm_mat mat, hm_host_desc* d) {
         nd += (size_t)m * n;
       }
     }
-    M.ex_factors.reset(new double[nf + 1]);
-    M.ex_dense.reset(new double[nd + 1]);
+    if (user) {
+      if ((nf && !fout) || (nd && !dout)) throw Error(HM_EINVAL, "hm_export_into: null payload buffer");
+    } else {
+      M.ex_factors.reset(new double[nf + 1]);
+      M.ex_dense.reset(new double[nd + 1]);
+      fout = M.ex_factors.get();
+      dout = M.ex_dense.get();
+    }
     // gather the blocks into export order on the device (one batched copy per
     // pool), then one bulk D2H per pool
     {
@@ -276,8 +281,8 @@ hm_status hm_export(hm_ctx ctx, hm_mat mat, hm_host_desc* d) {
       }
       if (!cj.empty()) launch_copy(ar.upload(cj), (int)cj.size(), tiles, ctx->c.stream);
       HM_CHECK_LAUNCH();
-      if (nf) HM_CUDA(cudaMemcpyAsync(M.ex_factors.get(), gf, nf * sizeof(double), cudaMemcpyDeviceToHost, ctx->c.stream));
-      if (nd) HM_CUDA(cudaMemcpyAsync(M.ex_dense.get(), gd, nd * sizeof(double), cudaMemcpyDeviceToHost, ctx->c.stream));
+      if (nf) HM_CUDA(cudaMemcpyAsync(fout, gf, nf * sizeof(double), cudaMemcpyDeviceToHost, ctx->c.stream));
+      if (nd) HM_CUDA(cudaMemcpyAsync(dout, gd, nd * sizeof(double), cudaMemcpyDeviceToHost, ctx->c.stream));
       HM_CUDA(cudaStreamSynchronize(ctx->c.stream));
       ar.release();
     }
@@ -298,11 +303,37 @@ hm_status hm_export(hm_ctx ctx, hm_mat mat, hm_host_desc* d) {
     d->bl_nsons = T.bl_nsons.data();
     d->bl_rank = M.ex_rank.data();
     d->bl_off = M.ex_off.data();
-    d->factors = M.ex_factors.get();
+    d->factors = fout;
     d->nfactors = (int64_t)nf;
-    d->dense = M.ex_dense.get();
+    d->dense = dout;
     d->ndense = (int64_t)nd;
     d->perm = T.perm.empty() ? nullptr : T.perm.data();
+  }
+}
+
+hm_status hm_export(hm_ctx ctx, hm_mat mat, hm_host_desc* d) {
+  if (!ctx || !mat || !d) return HM_EINVAL;
+  return guard(ctx, [&] { export_impl(ctx, mat, d, nullptr, nullptr, false); });
+}
+
+hm_status hm_export_into(hm_ctx ctx, hm_mat mat, hm_host_desc* d, double* factors_out, double* dense_out) {
+  if (!ctx || !mat || !d) return HM_EINVAL;
+  return guard(ctx, [&] { export_impl(ctx, mat, d, factors_out, dense_out, true); });
+}
+
+hm_status hm_export_sizes(hm_ctx ctx, hm_mat mat, int64_t* nfactors, int64_t* ndense) {
+  if (!ctx || !mat || !nfactors || !ndense) return HM_EINVAL;
+  return guard(ctx, [&] {
+    const Mat& M = mat->m;
+    const Tree& T = *M.tree;
+    int64_t nf = 0, nd = 0;
+    for (int b = 0; b < T.nblocks(); b++) {
+      const int64_t m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
+      if (T.bl_kind[b] == HM_BLOCK_ADM) nf += (m + n) * M.rank[b];
+      else if (T.bl_kind[b] == HM_BLOCK_DENSE) nd += m * n;
+    }
+    *nfactors = nf;
+    *ndense = nd;
   });
 }
 

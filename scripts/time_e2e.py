@@ -19,7 +19,7 @@ for rep in range(2):
     torch.cuda.synchronize(); t1 = time.perf_counter()
     hm.addmul(1.0, Xh, Yh, Zh, 1e-6)
     torch.cuda.synchronize(); t2 = time.perf_counter()
-    out = Zh.export()
+    out = Zh.export(pinned=len(sys.argv) > 1 and sys.argv[1] == "pinned")
     t3 = time.perf_counter()
     for m_ in (Xh, Yh, Zh):
         m_.free()
