@@ -46,6 +46,11 @@ FACTOR_RUNS = [
     ("cfg3_hchol_n20480", 5, 32, 1e-5, 1, "chol", 1),
     ("cfg4p_hlr_n81920", 6, 64, 1e-6, 0, "lr", 1),
 ]
+# profile class -> kernel (for the ncu traffic lookup)
+CLASS_KERNEL = {"eval": "k_eval2", "apply_q": "k_applyq", "copy": "k_copy", "memset": None,
+                "trunc_fused": "k_trunc_small", "gemm_M": "k_gemm", "dense_add": "k_gemm",
+                "qr_blk384": "k_qr_blocked", "qr_blk768": "k_qr_blocked", "qr_blk1536": "k_qr_blocked",
+                "svd_smem26k": "k_svd", "svd_global": "k_svd", "svd_smem8k": "k_svd", "svd_smem3k": "k_svd"}
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA: SMs x FMA/clk x 2 x max clock
 
 
@@ -285,8 +290,22 @@ def run_ours(args, cfg):
         achieved = p["flops"] / (p["ms"] * 1e-3) / 1e12 if p["ms"] else 0.0
         peak = NOMINAL_FP64_TFLOPS
         peak_src = "FP64 DFMA nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6); tcgen05 has no f64 kind"
+    # dram traffic per launch of the class's kernel: the committed ncu launch
+    # list of one bench step (scripts/ncu_traffic.py -> profiles/*_traffic.json)
+    traffic, traffic_src = None, None
+    kern = CLASS_KERNEL.get(name)
+    tfiles = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic.json"))
+    if kern and tfiles:
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", tfiles[-1])))
+            if kern in tj["kernels"]:
+                traffic = tj["kernels"][kern]["dram_bytes_per_launch"]
+                traffic_src = f"profiles/{tfiles[-1]} ({kern}, ncu dram__bytes_read+write per launch)"
+        except Exception:
+            pass
     roof = {"bound": bound, "kernel": name, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak if peak else None, "traffic": None,
+            "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_per_launch": (p["bytes"] if bound == "hbm" else p["flops"]) / max(p["launches"], 1),
             "per_launch_ms": p["ms"] / max(p["launches"], 1), "launches": p["launches"], "peak_source": peak_src,
             "dgemm_cublas_tflops_measured": dgemm,
             "classes": {k: {"ms": round(v["ms"], 3), "launches": v["launches"],

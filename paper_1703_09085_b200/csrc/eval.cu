@@ -19,137 +19,234 @@
 namespace hm {
 
 namespace {
-constexpr int kT = 64;    // tile rows (out rows) and K chunk
-constexpr int kW = 32;    // column block (of V / out) and rank chunk
+constexpr int kT = 64;     // tile rows (out rows) and K chunk
+constexpr int kW = 32;     // column block (of V / out) and rank chunk
 constexpr int kNT = 256;
-constexpr int kLdS = kT + 1;   // S: 64 x 64 tile, (i, p) at i + p * 65
-constexpr int kLdV = kW + 1;   // Vt: (p, j) at p * 33 + j ; Ts: (q, j) at q * 33 + j
-constexpr int kSmem = kT * kLdS + kT * kLdV + kW * kLdV;
+// Shared-memory leading dimensions = 4 (mod 16): the DMMA fragment loads (8
+// rows x 4 k per warp, lanes (r, k) = (lane >> 2, lane & 3)) and the staging
+// stores (consecutive elements) are both bank-conflict free.
+constexpr int kLd = 68;
+constexpr int kLdJ = 36;
+constexpr int kLdS = kT + 1;              // identity path / TRSM tiles: (i, p) at i + p * 65
+constexpr int kSmemS = kT * kLd;          // S: 64 x 64 operand tile, either orientation
+constexpr int kSmemV = kT * kLdJ;         // V: 64 x 32 (j + p * 36) or 32 x 64 (p + j * 68)
+constexpr int kSmemT = kW * kLdJ;         // Ts: (q, j) at j + q * 36
+constexpr int kSmem = kSmemS + kSmemV + kSmemT;
+static_assert(kW * kLd <= kSmemV, "V tile");
+static_assert(kT * kLdS <= kSmemS, "identity tile");
 
-__device__ __forceinline__ double vat(const EvalJob& J, int p, int j) {
-  return J.vtrans ? J.V[j + (int64_t)p * J.ldv] : J.V[p + (int64_t)j * J.ldv];
+// D(8x8) += A(8x4) B(4x8) in FP64 on the tensor pipe (DMMA.8x8x4).  Fragments
+// (PTX m8n8k4 .f64): a = A(lane >> 2, lane & 3), b = B(lane & 3, lane >> 2),
+// d = D(lane >> 2, 2 (lane & 3) + {0, 1}).
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
 }
 
-// Vt[p][j] = V(vrow + p0 + p, j0 + j), zero padded to 64 x 32
-__device__ __forceinline__ void stage_v(const EvalJob& J, int vrow, int p0, int pc, int j0, int wc, double* Vt) {
+// Warp tiling of an (8 MT) x (8 NCT) output over the 8 warps: each warp owns
+// RTW x CTW 8x8 tiles (row group rg, column group cg).
+template <int MT, int NCT>
+struct WarpTiling {
+  static constexpr int RTW = (MT == 8 && NCT == 4) ? 2 : 1;
+  static constexpr int CTW = (NCT == 4 || (NCT == 2 && MT == 8)) ? 2 : 1;
+  static constexpr int RG = MT / RTW;
+  static constexpr int CG = NCT / CTW;
+};
+
+// acc += A(8 MT x kc) B(kc x 8 NCT), A(i, p) = As[i ars + p acs], B(p, j) =
+// Bs[p brs + j bcs] (shared memory, zero padded to kc rounded up to 4).
+template <int MT, int NCT>
+__device__ __forceinline__ void tile_dmma(const double* As, int ars, int acs, const double* Bs, int brs, int bcs,
+                                          int kc, double (&acc)[WarpTiling<MT, NCT>::RTW * WarpTiling<MT, NCT>::CTW][2]) {
+  using WT = WarpTiling<MT, NCT>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp >= WT::RG * WT::CG) return;
+  const int rg = warp % WT::RG, cg = warp / WT::RG;
+  const int lr = lane >> 2, lk = lane & 3;
+  const double* a0 = As + (rg * WT::RTW * 8 + lr) * ars + lk * acs;
+  const double* b0 = Bs + lk * brs + (cg * WT::CTW * 8 + lr) * bcs;
+#pragma unroll 4
+  for (int k0 = 0; k0 < kc; k0 += 4) {
+    double a[WT::RTW], b[WT::CTW];
+#pragma unroll
+    for (int r = 0; r < WT::RTW; r++) a[r] = a0[r * 8 * ars + k0 * acs];
+#pragma unroll
+    for (int c = 0; c < WT::CTW; c++) b[c] = b0[c * 8 * bcs + k0 * brs];
+#pragma unroll
+    for (int r = 0; r < WT::RTW; r++)
+#pragma unroll
+      for (int c = 0; c < WT::CTW; c++) dmma(acc[r * WT::CTW + c], a[r], b[c]);
+  }
+}
+
+template <int MT, int NCT>
+__device__ __forceinline__ void acc_zero(double (&acc)[WarpTiling<MT, NCT>::RTW * WarpTiling<MT, NCT>::CTW][2]) {
+#pragma unroll
+  for (int t = 0; t < WarpTiling<MT, NCT>::RTW * WarpTiling<MT, NCT>::CTW; t++) acc[t][0] = acc[t][1] = 0.0;
+}
+
+// out[orow + i0 + i, ocol + j0 + j] += coef * D(i, j) for i < mc, j < wc
+template <int NCT>
+__device__ __forceinline__ void store_acc(const EvalJob& J, int orow, int ocol, int i0, int mc, int j0, int wc,
+                                          const double (&acc)[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2]) {
+  using WT = WarpTiling<8, NCT>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp >= WT::RG * WT::CG) return;
+  const int rg = warp % WT::RG, cg = warp / WT::RG;
+#pragma unroll
+  for (int r = 0; r < WT::RTW; r++) {
+    const int i = (rg * WT::RTW + r) * 8 + (lane >> 2);
+    if (i >= mc) continue;
+    double* o = J.out + (orow + i0 + i);
+#pragma unroll
+    for (int c = 0; c < WT::CTW; c++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int j = (cg * WT::CTW + c) * 8 + 2 * (lane & 3) + h;
+        if (j < wc) {
+          double* d = o + (int64_t)(ocol + j0 + j) * J.ldo;
+          *d = fma(J.coef, acc[r * WT::CTW + c][h], *d);
+        }
+      }
+  }
+}
+
+// V(vrow + p0 + p, j0 + j) for p < 64, j < 32, zero padded; the B operand
+// descriptor (brs, bcs) of the layout used.
+__device__ __forceinline__ void stage_v(const EvalJob& J, int vrow, int p0, int pc, int j0, int wc, double* Vs,
+                                        int& brs, int& bcs) {
   const int tid = threadIdx.x;
-  if (!J.vtrans) {
+  if (!J.vtrans) {   // p contiguous in global: Vs[p + j * 68]
     for (int e = tid; e < kT * kW; e += kNT) {
       const int p = e % kT, j = e / kT;
-      Vt[p * kLdV + j] = (p < pc && j < wc) ? J.V[(vrow + p0 + p) + (int64_t)(j0 + j) * J.ldv] : 0.0;
+      Vs[p + j * kLd] = (p < pc && j < wc) ? J.V[(vrow + p0 + p) + (int64_t)(j0 + j) * J.ldv] : 0.0;
     }
-  } else {
+    brs = 1;
+    bcs = kLd;
+  } else {           // j contiguous in global: Vs[j + p * 36]
     for (int e = tid; e < kT * kW; e += kNT) {
       const int j = e % kW, p = e / kW;
-      Vt[p * kLdV + j] = (p < pc && j < wc) ? J.V[(j0 + j) + (int64_t)(vrow + p0 + p) * J.ldv] : 0.0;
+      Vs[j + p * kLdJ] = (p < pc && j < wc) ? J.V[(j0 + j) + (int64_t)(vrow + p0 + p) * J.ldv] : 0.0;
     }
+    brs = kLdJ;
+    bcs = 1;
   }
 }
 
-// out[orow + i0 + i, ocol + j0 + j] += coef * acc  (thread: i = tid & 63, j = (tid >> 6) + 4 u, u < NU)
-template <int NU>
-__device__ __forceinline__ void store_acc(const EvalJob& J, int orow, int ocol, int i0, int mc, int j0, int wc,
-                                          const double (&acc)[NU]) {
-  const int i = threadIdx.x & (kT - 1), jg = threadIdx.x >> 6;
-  if (i >= mc) return;
-  double* o = J.out + (orow + i0 + i);
-#pragma unroll
-  for (int u = 0; u < NU; u++) {
-    const int j = jg + 4 * u;
-    if (j < wc) {
-      double* d = o + (int64_t)(ocol + j0 + j) * J.ldo;
-      *d = fma(J.coef, acc[u], *d);
-    }
-  }
-}
-
-// acc += S(i, 0:kc) * W(0:kc, j), S at i + p * 65 (shared), W at p * 33 + j (shared)
-template <int NU>
-__device__ __forceinline__ void tile_mma(const double* S, const double* W, int kc, double (&acc)[NU]) {
-  const int i = threadIdx.x & (kT - 1), jg = threadIdx.x >> 6;
-#pragma unroll 4
-  for (int p = 0; p < kc; p++) {
-    const double s = S[i + p * kLdS];
-    const double* w = W + p * kLdV + jg;
-#pragma unroll
-    for (int u = 0; u < NU; u++) acc[u] = fma(s, w[4 * u], acc[u]);
-  }
-}
-
-template <int NU>
+template <int NCT>
 __device__ void dense_tiles(const EvalJob& J, const LeafDesc& L, int orow, int vrow, int mo, int ko, int j0, int wc,
-                            double* S, double* Vt) {
+                            double* S, double* Vs) {
   const int tid = threadIdx.x;
   const int ldn = L.m;
   for (int i0 = 0; i0 < mo; i0 += kT) {
     const int mc = min(kT, mo - i0);
-    double acc[NU];
-#pragma unroll
-    for (int u = 0; u < NU; u++) acc[u] = 0.0;
+    double acc[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
+    acc_zero<8, NCT>(acc);
     for (int p0 = 0; p0 < ko; p0 += kT) {
       const int pc = min(kT, ko - p0);
-      // S(i, p) = op(N)(i0 + i, p0 + p)
-      if (!J.trans) {
+      int ars, acs, brs, bcs;
+      if (!J.trans) {   // op(N)(i, p) = N(i, p), i contiguous: S[i + p * 68]
         for (int e = tid; e < kT * kT; e += kNT) {
           const int i = e % kT, p = e / kT;
-          S[i + p * kLdS] = (i < mc && p < pc) ? L.A[(i0 + i) + (int64_t)(p0 + p) * ldn] : 0.0;
+          S[i + p * kLd] = (i < mc && p < pc) ? L.A[(i0 + i) + (int64_t)(p0 + p) * ldn] : 0.0;
         }
-      } else {
+        ars = 1;
+        acs = kLd;
+      } else {          // op(N)(i, p) = N(p, i), p contiguous: S[p + i * 68]
         for (int e = tid; e < kT * kT; e += kNT) {
           const int p = e % kT, i = e / kT;
-          S[i + p * kLdS] = (i < mc && p < pc) ? L.A[(p0 + p) + (int64_t)(i0 + i) * ldn] : 0.0;
+          S[p + i * kLd] = (i < mc && p < pc) ? L.A[(p0 + p) + (int64_t)(i0 + i) * ldn] : 0.0;
         }
+        ars = kLd;
+        acs = 1;
       }
-      stage_v(J, vrow, p0, pc, j0, wc, Vt);
+      stage_v(J, vrow, p0, pc, j0, wc, Vs, brs, bcs);
       __syncthreads();
-      tile_mma<NU>(S, Vt, pc, acc);
+      tile_dmma<8, NCT>(S, ars, acs, Vs, brs, bcs, (pc + 3) & ~3, acc);
       __syncthreads();
     }
-    store_acc<NU>(J, orow, 0, i0, mc, j0, wc, acc);
+    store_acc<NCT>(J, orow, 0, i0, mc, j0, wc, acc);
   }
 }
 
 __device__ void eval_dense(const EvalJob& J, const LeafDesc& L, int orow, int vrow, int mo, int ko, double* S,
-                           double* Vt) {
+                           double* Vs) {
   for (int j0 = 0; j0 < J.w; j0 += kW) {
     const int wc = min(kW, J.w - j0);
-    if (wc <= 8) dense_tiles<2>(J, L, orow, vrow, mo, ko, j0, wc, S, Vt);
-    else if (wc <= 16) dense_tiles<4>(J, L, orow, vrow, mo, ko, j0, wc, S, Vt);
-    else dense_tiles<8>(J, L, orow, vrow, mo, ko, j0, wc, S, Vt);
+    if (wc <= 8) dense_tiles<1>(J, L, orow, vrow, mo, ko, j0, wc, S, Vs);
+    else if (wc <= 16) dense_tiles<2>(J, L, orow, vrow, mo, ko, j0, wc, S, Vs);
+    else dense_tiles<4>(J, L, orow, vrow, mo, ko, j0, wc, S, Vs);
   }
 }
 
-// out(orow + i, ocol + j) += coef sum_q F1(i, q) Ts(q, j) for the rank chunk in Ts
-template <int NU>
+// out(orow + i, ocol + j0 + j) += coef sum_q F1(i, q0 + q) Ts(q, j), Ts(q, j) at j + q * 36
+template <int NCT>
 __device__ void apply_f1_t(const EvalJob& J, const double* F1, int ld1, int mo, int q0, int kc, int orow, int ocol,
                            int j0, int wc, double* S, const double* Ts) {
   const int tid = threadIdx.x;
   for (int i0 = 0; i0 < mo; i0 += kT) {
     const int mc = min(kT, mo - i0);
-    for (int e = tid; e < kT * kW; e += kNT) {
+    for (int e = tid; e < kT * kW; e += kNT) {   // S[i + q * 68] = F1(i0 + i, q0 + q)
       const int i = e % kT, q = e / kT;
-      S[i + q * kLdS] = (i < mc && q < kc) ? F1[(i0 + i) + (int64_t)(q0 + q) * ld1] : 0.0;
+      S[i + q * kLd] = (i < mc && q < kc) ? F1[(i0 + i) + (int64_t)(q0 + q) * ld1] : 0.0;
     }
     __syncthreads();
-    double acc[NU];
-#pragma unroll
-    for (int u = 0; u < NU; u++) acc[u] = 0.0;
-    tile_mma<NU>(S, Ts, kc, acc);
-    store_acc<NU>(J, orow, ocol, i0, mc, j0, wc, acc);
+    double acc[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
+    acc_zero<8, NCT>(acc);
+    tile_dmma<8, NCT>(S, 1, kLd, Ts, kLdJ, 1, (kc + 3) & ~3, acc);
+    store_acc<NCT>(J, orow, ocol, i0, mc, j0, wc, acc);
     __syncthreads();
   }
 }
 
 __device__ void apply_f1(const EvalJob& J, const double* F1, int ld1, int mo, int q0, int kc, int orow, int ocol,
                          int j0, int wc, double* S, const double* Ts) {
-  if (wc <= 8) apply_f1_t<2>(J, F1, ld1, mo, q0, kc, orow, ocol, j0, wc, S, Ts);
-  else if (wc <= 16) apply_f1_t<4>(J, F1, ld1, mo, q0, kc, orow, ocol, j0, wc, S, Ts);
-  else apply_f1_t<8>(J, F1, ld1, mo, q0, kc, orow, ocol, j0, wc, S, Ts);
+  if (wc <= 8) apply_f1_t<1>(J, F1, ld1, mo, q0, kc, orow, ocol, j0, wc, S, Ts);
+  else if (wc <= 16) apply_f1_t<2>(J, F1, ld1, mo, q0, kc, orow, ocol, j0, wc, S, Ts);
+  else apply_f1_t<4>(J, F1, ld1, mo, q0, kc, orow, ocol, j0, wc, S, Ts);
+}
+
+// Ts(q, j) = sum_p F2(p, q0 + q) V(vrow + p, j0 + j)  (q < 32, j < 8 NCT), by DMMA
+// over 64-row chunks of F2 (staged p-contiguous: S[p + q * 68])
+template <int NCT>
+__device__ void lowrank_t(const EvalJob& J, const double* F2, int ld2, int ko, int vrow, int q0, int kc, int j0,
+                          int wc, double* S, double* Vs, double* Ts) {
+  using WT = WarpTiling<4, NCT>;
+  const int tid = threadIdx.x;
+  double acc[WT::RTW * WT::CTW][2];
+  acc_zero<4, NCT>(acc);
+  for (int p0 = 0; p0 < ko; p0 += kT) {
+    const int pc = min(kT, ko - p0);
+    for (int e = tid; e < kT * kW; e += kNT) {
+      const int p = e % kT, q = e / kT;
+      S[p + q * kLd] = (p < pc && q < kc) ? F2[(p0 + p) + (int64_t)(q0 + q) * ld2] : 0.0;
+    }
+    int brs, bcs;
+    stage_v(J, vrow, p0, pc, j0, wc, Vs, brs, bcs);
+    __syncthreads();
+    tile_dmma<4, NCT>(S, kLd, 1, Vs, brs, bcs, (pc + 3) & ~3, acc);
+    __syncthreads();
+  }
+  // fragments -> Ts (every (q, j) of the 32 x 8 NCT tile is written; q >= kc rows are 0)
+  const int lane = tid & 31, warp = tid >> 5;
+  if (warp < WT::RG * WT::CG) {
+    const int rg = warp % WT::RG, cg = warp / WT::RG;
+#pragma unroll
+    for (int r = 0; r < WT::RTW; r++)
+#pragma unroll
+      for (int c = 0; c < WT::CTW; c++) {
+        const int q = (rg * WT::RTW + r) * 8 + (lane >> 2);
+        const int j = (cg * WT::CTW + c) * 8 + 2 * (lane & 3);
+        Ts[j + q * kLdJ] = acc[r * WT::CTW + c][0];
+        Ts[j + 1 + q * kLdJ] = acc[r * WT::CTW + c][1];
+      }
+  }
+  __syncthreads();
 }
 
 __device__ void eval_lowrank(const EvalJob& J, const LeafDesc& L, int orow, int vrow, int mo, int ko, double* S,
-                             double* Vt, double* Ts) {
-  const int tid = threadIdx.x;
+                             double* Vs, double* Ts) {
   const double* F1 = J.trans ? L.B : L.A;
   const int ld1 = J.trans ? L.n : L.m;
   const double* F2 = J.trans ? L.A : L.B;
@@ -158,29 +255,9 @@ __device__ void eval_lowrank(const EvalJob& J, const LeafDesc& L, int orow, int 
     const int wc = min(kW, J.w - j0);
     for (int q0 = 0; q0 < L.k; q0 += kW) {
       const int kc = min(kW, L.k - q0);
-      // T(q, j) = sum_p F2(p, q0 + q) V(vrow + p, j0 + j); thread: q = tid & 31, j = warp + 8 u
-      const int q = tid & 31, jw = tid >> 5;
-      double t[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int p0 = 0; p0 < ko; p0 += kT) {
-        const int pc = min(kT, ko - p0);
-        for (int e = tid; e < kT * kW; e += kNT) {   // S2(q, p) at q + p * 33 (conflict-free reads)
-          const int p = e % kT, qq = e / kT;
-          S[qq + p * kLdV] = (p < pc && qq < kc) ? F2[(p0 + p) + (int64_t)(q0 + qq) * ld2] : 0.0;
-        }
-        stage_v(J, vrow, p0, pc, j0, wc, Vt);
-        __syncthreads();
-#pragma unroll 4
-        for (int p = 0; p < pc; p++) {
-          const double f = S[q + p * kLdV];
-          const double* v = Vt + p * kLdV + jw;
-#pragma unroll
-          for (int u = 0; u < 4; u++) t[u] = fma(f, v[8 * u], t[u]);
-        }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++) Ts[q * kLdV + jw + 8 * u] = t[u];
-      __syncthreads();
+      if (wc <= 8) lowrank_t<1>(J, F2, ld2, ko, vrow, q0, kc, j0, wc, S, Vs, Ts);
+      else if (wc <= 16) lowrank_t<2>(J, F2, ld2, ko, vrow, q0, kc, j0, wc, S, Vs, Ts);
+      else lowrank_t<4>(J, F2, ld2, ko, vrow, q0, kc, j0, wc, S, Vs, Ts);
       apply_f1(J, F1, ld1, mo, q0, kc, orow, 0, j0, wc, S, Ts);
     }
   }
@@ -229,9 +306,9 @@ __device__ void eval_identity(const EvalJob& J, const LeafDesc& L, int orow, int
     const int wc = min(kW, ko - j0);
     for (int q0 = 0; q0 < L.k; q0 += kW) {
       const int kc = min(kW, L.k - q0);
-      for (int e = tid; e < kW * kW; e += kNT) {   // Ts(q, j) = F2(j0 + j, q0 + q)
+      for (int e = tid; e < kW * kW; e += kNT) {   // Ts(q, j) = F2(j0 + j, q0 + q) at j + q * 36
         const int j = e % kW, q = e / kW;
-        Ts[q * kLdV + j] = (j < wc && q < kc) ? F2[(j0 + j) + (int64_t)(q0 + q) * ld2] : 0.0;
+        Ts[j + q * kLdJ] = (j < wc && q < kc) ? F2[(j0 + j) + (int64_t)(q0 + q) * ld2] : 0.0;
       }
       __syncthreads();
       apply_f1(J, F1, ld1, mo, q0, kc, orow, vrow, j0, wc, S, Ts);
@@ -242,8 +319,8 @@ __device__ void eval_identity(const EvalJob& J, const LeafDesc& L, int orow, int
 
 __device__ void eval_range(const EvalJob& J, int lb, int le, double* sm) {
   double* S = sm;
-  double* Vt = S + kT * kLdS;
-  double* Ts = Vt + kT * kLdV;
+  double* Vt = S + kSmemS;
+  double* Ts = Vt + kSmemV;
   for (int li = lb; li < le; li++) {
     __syncthreads();   // the previous leaf's output writes are visible to every thread
     const LeafDesc L = J.leaves[li];
@@ -259,10 +336,17 @@ __device__ void eval_range(const EvalJob& J, int lb, int le, double* sm) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kNT) k_eval2(const EvalJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kNT, 3) k_eval2(const EvalJob* __restrict__ jobs) {
   extern __shared__ double sm[];
   const EvalJob J = jobs[blockIdx.x];
-  eval_range(J, J.leaf_begin, J.leaf_end, sm);
+  if (J.nrng == 0) {
+    eval_range(J, J.leaf_begin, J.leaf_end, sm);
+  } else {
+    for (int g = 0; g < J.nrng; g++) {
+      const int2 r = J.rng[g];
+      eval_range(J, r.x, r.y, sm);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ TRSM

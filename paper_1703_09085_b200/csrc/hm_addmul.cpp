@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <unordered_map>
 
@@ -173,6 +174,10 @@ struct Planner {
 
   // H-side product over the DFS leaves of block blk of X (yside = false) or Y
   // (yside = true); trans: out += coef H|_blk^T V instead of H|_blk V.
+  struct EvalMeta { double cost; int blk, yside; };
+  std::vector<EvalMeta> emeta;   // host-side companions of the level's EvalJobs
+  std::vector<int2> erng;        // leaf-range table of split jobs (uploaded with the jobs)
+
   void add_eval(std::vector<EvalJob>& ej, bool yside, int blk, int trans, double coef, double* out,
                 int ldo, int w, const double* V, int ldv, int vtrans, int videntity) {
     if (w <= 0) return;
@@ -201,8 +206,89 @@ struct Planner {
     const double by = 8.0 * (smat + smn * w);
     fl_eval += fl;
     by_eval += by;
-    e.cost = (int64_t)(by + fl);
+    e.nrng = 0;
+    e.rng = nullptr;
     ej.push_back(e);
+    emeta.push_back(EvalMeta{by + fl, blk, yside ? 1 : 0});
+  }
+
+  // Load balance of one eval batch: a job whose cost exceeds thr is cut into
+  // row groups of its block -- the output-row cluster (row cluster for
+  // trans = 0, column cluster for trans = 1) is descended while every block of
+  // the group is subdivided; each group keeps the DFS ranges of its sub-blocks
+  // (at most kEvalRanges) and writes only its own output rows.  The sums per
+  // output entry run over the same leaves in the same order, so the result is
+  // bit-identical to the unsplit job.
+  void split_evals(std::vector<EvalJob>& ej) {
+    erng.clear();
+    double total = 0;
+    for (auto& m : emeta) total += m.cost;
+    static const double div = [] { const char* e = std::getenv("HM_EVAL_SPLIT"); return e ? std::atof(e) : 1184.0; }();
+    if (div <= 0) return;
+    const double thr = std::max(total / div, 2e5);
+    std::vector<EvalJob> out;
+    std::vector<EvalMeta> mout;
+    out.reserve(ej.size());
+    mout.reserve(ej.size());
+    for (size_t ji = 0; ji < ej.size(); ji++) {
+      const EvalJob& e = ej[ji];
+      const EvalMeta& em = emeta[ji];
+      if (em.cost <= thr) { out.push_back(e); mout.push_back(em); continue; }
+      const std::vector<double>& pm = em.yside ? ly_mat : lx_mat;
+      const std::vector<double>& pn = em.yside ? ly_mn : lx_mn;
+      auto bcost = [&](int b) {
+        const double smat = pm[T.bl_lend[b]] - pm[T.bl_lbeg[b]], smn = pn[T.bl_lend[b]] - pn[T.bl_lbeg[b]];
+        return 8.0 * (smat + smn * e.w) + (e.videntity ? 0.0 : 2.0 * e.w * smat);
+      };
+      struct G { std::vector<int> blocks; double cost; };
+      std::vector<G> groups{G{{em.blk}, em.cost}};
+      for (int it = 0; it < 3; it++) {
+        std::vector<G> nx;
+        bool any = false;
+        for (G& g : groups) {
+          bool ok = g.cost > thr;
+          int nsplit = 0;
+          for (int b : g.blocks) {
+            if (T.bl_kind[b] != HM_BLOCK_SUB) { ok = false; break; }
+            nsplit = T.cl_nsons[e.trans ? T.bl_col[b] : T.bl_row[b]];
+          }
+          const int other = ok ? T.cl_nsons[e.trans ? T.bl_row[g.blocks[0]] : T.bl_col[g.blocks[0]]] : 0;
+          if (!ok || (int)g.blocks.size() * other > kEvalRanges) { nx.push_back(std::move(g)); continue; }
+          any = true;
+          for (int i = 0; i < nsplit; i++) {
+            G h{{}, 0.0};
+            for (int b : g.blocks) {
+              const int no = T.cl_nsons[e.trans ? T.bl_row[b] : T.bl_col[b]];
+              for (int j = 0; j < no; j++) {
+                const int sb = e.trans ? T.son(b, j, i) : T.son(b, i, j);
+                h.blocks.push_back(sb);
+                h.cost += bcost(sb);
+              }
+            }
+            nx.push_back(std::move(h));
+          }
+        }
+        groups.swap(nx);
+        if (!any) break;
+      }
+      for (G& g : groups) {
+        EvalJob s = e;
+        // sub-blocks in DFS order; adjacent ranges merged; the range table
+        // offset is stored in rng until the table is uploaded
+        std::sort(g.blocks.begin(), g.blocks.end(), [&](int a, int b) { return T.bl_lbeg[a] < T.bl_lbeg[b]; });
+        const size_t r0 = erng.size();
+        for (int b : g.blocks) {
+          if (T.bl_lbeg[b] == T.bl_lend[b]) continue;
+          if (erng.size() > r0 && erng.back().y == T.bl_lbeg[b]) erng.back().y = T.bl_lend[b];
+          else erng.push_back(make_int2(T.bl_lbeg[b], T.bl_lend[b]));
+        }
+        s.nrng = (int)(erng.size() - r0);
+        s.rng = reinterpret_cast<const int2*>(static_cast<intptr_t>(r0));
+        if (s.nrng > 0) { out.push_back(s); mout.push_back(EvalMeta{g.cost, em.blk, em.yside}); }
+      }
+    }
+    ej.swap(out);
+    emeta.swap(mout);
   }
 
   // Emit the A2 realisation of one evaluated term into stack columns [col, col+w).
@@ -271,9 +357,35 @@ struct Planner {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
   }
 
-  void run_level(std::vector<Node>& nodes) {
+  // Device work of one level is enqueued by run_level_enqueue; the ranks it
+  // produces are read back by run_level_finish.  Between the two the host may
+  // plan the next level (split_level needs only the FP ids, not their ranks).
+  struct LevelTail {
+    std::unique_ptr<Arena> scratch;
+    int* d_ranks = nullptr;
+    std::vector<TruncReq> tr;
+    std::vector<int> tr_fp;
+  };
+
+  void run_level(std::vector<Node>& nodes) { run_level_finish(run_level_enqueue(nodes)); }
+
+  void run_level_finish(LevelTail lt) {
+    sync_ranks(lt.d_ranks, lt.tr_fp);
+    for (size_t i = 0; i < lt.tr.size(); i++) {
+      const double k = fps[lt.tr_fp[i]].k;
+      fl_trunc += trunc_flops(lt.tr[i].m, lt.tr[i].n, lt.tr[i].l, k);
+      by_trunc += trunc_bytes(lt.tr[i].m, lt.tr[i].n, lt.tr[i].l, k);
+      n_cols += lt.tr[i].l;
+    }
+    n_trunc += (int64_t)lt.tr.size();
+    if (lt.scratch) lt.scratch->release();
+  }
+
+  LevelTail run_level_enqueue(std::vector<Node>& nodes) {
     double t0 = now_s();
-    Arena scratch(c);
+    LevelTail lt;
+    lt.scratch.reset(new Arena(c));
+    Arena& scratch = *lt.scratch;
     std::vector<Stack> stacks;
     for (int i = 0; i < (int)nodes.size(); i++) {
       Node& nd = nodes[i];
@@ -297,7 +409,7 @@ struct Planner {
       }
       if (kind) stacks.push_back(Stack{i, kind, m, n, l, nullptr, nullptr, -1});
     }
-    if (stacks.empty()) return;
+    if (stacks.empty()) return lt;
     size_t total = 0;
     for (auto& s : stacks) total += (size_t)(s.m + s.n) * s.l;
     double* buf = c->stack_ws(total + 1);
@@ -345,10 +457,30 @@ struct Planner {
     double t2 = now_s();
     t_b += t2 - t1;
     if (!ej.empty()) {
-      std::stable_sort(ej.begin(), ej.end(),
-                       [](const EvalJob& a, const EvalJob& b) { return a.cost > b.cost; });
-      ProfScope ps(c, PC_EVAL, fl_eval - fl_eval0, by_eval - by_eval0);
       static const bool old_eval = std::getenv("HM_EVAL_OLD") != nullptr;
+      if (!old_eval) split_evals(ej);
+      // largest first (index sort: the jobs themselves are moved once)
+      std::vector<int> order(ej.size());
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return emeta[a].cost > emeta[b].cost; });
+      if (const char* dump = std::getenv("HM_DUMP_EVAL")) {   // diagnostics: job cost spread per batch
+        if (FILE* f = std::fopen(dump, "a")) {
+          double sum = 0;
+          for (auto& m : emeta) sum += m.cost;
+          std::fprintf(f, "jobs %zu sum %.4g max %.4g p50 %.4g ranges %zu\n", ej.size(), sum,
+                       emeta[order[0]].cost, emeta[order[order.size() / 2]].cost, erng.size());
+          std::fclose(f);
+        }
+      }
+      const int2* drng = erng.empty() ? nullptr : scratch.upload(erng);
+      std::vector<EvalJob> sorted(ej.size());
+      for (size_t i = 0; i < order.size(); i++) {
+        sorted[i] = ej[order[i]];
+        if (sorted[i].nrng > 0) sorted[i].rng = drng + reinterpret_cast<intptr_t>(sorted[i].rng);
+      }
+      ej.swap(sorted);
+      emeta.clear();
+      ProfScope ps(c, PC_EVAL, fl_eval - fl_eval0, by_eval - by_eval0);
       if (old_eval) launch_eval(scratch.upload(ej), (int)ej.size(), c->stream);
       else launch_eval2(scratch.upload(ej), (int)ej.size(), c->stream);
       HM_CHECK_LAUNCH();
@@ -395,19 +527,14 @@ struct Planner {
     t_c += t3 - t2;
     trunc_batched(c, scratch, tr, eps);
     t_d += now_s() - t3;
-    sync_ranks(d_ranks, tr_fp);
-    for (size_t i = 0; i < tr.size(); i++) {
-      const double k = fps[tr_fp[i]].k;
-      fl_trunc += trunc_flops(tr[i].m, tr[i].n, tr[i].l, k);
-      by_trunc += trunc_bytes(tr[i].m, tr[i].n, tr[i].l, k);
-      n_cols += tr[i].l;
-    }
-    n_trunc += (int64_t)tr.size();
     for (auto& s : stacks) {
       Node& nd = nodes[s.node];
       if (s.kind == 2 && nd.zt == ZA) zresult[nd.zb] = nd.result;
     }
-    scratch.release();
+    lt.d_ranks = d_ranks;
+    lt.tr = std::move(tr);
+    lt.tr_fp = std::move(tr_fp);
+    return lt;
   }
 
   // Fig. 6 split for every node with pending products -> next level.
@@ -628,10 +755,11 @@ struct Planner {
     levels.push_back(std::move(roots));
     while (true) {
       auto a = clk::now();
-      run_level(levels.back());
+      LevelTail tail = run_level_enqueue(levels.back());
       auto b = clk::now();
-      std::vector<Node> next = split_level(levels.back());
+      std::vector<Node> next = split_level(levels.back());   // overlaps the level's device work
       auto d = clk::now();
+      run_level_finish(std::move(tail));
       t_level += sec(a, b);
       t_split += sec(b, d);
       if (next.empty()) break;

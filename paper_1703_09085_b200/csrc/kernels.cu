@@ -219,7 +219,7 @@ void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
 // factors the reflectors are applied 16 at a time (Q_p = I - Y_p T_p Y_p^T,
 // last panel first): two passes over the rows per panel instead of two per
 // reflector.
-__global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(256, 3) k_applyq(const ApplyQJob* __restrict__ jobs) {
   const ApplyQJob J = jobs[blockIdx.x];
   const int c = J.cdyn ? *J.cdyn : J.c;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -247,13 +247,9 @@ __global__ void __launch_bounds__(256) k_applyq(const ApplyQJob* __restrict__ jo
       }
       for (; i + 32 < J.m; i += 64) {
         const double xa = x[i], xb = x[i + 32];
-        double va[16], vb[16];
 #pragma unroll
         for (int q = 0; q < 16; q++)
-          if (q < kb) { va[q] = Vp[i + (int64_t)q * J.ldv]; vb[q] = Vp[i + 32 + (int64_t)q * J.ldv]; }
-#pragma unroll
-        for (int q = 0; q < 16; q++)
-          if (q < kb) w[q] = fma(vb[q], xb, fma(va[q], xa, w[q]));
+          if (q < kb) w[q] = fma(Vp[i + 32 + (int64_t)q * J.ldv], xb, fma(Vp[i + (int64_t)q * J.ldv], xa, w[q]));
       }
       for (; i < J.m; i += 32) {
         const double xi = x[i];

@@ -106,6 +106,7 @@ struct LeafDesc {
   const double* B;     // adm: n x k
 };
 
+constexpr int kEvalRanges = 8;
 // out += coef * H|_{t x s} V   (trans=0; out rows = #t, V rows = #s) or
 // out += coef * H|_{t x s}^T V (trans=1; out rows = #s, V rows = #t),
 // summed over the leaves [leaf_begin, leaf_end) of block (t,s)  (Fig. 1).
@@ -120,7 +121,12 @@ struct EvalJob {
   int ldo, w;
   const double* V;
   int ldv, vtrans, videntity;
-  int64_t cost;        // for scheduling (largest first)
+  // k_eval2: nrng = 0 visits [leaf_begin, leaf_end) (the whole block); else the
+  // leaf ranges rng[0:nrng] = a row group of the block (every range writes
+  // output rows no other job of the batch writes), so one large block can be
+  // spread over several CTAs without atomics.
+  int nrng;
+  const int2* rng;
 };
 
 // Triangular solve through the H-structure on a thin panel (one CTA per job).

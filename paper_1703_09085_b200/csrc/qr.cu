@@ -310,7 +310,9 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
   if (cap > 24 * 1024) cap = 24 * 1024;
   count_launch();
   static const int thr = [] { const char* e = std::getenv("HM_QR_THREADS"); return e ? std::atoi(e) : 0; }();
-  const int threads = thr > 0 ? thr : (cap <= 6 * 1024 ? 256 : 512);
+  static const int thr12 = [] { const char* e = std::getenv("HM_QR_T12K"); return e ? std::atoi(e) : 0; }();
+  int threads = thr > 0 ? thr : (cap <= 6 * 1024 ? 256 : 512);
+  if (thr12 > 0 && cap > 6 * 1024 && cap <= 12 * 1024) threads = thr12;
   k_qr_blocked<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, cap);
 }
 

@@ -873,7 +873,9 @@ void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int 
   // the L x c loops lose more than the cheaper barriers gain)
   // few stacks (latency-bound, e.g. the H-LR critical path): 512 threads so
   // every Jacobi pair of a round is in flight; many stacks: 256 (two CTAs/SM)
-  const int threads = njobs < 296 ? 512 : 256;
+  static const int tsmall = [] { const char* e = std::getenv("HM_TS_THREADS"); return e ? std::atoi(e) : 0; }();
+  int threads = njobs < 296 ? 512 : 256;
+  if (tsmall > 0 && njobs >= 296 && cap <= 4 * 1024) threads = tsmall;
   k_trunc_small<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps);
 }
 

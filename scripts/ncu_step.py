@@ -7,6 +7,8 @@
                                              then ONE profiled step
 """
 import sys
+import time
+T0 = time.time()
 sys.path.insert(0, '.')
 import numpy as np
 import torch
@@ -25,16 +27,23 @@ if mode == "save":
 z = np.load(path)
 d = {k: z[k] for k in z.files}
 d["perm"] = d.get("perm")
+print(f"[{time.time()-T0:.1f}s] loaded npz", flush=True)
 G = ctx.import_desc(d)
+torch.cuda.synchronize()
+print(f"[{time.time()-T0:.1f}s] imported", flush=True)
 X, Y = G.clone(), G.clone()
 Z = G.clone()
-hm.addmul(1.0, X, Y, Z, eps)          # warm-up (pools, caches)
-Z.free()
-Z = G.clone()
+import os
+if not os.environ.get("HM_NCU_NOWARM"):
+    hm.addmul(1.0, X, Y, Z, eps)          # warm-up (pools, caches)
+    torch.cuda.synchronize()
+    print(f"[{time.time()-T0:.1f}s] warm-up step done", flush=True)
+    Z.free()
+    Z = G.clone()
 torch.cuda.synchronize()
 print("launches before step:", ctx.last_stats()["kernel_launches"], flush=True)
 torch.cuda.profiler.start()
 hm.addmul(1.0, X, Y, Z, eps)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("launches after step:", ctx.last_stats()["kernel_launches"], flush=True)
+print(f"[{time.time()-T0:.1f}s] launches after step:", ctx.last_stats()["kernel_launches"], flush=True)
