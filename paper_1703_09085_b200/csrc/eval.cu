@@ -35,6 +35,15 @@ constexpr int kSmem = kSmemS + kSmemV + kSmemT;
 static_assert(kW * kLd <= kSmemV, "V tile");
 static_assert(kT * kLdS <= kSmemS, "identity tile");
 
+// Asynchronous global -> shared copy of one double (LDGSTS; zero fill when
+// !ok, the source is then not read): every staging load of a tile is in
+// flight at once instead of one load -> store round trip per element.
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // D(8x8) += A(8x4) B(4x8) in FP64 on the tensor pipe (DMMA.8x8x4).  Fragments
 // (PTX m8n8k4 .f64): a = A(lane >> 2, lane & 3), b = B(lane & 3, lane >> 2),
 // d = D(lane >> 2, 2 (lane & 3) + {0, 1}).
@@ -120,14 +129,16 @@ __device__ __forceinline__ void stage_v(const EvalJob& J, int vrow, int p0, int 
   if (!J.vtrans) {   // p contiguous in global: Vs[p + j * 68]
     for (int e = tid; e < kT * kW; e += kNT) {
       const int p = e % kT, j = e / kT;
-      Vs[p + j * kLd] = (p < pc && j < wc) ? J.V[(vrow + p0 + p) + (int64_t)(j0 + j) * J.ldv] : 0.0;
+      const bool ok = p < pc && j < wc;
+      cp8(Vs + p + j * kLd, ok ? J.V + (vrow + p0 + p) + (int64_t)(j0 + j) * J.ldv : J.V, ok);
     }
     brs = 1;
     bcs = kLd;
   } else {           // j contiguous in global: Vs[j + p * 36]
     for (int e = tid; e < kT * kW; e += kNT) {
       const int j = e % kW, p = e / kW;
-      Vs[j + p * kLdJ] = (p < pc && j < wc) ? J.V[(j0 + j) + (int64_t)(vrow + p0 + p) * J.ldv] : 0.0;
+      const bool ok = p < pc && j < wc;
+      cp8(Vs + j + p * kLdJ, ok ? J.V + (j0 + j) + (int64_t)(vrow + p0 + p) * J.ldv : J.V, ok);
     }
     brs = kLdJ;
     bcs = 1;
@@ -149,19 +160,22 @@ __device__ void dense_tiles(const EvalJob& J, const LeafDesc& L, int orow, int v
       if (!J.trans) {   // op(N)(i, p) = N(i, p), i contiguous: S[i + p * 68]
         for (int e = tid; e < kT * kT; e += kNT) {
           const int i = e % kT, p = e / kT;
-          S[i + p * kLd] = (i < mc && p < pc) ? L.A[(i0 + i) + (int64_t)(p0 + p) * ldn] : 0.0;
+          const bool ok = i < mc && p < pc;
+          cp8(S + i + p * kLd, ok ? L.A + (i0 + i) + (int64_t)(p0 + p) * ldn : L.A, ok);
         }
         ars = 1;
         acs = kLd;
       } else {          // op(N)(i, p) = N(p, i), p contiguous: S[p + i * 68]
         for (int e = tid; e < kT * kT; e += kNT) {
           const int p = e % kT, i = e / kT;
-          S[p + i * kLd] = (i < mc && p < pc) ? L.A[(p0 + p) + (int64_t)(i0 + i) * ldn] : 0.0;
+          const bool ok = i < mc && p < pc;
+          cp8(S + p + i * kLd, ok ? L.A + (p0 + p) + (int64_t)(i0 + i) * ldn : L.A, ok);
         }
         ars = kLd;
         acs = 1;
       }
       stage_v(J, vrow, p0, pc, j0, wc, Vs, brs, bcs);
+      cp_wait();
       __syncthreads();
       tile_dmma<8, NCT>(S, ars, acs, Vs, brs, bcs, (pc + 3) & ~3, acc);
       __syncthreads();
@@ -189,8 +203,10 @@ __device__ void apply_f1_t(const EvalJob& J, const double* F1, int ld1, int mo, 
     const int mc = min(kT, mo - i0);
     for (int e = tid; e < kT * kW; e += kNT) {   // S[i + q * 68] = F1(i0 + i, q0 + q)
       const int i = e % kT, q = e / kT;
-      S[i + q * kLd] = (i < mc && q < kc) ? F1[(i0 + i) + (int64_t)(q0 + q) * ld1] : 0.0;
+      const bool ok = i < mc && q < kc;
+      cp8(S + i + q * kLd, ok ? F1 + (i0 + i) + (int64_t)(q0 + q) * ld1 : F1, ok);
     }
+    cp_wait();
     __syncthreads();
     double acc[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
     acc_zero<8, NCT>(acc);
@@ -220,10 +236,12 @@ __device__ void lowrank_t(const EvalJob& J, const double* F2, int ld2, int ko, i
     const int pc = min(kT, ko - p0);
     for (int e = tid; e < kT * kW; e += kNT) {
       const int p = e % kT, q = e / kT;
-      S[p + q * kLd] = (p < pc && q < kc) ? F2[(p0 + p) + (int64_t)(q0 + q) * ld2] : 0.0;
+      const bool ok = p < pc && q < kc;
+      cp8(S + p + q * kLd, ok ? F2 + (p0 + p) + (int64_t)(q0 + q) * ld2 : F2, ok);
     }
     int brs, bcs;
     stage_v(J, vrow, p0, pc, j0, wc, Vs, brs, bcs);
+    cp_wait();
     __syncthreads();
     tile_dmma<4, NCT>(S, kLd, 1, Vs, brs, bcs, (pc + 3) & ~3, acc);
     __syncthreads();
@@ -308,8 +326,10 @@ __device__ void eval_identity(const EvalJob& J, const LeafDesc& L, int orow, int
       const int kc = min(kW, L.k - q0);
       for (int e = tid; e < kW * kW; e += kNT) {   // Ts(q, j) = F2(j0 + j, q0 + q) at j + q * 36
         const int j = e % kW, q = e / kW;
-        Ts[j + q * kLdJ] = (j < wc && q < kc) ? F2[(j0 + j) + (int64_t)(q0 + q) * ld2] : 0.0;
+        const bool ok = j < wc && q < kc;
+        cp8(Ts + j + q * kLdJ, ok ? F2 + (j0 + j) + (int64_t)(q0 + q) * ld2 : F2, ok);
       }
+      cp_wait();
       __syncthreads();
       apply_f1(J, F1, ld1, mo, q0, kc, orow, vrow, j0, wc, S, Ts);
     }

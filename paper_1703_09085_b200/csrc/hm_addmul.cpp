@@ -428,35 +428,31 @@ struct Planner {
     t_a += t1 - t0;
     std::vector<CopyJob> cj;
     std::vector<EvalJob> ej;
-    int64_t ctiles = 0;
-    const double fl_eval0 = fl_eval, by_eval0 = by_eval;
-    for (auto& s : stacks) {
-      Node& nd = nodes[s.node];
-      int col = 0;
-      if (s.kind == 2) {
-        FP zf = zview(nd.zb);
-        copy_view(zf, nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
-        col += zf.k;
-      }
-      if (nd.base >= 0) {
-        copy_view(fps[nd.base], nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
-        col += fps[nd.base].k;
-      }
-      for (auto& tm : nd.terms) {
-        emit_term(tm, s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
-        col += tm.w;
-      }
-    }
     {
+      size_t nterms = 0;
+      for (auto& s : stacks) nterms += nodes[s.node].terms.size();
+      cj.reserve(nterms + 2 * stacks.size());
+      ej.reserve(nterms);
+      emeta.reserve(nterms);
+    }
+    int64_t ctiles = 0;
+    double fl_eval0 = fl_eval, by_eval0 = by_eval;
+    // The level's copy and eval jobs are launched in chunks as they are built,
+    // so the device starts on the first chunk while the host builds the rest
+    // (copies and evaluations write disjoint stack columns: any order).
+    static const size_t kChunk = [] { const char* e = std::getenv("HM_JOB_CHUNK"); return e ? (size_t)std::atoll(e) : (size_t)1 << 16; }();
+    auto flush_copy = [&]() {
+      if (cj.empty()) return;
       double cb = 0;
       for (auto& j : cj) cb += 16.0 * j.rows * (j.identity ? 1 : j.cols);
       ProfScope ps(c, PC_COPY, 0, cb);
       launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
       HM_CHECK_LAUNCH();
-    }
-    double t2 = now_s();
-    t_b += t2 - t1;
-    if (!ej.empty()) {
+      cj.clear();
+      ctiles = 0;
+    };
+    auto flush_eval = [&]() {
+      if (ej.empty()) return;
       static const bool old_eval = std::getenv("HM_EVAL_OLD") != nullptr;
       if (!old_eval) split_evals(ej);
       // largest first (index sort: the jobs themselves are moved once)
@@ -478,13 +474,39 @@ struct Planner {
         sorted[i] = ej[order[i]];
         if (sorted[i].nrng > 0) sorted[i].rng = drng + reinterpret_cast<intptr_t>(sorted[i].rng);
       }
-      ej.swap(sorted);
       emeta.clear();
+      erng.clear();
+      ej.clear();
       ProfScope ps(c, PC_EVAL, fl_eval - fl_eval0, by_eval - by_eval0);
-      if (old_eval) launch_eval(scratch.upload(ej), (int)ej.size(), c->stream);
-      else launch_eval2(scratch.upload(ej), (int)ej.size(), c->stream);
+      fl_eval0 = fl_eval;
+      by_eval0 = by_eval;
+      if (old_eval) launch_eval(scratch.upload(sorted), (int)sorted.size(), c->stream);
+      else launch_eval2(scratch.upload(sorted), (int)sorted.size(), c->stream);
       HM_CHECK_LAUNCH();
+    };
+    for (auto& s : stacks) {
+      Node& nd = nodes[s.node];
+      int col = 0;
+      if (s.kind == 2) {
+        FP zf = zview(nd.zb);
+        copy_view(zf, nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
+        col += zf.k;
+      }
+      if (nd.base >= 0) {
+        copy_view(fps[nd.base], nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
+        col += fps[nd.base].k;
+      }
+      for (auto& tm : nd.terms) {
+        emit_term(tm, s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
+        col += tm.w;
+      }
+      if (ej.size() >= kChunk) flush_eval();
+      if (cj.size() >= kChunk) flush_copy();
     }
+    flush_copy();
+    double t2 = now_s();
+    t_b += t2 - t1;
+    flush_eval();
     // truncations and dense adds
     std::vector<TruncReq> tr;
     std::vector<int> tr_fp;

@@ -311,7 +311,9 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
   count_launch();
   static const int thr = [] { const char* e = std::getenv("HM_QR_THREADS"); return e ? std::atoi(e) : 0; }();
   static const int thr12 = [] { const char* e = std::getenv("HM_QR_T12K"); return e ? std::atoi(e) : 0; }();
-  int threads = thr > 0 ? thr : (cap <= 6 * 1024 ? 256 : 512);
+  // <= 12 K doubles (96 KB): 256 threads, two CTAs per SM (measured on B200:
+  // the 768-row bucket 194 -> 165 ms per cfg-4 product vs one 512-thread CTA)
+  int threads = thr > 0 ? thr : (cap <= 12 * 1024 ? 256 : 512);
   if (thr12 > 0 && cap > 6 * 1024 && cap <= 12 * 1024) threads = thr12;
   k_qr_blocked<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, cap);
 }
