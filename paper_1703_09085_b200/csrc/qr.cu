@@ -42,7 +42,11 @@ __device__ __forceinline__ double wsum(double v) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(512, 1) k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
+// Instantiated per launch shape (the body reads blockDim.x): <512, 1> for
+// the 24 K-double buckets (one CTA per SM by shared memory), <256, 2> for
+// 12 K, <256, 3> for 6 K -- register caps that let that many CTAs share an SM.
+template <int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
   extern __shared__ double Vs[];            // panel / V (rows x nb), column-major
   __shared__ double T[kNbMax * kNbMax];     // upper triangular, column-major
   __shared__ double G[kNbMax * kNbMax];     // V^T V
@@ -304,18 +308,19 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
   if (njobs <= 0) return;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_qr_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * 1024 * 8);
+    cudaFuncSetAttribute(k_qr_blocked<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * 1024 * 8);
+    cudaFuncSetAttribute(k_qr_blocked<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 1024 * 8);
+    cudaFuncSetAttribute(k_qr_blocked<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 1024 * 8);
     attr = true;
   }
   if (cap > 24 * 1024) cap = 24 * 1024;
   count_launch();
-  static const int thr = [] { const char* e = std::getenv("HM_QR_THREADS"); return e ? std::atoi(e) : 0; }();
-  static const int thr12 = [] { const char* e = std::getenv("HM_QR_T12K"); return e ? std::atoi(e) : 0; }();
-  // <= 12 K doubles (96 KB): 256 threads, two CTAs per SM (measured on B200:
-  // the 768-row bucket 194 -> 165 ms per cfg-4 product vs one 512-thread CTA)
-  int threads = thr > 0 ? thr : (cap <= 12 * 1024 ? 256 : 512);
-  if (thr12 > 0 && cap > 6 * 1024 && cap <= 12 * 1024) threads = thr12;
-  k_qr_blocked<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, cap);
+  static const int occ3 = [] { const char* e = std::getenv("HM_QR_OCC3"); return e ? std::atoi(e) : 1; }();
+  // <= 12 K doubles (96 KB): 256 threads, two or three CTAs per SM (measured on
+  // B200: the 768-row bucket 194 -> 165 ms per cfg-4 product vs one 512-thread CTA)
+  if (cap <= 6 * 1024 && occ3) k_qr_blocked<256, 3><<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, cap);
+  else if (cap <= 12 * 1024) k_qr_blocked<256, 2><<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, cap);
+  else k_qr_blocked<512, 1><<<njobs, 512, (size_t)cap * 8, st>>>(d_jobs, cap);
 }
 
 }  // namespace hm

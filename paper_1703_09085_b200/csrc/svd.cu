@@ -4,8 +4,9 @@
 // Algorithm, on C = M (p >= q) or C = M^T (p < q), L x c:
 //   1. Householder QR with column pivoting C P = Q R (Businger-Golub), stopped
 //      at step r~ once the trailing Frobenius norm is <= delta =
-//      4 u sqrt(c) ||M||_F: the dropped block only perturbs M by rounding-level
-//      amounts (the backward error of the QR/GEMM that formed M).  QRCP is
+//      max(4 u sqrt(c), 1e-6 eps) ||M||_F: the dropped block perturbs M by at
+//      most the rounding level of the QR/GEMM that formed M or 1e-6 of the
+//      truncation tolerance (svd_core, reading R7c).  QRCP is
 //      also the classic preconditioner of one-sided Jacobi (Drmac-Veselic):
 //      kernel blocks need ~6 sweeps on R^T instead of ~25 on M.
 //   2. One-sided Jacobi (Hestenes) on X = R^T (c x r~), round-robin parallel
@@ -29,6 +30,7 @@ namespace hm {
 
 static constexpr double kUs = 1.1102230246251565e-16;  // 2^-53
 static constexpr int kE = 8;   // column elements per lane kept in registers
+static constexpr double kDropRel = 1e-6;   // QRCP stop level relative to eps (see svd_core)
 
 // diagnostics: -DHM_PHASE_TIMING prints per-phase SM cycles of CTA 0
 #ifdef HM_PHASE_TIMING
@@ -304,7 +306,15 @@ __device__ void svd_core(const SvdJob& J, double eps, bool tr, int L, int c, dou
   double part = 0.0;
   for (int j = tid; j < c; j += NT) part += nrm[j];
   const double fro2 = bsum(part, red);
-  const double delta2 = (16.0 * kUs * kUs) * (double)c * fro2;
+  // QRCP stop / Jacobi skip level delta = max(4 u sqrt(c), kDropRel eps) ||M||_F
+  // (reading R7c).  The dropped trailing block E = Q [0 0; 0 R22] P^T
+  // satisfies M'^T E = 0 for the kept M', so M^T M = M'^T M' + E^T E: every
+  // sigma_i^2 moves by <= ||E||^2 <= delta^2 = 1e-12 eps^2 ||M||^2, far inside
+  // the near-threshold window of the rank rule (1e-10 eps ||M||, R16), and
+  // the represented matrix by <= 1e-6 eps ||M||_F (<= 1e-10 relative at the
+  // configs' eps, under the 1e-9 parity bar).
+  const double drop = fmax(16.0 * kUs * kUs * (double)c, (kDropRel * eps) * (kDropRel * eps));
+  const double delta2 = drop * fro2;
   PHASE("norms");
   // ---------------------------------------------------------------- 1. QRCP
   // Two barriers per step at most: every warp finds the pivot itself (argmax of
