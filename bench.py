@@ -106,6 +106,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def max_over_ranks(ms, device=None):
+    """Device time of the timed region as the MAX over ranks (replicas: the
+    job ends when the slowest rank ends).  Single process: unchanged."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(ms)
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_value(world_size, flops_per_rank_step, ms_per_step):
+    """`value` = the units ALL ranks processed / the (max-over-ranks) time:
+    every replica runs the same product, so ws x its convention flops."""
+    return world_size * flops_per_rank_step / (ms_per_step * 1e-3) / 1e9
+
+
 def measure_dgemm_tflops(torch, dev):
     n = 8192
     a = torch.randn(n, n, dtype=torch.float64, device=dev)
@@ -239,12 +257,9 @@ def run_ours(args, cfg):
     launches = ctx.last_stats()["kernel_launches"] - l0
     prof = ctx.profile_get()
     ctx.profile(False)
-    if ws > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dev)
     ms_step = ms / args.steps
-    value = ws * flops / (ms_step * 1e-3) / 1e9
+    value = whole_job_value(ws, flops, ms_step)
 
     # ---- end to end through the C-ABI with host buffers
     dX, dY, dZ = X.export(), Y.export(), G.export()

@@ -884,7 +884,10 @@ void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int 
   // few stacks (latency-bound, e.g. the H-LR critical path): 512 threads so
   // every Jacobi pair of a round is in flight; many stacks: 256 (two CTAs/SM)
   static const int tsmall = [] { const char* e = std::getenv("HM_TS_THREADS"); return e ? std::atoi(e) : 0; }();
-  int threads = njobs < 296 ? 512 : 256;
+  // the 26 K bucket (208 KB) fits one CTA per SM whatever the batch: 512
+  // threads (ncu: 256-thread CTAs left it at 12 % achieved occupancy)
+  static const int t26 = [] { const char* e = std::getenv("HM_TS26_THREADS"); return e ? std::atoi(e) : 512; }();
+  int threads = njobs < 296 ? 512 : (cap > 10 * 1024 ? t26 : 256);
   if (tsmall > 0 && njobs >= 296 && cap <= 4 * 1024) threads = tsmall;
   k_trunc_small<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps);
 }
@@ -899,7 +902,9 @@ void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream
     attr = true;
   }
   if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
-  const int threads = (cap == 0 || cap > 8 * 1024 || njobs < 296) ? 512 : 256;
+  static const int tg = [] { const char* e = std::getenv("HM_SVDG_THREADS"); return e ? std::atoi(e) : 512; }();
+  int threads = (cap == 0 || cap > 8 * 1024 || njobs < 296) ? 512 : 256;
+  if (cap == 0) threads = tg;   // global workspace: no shared-memory limit on CTAs per SM
   count_launch();
   k_svd<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, cap);
 }
