@@ -126,18 +126,22 @@ __device__ __forceinline__ void store_acc(const EvalJob& J, int orow, int ocol, 
 __device__ __forceinline__ void stage_v(const EvalJob& J, int vrow, int p0, int pc, int j0, int wc, double* Vs,
                                         int& brs, int& bcs) {
   const int tid = threadIdx.x;
+  const int pcp = (pc + 3) & ~3;   // rows [pc, pcp) zero (read by the k loop); columns >= wc and rows >= pcp
+                                   // are left stale: they only reach output columns that are discarded
   if (!J.vtrans) {   // p contiguous in global: Vs[p + j * 68]
-    for (int e = tid; e < kT * kW; e += kNT) {
-      const int p = e % kT, j = e / kT;
-      const bool ok = p < pc && j < wc;
+    for (int e = tid; e < kT * wc; e += kNT) {
+      const int p = e & (kT - 1), j = e >> 6;
+      if (p >= pcp) continue;
+      const bool ok = p < pc;
       cp8(Vs + p + j * kLd, ok ? J.V + (vrow + p0 + p) + (int64_t)(j0 + j) * J.ldv : J.V, ok);
     }
     brs = 1;
     bcs = kLd;
   } else {           // j contiguous in global: Vs[j + p * 36]
-    for (int e = tid; e < kT * kW; e += kNT) {
-      const int j = e % kW, p = e / kW;
-      const bool ok = p < pc && j < wc;
+    for (int e = tid; e < kW * pcp; e += kNT) {
+      const int j = e & (kW - 1), p = e >> 5;
+      if (j >= wc) continue;
+      const bool ok = p < pc;
       cp8(Vs + j + p * kLdJ, ok ? J.V + (j0 + j) + (int64_t)(vrow + p0 + p) * J.ldv : J.V, ok);
     }
     brs = kLdJ;
@@ -155,20 +159,23 @@ __device__ void dense_tiles(const EvalJob& J, const LeafDesc& L, int orow, int v
     double acc[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
     acc_zero<8, NCT>(acc);
     for (int p0 = 0; p0 < ko; p0 += kT) {
-      const int pc = min(kT, ko - p0);
+      const int pc = min(kT, ko - p0), pcp = (pc + 3) & ~3;
       int ars, acs, brs, bcs;
+      // S: rows >= mc stale (their output rows are discarded), k columns [pc, pcp) zero
       if (!J.trans) {   // op(N)(i, p) = N(i, p), i contiguous: S[i + p * 68]
-        for (int e = tid; e < kT * kT; e += kNT) {
-          const int i = e % kT, p = e / kT;
-          const bool ok = i < mc && p < pc;
+        for (int e = tid; e < kT * pcp; e += kNT) {
+          const int i = e & (kT - 1), p = e >> 6;
+          if (i >= mc) continue;
+          const bool ok = p < pc;
           cp8(S + i + p * kLd, ok ? L.A + (i0 + i) + (int64_t)(p0 + p) * ldn : L.A, ok);
         }
         ars = 1;
         acs = kLd;
       } else {          // op(N)(i, p) = N(p, i), p contiguous: S[p + i * 68]
-        for (int e = tid; e < kT * kT; e += kNT) {
-          const int p = e % kT, i = e / kT;
-          const bool ok = i < mc && p < pc;
+        for (int e = tid; e < kT * mc; e += kNT) {
+          const int p = e & (kT - 1), i = e >> 6;
+          if (p >= pcp) continue;
+          const bool ok = p < pc;
           cp8(S + p + i * kLd, ok ? L.A + (p0 + p) + (int64_t)(i0 + i) * ldn : L.A, ok);
         }
         ars = kLd;
@@ -199,11 +206,13 @@ template <int NCT>
 __device__ void apply_f1_t(const EvalJob& J, const double* F1, int ld1, int mo, int q0, int kc, int orow, int ocol,
                            int j0, int wc, double* S, const double* Ts) {
   const int tid = threadIdx.x;
+  const int kcp = (kc + 3) & ~3;
   for (int i0 = 0; i0 < mo; i0 += kT) {
     const int mc = min(kT, mo - i0);
-    for (int e = tid; e < kT * kW; e += kNT) {   // S[i + q * 68] = F1(i0 + i, q0 + q)
-      const int i = e % kT, q = e / kT;
-      const bool ok = i < mc && q < kc;
+    for (int e = tid; e < kT * kcp; e += kNT) {   // S[i + q * 68] = F1(i0 + i, q0 + q)
+      const int i = e & (kT - 1), q = e >> 6;
+      if (i >= mc) continue;
+      const bool ok = q < kc;
       cp8(S + i + q * kLd, ok ? F1 + (i0 + i) + (int64_t)(q0 + q) * ld1 : F1, ok);
     }
     cp_wait();
@@ -232,10 +241,12 @@ __device__ void lowrank_t(const EvalJob& J, const double* F2, int ld2, int ko, i
   const int tid = threadIdx.x;
   double acc[WT::RTW * WT::CTW][2];
   acc_zero<4, NCT>(acc);
+  const int kcp = (kc + 3) & ~3;   // T rows [kc, kcp) are zero; rows >= kcp are never read
   for (int p0 = 0; p0 < ko; p0 += kT) {
-    const int pc = min(kT, ko - p0);
-    for (int e = tid; e < kT * kW; e += kNT) {
-      const int p = e % kT, q = e / kT;
+    const int pc = min(kT, ko - p0), pcp = (pc + 3) & ~3;
+    for (int e = tid; e < kT * kcp; e += kNT) {
+      const int p = e & (kT - 1), q = e >> 6;
+      if (p >= pcp) continue;
       const bool ok = p < pc && q < kc;
       cp8(S + p + q * kLd, ok ? F2 + (p0 + p) + (int64_t)(q0 + q) * ld2 : F2, ok);
     }
@@ -324,9 +335,11 @@ __device__ void eval_identity(const EvalJob& J, const LeafDesc& L, int orow, int
     const int wc = min(kW, ko - j0);
     for (int q0 = 0; q0 < L.k; q0 += kW) {
       const int kc = min(kW, L.k - q0);
-      for (int e = tid; e < kW * kW; e += kNT) {   // Ts(q, j) = F2(j0 + j, q0 + q) at j + q * 36
-        const int j = e % kW, q = e / kW;
-        const bool ok = j < wc && q < kc;
+      const int kcp = (kc + 3) & ~3;
+      for (int e = tid; e < kW * kcp; e += kNT) {   // Ts(q, j) = F2(j0 + j, q0 + q) at j + q * 36
+        const int j = e & (kW - 1), q = e >> 5;
+        if (j >= wc) continue;
+        const bool ok = q < kc;
         cp8(Ts + j + q * kLdJ, ok ? F2 + (j0 + j) + (int64_t)(q0 + q) * ld2 : F2, ok);
       }
       cp_wait();

@@ -315,7 +315,9 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
   }
   if (cap > 24 * 1024) cap = 24 * 1024;
   count_launch();
-  static const int occ3 = [] { const char* e = std::getenv("HM_QR_OCC3"); return e ? std::atoi(e) : 1; }();
+  // <256, 3> (80 registers) spills ~650 B per thread: measured slower on B200
+  // (6 K bucket 133 -> 177 ms per cfg-4 product), so off unless HM_QR_OCC3=1
+  static const int occ3 = [] { const char* e = std::getenv("HM_QR_OCC3"); return e ? std::atoi(e) : 0; }();
   // <= 12 K doubles (96 KB): 256 threads, two or three CTAs per SM (measured on
   // B200: the 768-row bucket 194 -> 165 ms per cfg-4 product vs one 512-thread CTA)
   if (cap <= 6 * 1024 && occ3) k_qr_blocked<256, 3><<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, cap);
