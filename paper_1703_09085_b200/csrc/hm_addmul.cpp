@@ -445,8 +445,14 @@ struct Planner {
       if (cj.empty()) return;
       double cb = 0;
       for (auto& j : cj) cb += 16.0 * j.rows * (j.identity ? 1 : j.cols);
+      std::vector<int> tmap((size_t)ctiles);
+      for (size_t j = 0; j < cj.size(); j++) {
+        const int64_t t1 = j + 1 < cj.size() ? cj[j + 1].tile0 : ctiles;
+        std::fill(tmap.begin() + cj[j].tile0, tmap.begin() + t1, (int)j);
+      }
       ProfScope ps(c, PC_COPY, 0, cb);
-      launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
+      const CopyJob* dj = scratch.upload(cj);
+      launch_copy_mapped(dj, (int)cj.size(), scratch.upload(tmap), ctiles, c->stream);
       HM_CHECK_LAUNCH();
       cj.clear();
       ctiles = 0;

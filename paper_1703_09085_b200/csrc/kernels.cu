@@ -325,9 +325,11 @@ void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st
 // SVD kernels: see svd.cu
 
 // ------------------------------------------------------------------ copy
-__global__ void __launch_bounds__(256) k_copy(const CopyJob* __restrict__ jobs, int njobs) {
+// tmap (optional): job index of every tile (host-built; one load instead of a
+// binary search of dependent loads per CTA)
+__global__ void __launch_bounds__(256) k_copy(const CopyJob* __restrict__ jobs, int njobs, const int* __restrict__ tmap) {
   const int64_t tile = blockIdx.x;
-  const CopyJob& J = jobs[find_job(jobs, njobs, tile)];
+  const CopyJob& J = jobs[tmap ? tmap[tile] : find_job(jobs, njobs, tile)];
   const int mt = (J.rows + 31) >> 5;
   const int64_t local = tile - J.tile0;
   const int ti = (int)(local % mt), tj = (int)(local / mt);
@@ -351,7 +353,13 @@ __global__ void __launch_bounds__(256) k_copy(const CopyJob* __restrict__ jobs, 
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
   count_launch();
-  k_copy<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs);
+  k_copy<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, nullptr);
+}
+
+void launch_copy_mapped(const CopyJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st) {
+  if (njobs <= 0 || ntiles <= 0) return;
+  count_launch();
+  k_copy<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, d_tmap);
 }
 
 // ------------------------------------------------------------------ eval

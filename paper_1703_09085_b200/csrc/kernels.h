@@ -174,6 +174,7 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
+void launch_copy_mapped(const CopyJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
 void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st);
 void launch_eval2(const EvalJob* d_jobs, int njobs, cudaStream_t st);   // eval.cu (shared-memory tiles)
 void launch_trsm2(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, const LeafDesc* leaves,

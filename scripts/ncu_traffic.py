@@ -31,7 +31,7 @@ def main(path, out):
         else:
             v *= SCALE_B.get(unit, 1.0)
         per[r[ii]][metric] = v
-        names[r[ii]] = r[ki].split("(")[0].replace("hm::", "")
+        names[r[ii]] = r[ki].split("(")[0].replace("hm::", "").replace("void ", "")
     agg = collections.defaultdict(lambda: {"launches": 0, "ms": 0.0, "dram_bytes": 0.0})
     for lid, m in per.items():
         a = agg[names[lid]]
