@@ -9,6 +9,8 @@ def summarise(path):
     i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr, data = rows[i], rows[i + 1:]
     ki, ui, vi = hdr.index("Kernel Name"), hdr.index("Metric Unit"), hdr.index("Metric Value")
+    ni = hdr.index("Metric Name")
+    data = [r for r in data if len(r) > ni and r[ni] == "gpu__time_duration.sum"]
     scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in data:
