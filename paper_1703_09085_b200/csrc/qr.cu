@@ -45,7 +45,8 @@ __device__ __forceinline__ double wsum(double v) {
 // Instantiated per launch shape (the body reads blockDim.x): <512, 1> for
 // the 24 K-double buckets (one CTA per SM by shared memory), <256, 2> for
 // 12 K, <256, 3> for 6 K -- register caps that let that many CTAs share an SM.
-template <int kThreads, int kMinBlocks>
+// kRB: trailing-update rows per lane in flight (x 2 columns).
+template <int kThreads, int kMinBlocks, int kRB>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
   extern __shared__ double Vs[];            // panel / V (rows x nb), column-major
   __shared__ double T[kNbMax * kNbMax];     // upper triangular, column-major
@@ -216,14 +217,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
       double w0[kNbMax], w1[kNbMax];
 #pragma unroll
       for (int q = 0; q < kNbMax; q++) w0[q] = w1[q] = 0.0;
-      // rows in blocks of 4 per lane: 8 global loads in flight per lane
+      // rows in blocks of kRB per lane: 2 kRB global loads in flight per lane
       int i = lane;
-      for (; i + 96 < rows; i += 128) {
-        double x0[4], x1[4];
+      for (; i + 32 * (kRB - 1) < rows; i += 32 * kRB) {
+        double x0[kRB], x1[kRB];
 #pragma unroll
-        for (int u = 0; u < 4; u++) { x0[u] = a0[i + 32 * u]; x1[u] = a1[i + 32 * u]; }
+        for (int u = 0; u < kRB; u++) { x0[u] = a0[i + 32 * u]; x1[u] = a1[i + 32 * u]; }
 #pragma unroll
-        for (int u = 0; u < 4; u++)
+        for (int u = 0; u < kRB; u++)
 #pragma unroll
           for (int q = 0; q < kNbMax; q++)
             if (q < kb) {
@@ -259,12 +260,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
         w1[q] = s1;
       }
       i = lane;
-      for (; i + 96 < rows; i += 128) {
-        double x0[4], x1[4];
+      for (; i + 32 * (kRB - 1) < rows; i += 32 * kRB) {
+        double x0[kRB], x1[kRB];
 #pragma unroll
-        for (int u = 0; u < 4; u++) { x0[u] = a0[i + 32 * u]; x1[u] = a1[i + 32 * u]; }
+        for (int u = 0; u < kRB; u++) { x0[u] = a0[i + 32 * u]; x1[u] = a1[i + 32 * u]; }
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < kRB; u++) {
           double s0 = 0.0, s1 = 0.0;
 #pragma unroll
           for (int q = 0; q < kNbMax; q++)
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
           x1[u] -= s1;
         }
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < kRB; u++) {
           a0[i + 32 * u] = x0[u];
           if (two) a1[i + 32 * u] = x1[u];
         }
@@ -304,25 +305,32 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 #endif
 }
 
-void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
-  if (njobs <= 0) return;
+template <int kThreads, int kMinBlocks>
+static void launch_qr_variant(const QrJob* d_jobs, int njobs, int cap, int rb, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_qr_blocked<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * 1024 * 8);
-    cudaFuncSetAttribute(k_qr_blocked<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 1024 * 8);
-    cudaFuncSetAttribute(k_qr_blocked<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 1024 * 8);
+    const int bytes = (kThreads == 512 ? 24 : (kMinBlocks == 2 ? 12 : 6)) * 1024 * 8;
+    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
+  if (rb == 8) k_qr_blocked<kThreads, kMinBlocks, 8><<<njobs, kThreads, (size_t)cap * 8, st>>>(d_jobs, cap);
+  else k_qr_blocked<kThreads, kMinBlocks, 4><<<njobs, kThreads, (size_t)cap * 8, st>>>(d_jobs, cap);
+}
+
+void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
+  if (njobs <= 0) return;
   if (cap > 24 * 1024) cap = 24 * 1024;
   count_launch();
   // <256, 3> (80 registers) spills ~650 B per thread: measured slower on B200
   // (6 K bucket 133 -> 177 ms per cfg-4 product), so off unless HM_QR_OCC3=1
   static const int occ3 = [] { const char* e = std::getenv("HM_QR_OCC3"); return e ? std::atoi(e) : 0; }();
-  // <= 12 K doubles (96 KB): 256 threads, two or three CTAs per SM (measured on
-  // B200: the 768-row bucket 194 -> 165 ms per cfg-4 product vs one 512-thread CTA)
-  if (cap <= 6 * 1024 && occ3) k_qr_blocked<256, 3><<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, cap);
-  else if (cap <= 12 * 1024) k_qr_blocked<256, 2><<<njobs, 256, (size_t)cap * 8, st>>>(d_jobs, cap);
-  else k_qr_blocked<512, 1><<<njobs, 512, (size_t)cap * 8, st>>>(d_jobs, cap);
+  static const int rb = [] { const char* e = std::getenv("HM_QR_RB"); return e ? std::atoi(e) : 4; }();
+  // <= 12 K doubles (96 KB): 256 threads, two CTAs per SM (measured on B200:
+  // the 768-row bucket 194 -> 165 ms per cfg-4 product vs one 512-thread CTA)
+  if (cap <= 6 * 1024 && occ3) launch_qr_variant<256, 3>(d_jobs, njobs, cap, rb, st);
+  else if (cap <= 12 * 1024) launch_qr_variant<256, 2>(d_jobs, njobs, cap, rb, st);
+  else launch_qr_variant<512, 1>(d_jobs, njobs, cap, rb, st);
 }
 
 }  // namespace hm
