@@ -548,7 +548,7 @@ struct Planner {
     }
     if (!gj.empty()) {
       ProfScope ps(c, PC_DENSE, fl_dense - fl_dense0, by_dense - by_dense0);
-      launch_gemm(scratch.upload(gj), (int)gj.size(), gtiles, c->stream);
+      launch_gemm_mapped(scratch.upload(gj), (int)gj.size(), scratch.tile_map(gj, gtiles), gtiles, c->stream);
       HM_CHECK_LAUNCH();
     }
     double t3 = now_s();
@@ -691,7 +691,7 @@ struct Planner {
         }
         {
           ProfScope ps(c, PC_COPY, 0, 0);
-          launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
+          launch_copy_mapped(scratch.upload(cj), (int)cj.size(), scratch.tile_map(cj, ctiles), ctiles, c->stream);
           HM_CHECK_LAUNCH();
         }
         std::vector<TruncReq> tr;
@@ -758,7 +758,7 @@ struct Planner {
       add_copy(cj, ctiles, nB[b], f.ldb, f.B, f.ldb, f.ldb, f.k, 0, 0, 1.0);
     }
     Arena scratch(c);
-    launch_copy(scratch.upload(cj), (int)cj.size(), ctiles, c->stream);
+    launch_copy_mapped(scratch.upload(cj), (int)cj.size(), scratch.tile_map(cj, ctiles), ctiles, c->stream);
     HM_CHECK_LAUNCH();
     HM_CUDA(cudaStreamSynchronize(c->stream));
     scratch.release();
@@ -1106,9 +1106,9 @@ struct Factorizer {
     }
     n_trsm += (int64_t)jobs.size();
     ProfScope ps(c, PC_TRSM, 0, 0);
-    if (!pre.empty()) launch_copy(ar.upload(pre), (int)pre.size(), pt, c->stream);
+    if (!pre.empty()) launch_copy_mapped(ar.upload(pre), (int)pre.size(), ar.tile_map(pre, pt), pt, c->stream);
     if (!jobs.empty()) trsm_launch(ar.upload(jobs), (int)jobs.size(), ar.upload(st), dlt, c->stream);
-    if (!post.empty()) launch_copy(ar.upload(post), (int)post.size(), qt, c->stream);
+    if (!post.empty()) launch_copy_mapped(ar.upload(post), (int)post.size(), ar.tile_map(post, qt), qt, c->stream);
     HM_CHECK_LAUNCH();
   }
 
@@ -1315,7 +1315,7 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
       cj.push_back(CopyJob{G->pA[b], nullptr, m, 0, m, m, 0, 1, 1, shift, tiles});
       tiles += (int64_t)((m + 31) / 32) * ((m + 31) / 32);
     }
-    launch_copy(ar.upload(cj), (int)cj.size(), tiles, c->stream);
+    launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, c->stream);
     HM_CHECK_LAUNCH();
   }
   c->sp_prepare();

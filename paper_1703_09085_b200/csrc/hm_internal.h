@@ -111,6 +111,19 @@ struct Arena {
     HM_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     return d;
   }
+  // job index of every tile of a tiled launch (jobs carry a prefix-summed
+  // tile0), uploaded next to the jobs: one load per CTA instead of a binary
+  // search of dependent loads
+  template <class J>
+  const int* tile_map(const std::vector<J>& v, int64_t ntiles) {
+    if (v.empty() || ntiles <= 0) return nullptr;
+    std::vector<int> m((size_t)ntiles);
+    for (size_t j = 0; j < v.size(); j++) {
+      const int64_t t1 = j + 1 < v.size() ? v[j + 1].tile0 : ntiles;
+      for (int64_t t = v[j].tile0; t < t1; t++) m[(size_t)t] = (int)j;
+    }
+    return upload(m);
+  }
   void release();
 };
 

@@ -116,8 +116,15 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   // chunk remains.  Same factorisation A = Q R (Q = blockdiag(Q_chunks) Q_stack,
   // R = the last level's R), but the single-CTA row sweep over thousands of
   // rows becomes nch independent CTAs.
-  static const int ts_min = [] { const char* e = std::getenv("HM_TSQR_ROWS"); return e ? std::atoi(e) : 1536; }();
-  static const int ts_h = [] { const char* e = std::getenv("HM_TSQR_H"); return e ? std::atoi(e) : 768; }();
+  static const int ts_min_b = [] { const char* e = std::getenv("HM_TSQR_ROWS"); return e ? std::atoi(e) : 1536; }();
+  static const int ts_h_b = [] { const char* e = std::getenv("HM_TSQR_H"); return e ? std::atoi(e) : 768; }();
+  // small batches (latency-bound, e.g. the H-LR critical path) may cut tall
+  // factors into more, shorter chunks (more CTAs on one QR)
+  static const int ts_min_l = [] { const char* e = std::getenv("HM_TSQR_ROWS_LAT"); return e ? std::atoi(e) : 1536; }();
+  static const int ts_h_l = [] { const char* e = std::getenv("HM_TSQR_H_LAT"); return e ? std::atoi(e) : 768; }();
+  const bool lat_batch = nj < 64;
+  const int ts_min = lat_batch ? ts_min_l : ts_min_b;
+  const int ts_h = lat_batch ? ts_h_l : ts_h_b;
   struct TsLevel { double* V; int rows, ld, h, nch; double* tau; size_t xoff; double* X; int ldx; double* T; };
   struct TsPlan { int job, side, l, kcap; std::vector<TsLevel> lv; };
   std::vector<TsPlan> ts;
@@ -242,7 +249,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
           qj.push_back(QrJob{U.V + r0, cr, P.l, U.ld, U.tau + (size_t)ch * P.l, chunkT(U, ch, cr, P.l)});
         }
       }
-      launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
+      launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
       launch_qr_set(qj);
     }
     HM_CHECK_LAUNCH();
@@ -285,7 +292,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   }
   {
     ProfScope ps(c, PC_GEMM_M, fl_m, 0);
-    launch_gemm(ar.upload(gj), (int)gj.size(), tiles, st);
+    launch_gemm_mapped(ar.upload(gj), (int)gj.size(), ar.tile_map(gj, tiles), tiles, st);
     HM_CHECK_LAUNCH();
   }
   if (const char* dm = std::getenv("HM_DUMP_M")) {   // diagnostics: first job's M (tall orientation)
@@ -426,7 +433,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       int64_t tiles = 0;
       for (const TsPlan& P : ts)
         add_copy(cj, tiles, P.lv.back().X, P.lv.back().ldx, P.lv[0].X, P.lv[0].ldx, P.l, P.kcap, 0);
-      launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
+      launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
       for (size_t lvl = maxdepth - 1; lvl >= 1; lvl--) {
         std::vector<ApplyQJob> tq;
         cj.clear();
@@ -448,7 +455,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
           }
         }
         launch_applyq(ar.upload(tq), (int)tq.size(), cmax(tq), st);
-        launch_copy(ar.upload(cj), (int)cj.size(), tiles, st);
+        launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
       }
     }
     if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), cmax(aq), st);

@@ -58,11 +58,11 @@ __device__ __forceinline__ int find_job(const J* jobs, int njobs, int64_t tile) 
 
 // ------------------------------------------------------------------ GEMM
 // 64x64 output tile per CTA, K chunks of 16, 256 threads x (4x4) outputs.
-__global__ void __launch_bounds__(256) k_gemm(const GemmJob* __restrict__ jobs, int njobs) {
+__global__ void __launch_bounds__(256) k_gemm(const GemmJob* __restrict__ jobs, int njobs, const int* __restrict__ tmap) {
   __shared__ double As[16][64 + 1];
   __shared__ double Bs[16][64 + 1];
   const int64_t tile = blockIdx.x;
-  const GemmJob& J = jobs[find_job(jobs, njobs, tile)];
+  const GemmJob& J = jobs[tmap ? tmap[tile] : find_job(jobs, njobs, tile)];
   const int m = J.m;
   const int n = J.ndyn ? *J.ndyn : J.n;
   const int k = J.kdyn ? *J.kdyn : J.k;
@@ -130,7 +130,13 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmJob* __restrict__ jobs, 
 void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
   count_launch();
-  k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs);
+  k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, nullptr);
+}
+
+void launch_gemm_mapped(const GemmJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st) {
+  if (njobs <= 0 || ntiles <= 0) return;
+  count_launch();
+  k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, d_tmap);
 }
 
 // ------------------------------------------------------------------ QR

@@ -169,6 +169,7 @@ struct NormJob {
 };
 
 void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
+void launch_gemm_mapped(const GemmJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
 void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
 void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);   // rows <= 24576
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);

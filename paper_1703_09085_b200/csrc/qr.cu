@@ -328,7 +328,11 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
   static const int rb = [] { const char* e = std::getenv("HM_QR_RB"); return e ? std::atoi(e) : 4; }();
   // <= 12 K doubles (96 KB): 256 threads, two CTAs per SM (measured on B200:
   // the 768-row bucket 194 -> 165 ms per cfg-4 product vs one 512-thread CTA)
-  if (cap <= 6 * 1024 && occ3) launch_qr_variant<256, 3>(d_jobs, njobs, cap, rb, st);
+  // fewer jobs than SMs (latency-bound, e.g. the H-LR critical path): 512
+  // threads per QR whatever the bucket
+  static const int lat = [] { const char* e = std::getenv("HM_QR_LAT512"); return e ? std::atoi(e) : 1; }();
+  if (lat && njobs < 148) launch_qr_variant<512, 1>(d_jobs, njobs, cap, rb, st);
+  else if (cap <= 6 * 1024 && occ3) launch_qr_variant<256, 3>(d_jobs, njobs, cap, rb, st);
   else if (cap <= 12 * 1024) launch_qr_variant<256, 2>(d_jobs, njobs, cap, rb, st);
   else launch_qr_variant<512, 1>(d_jobs, njobs, cap, rb, st);
 }
