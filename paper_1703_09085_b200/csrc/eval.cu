@@ -382,6 +382,92 @@ __global__ void __launch_bounds__(kNT, 3) k_eval2(const EvalJob* __restrict__ jo
   }
 }
 
+// ------------------------------------------------------------------ GEMM
+// C = alpha op(A) op(B) + beta C on the FP64 tensor pipe: one 64 x 64 output
+// tile per CTA (host tile map), K chunks of 16 staged by cp.async in the
+// orientation that keeps both the global loads coalesced and the DMMA
+// fragment loads conflict-free (leading dimensions 68 / 20 = 4 mod 16);
+// warp (rg, cg) owns rows 16 rg .. +16 and columns 32 cg .. +32 (2 x 4 tiles).
+// Stored-upper masks (R factors sharing storage with reflectors) read as 0.
+__global__ void __launch_bounds__(256) k_gemm2(const GemmJob* __restrict__ jobs, const int* __restrict__ tmap) {
+  __shared__ __align__(16) double As[64 * 20];
+  __shared__ __align__(16) double Bs[64 * 20];
+  const int64_t tile = blockIdx.x;
+  const GemmJob& J = jobs[tmap[tile]];
+  const int m = J.m;
+  const int n = J.ndyn ? *J.ndyn : J.n;
+  const int k = J.kdyn ? *J.kdyn : J.k;
+  const int mt = (m + 63) >> 6;
+  const int64_t local = tile - J.tile0;
+  const int ti = (int)(local % mt), tj = (int)(local / mt);
+  if (tj * 64 >= n || ti * 64 >= m) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3, rg = warp & 3, cg = warp >> 2;
+  const int ars = J.transA ? 20 : 1, acs = J.transA ? 1 : kLd;
+  const int brs = J.transB ? kLd : 1, bcs = J.transB ? 1 : 20;
+  double acc[2][4][2];
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int c = 0; c < 4; c++) acc[r][c][0] = acc[r][c][1] = 0.0;
+  for (int p0 = 0; p0 < k; p0 += 16) {
+    for (int e = tid; e < 1024; e += 256) {
+      int i, p;
+      double* dst;
+      if (!J.transA) { i = e & 63; p = e >> 6; dst = As + i + p * kLd; }
+      else { p = e & 15; i = e >> 4; dst = As + p + i * 20; }
+      const int gi = ti * 64 + i, gp = p0 + p;
+      const int r = J.transA ? gp : gi, c = J.transA ? gi : gp;
+      const bool ok = gi < m && gp < k && !(J.maskA && r > c);
+      cp8(dst, ok ? J.A + r + (int64_t)c * J.lda : J.A, ok);
+    }
+    for (int e = tid; e < 1024; e += 256) {
+      int j, p;
+      double* dst;
+      if (J.transB) { j = e & 63; p = e >> 6; dst = Bs + j + p * kLd; }
+      else { p = e & 15; j = e >> 4; dst = Bs + p + j * 20; }
+      const int gj = tj * 64 + j, gp = p0 + p;
+      const int r = J.transB ? gj : gp, c = J.transB ? gp : gj;
+      const bool ok = gj < n && gp < k && !(J.maskB && r > c);
+      cp8(dst, ok ? J.B + r + (int64_t)c * J.ldb : J.B, ok);
+    }
+    cp_wait();
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 4) {
+      double a[2], b[4];
+#pragma unroll
+      for (int r = 0; r < 2; r++) a[r] = As[(rg * 16 + r * 8 + lr) * ars + (kk + lk) * acs];
+#pragma unroll
+      for (int c = 0; c < 4; c++) b[c] = Bs[(kk + lk) * brs + (cg * 32 + c * 8 + lr) * bcs];
+#pragma unroll
+      for (int r = 0; r < 2; r++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) dmma(acc[r][c], a[r], b[c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    const int gi = ti * 64 + rg * 16 + r * 8 + lr;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int gj = tj * 64 + cg * 32 + c * 8 + 2 * lk + h;
+        if (gj >= n) continue;
+        double* d = J.C + gi + (int64_t)gj * J.ldc;
+        const double v = J.alpha * acc[r][c][h];
+        *d = (J.beta == 0.0) ? v : fma(J.beta, *d, v);
+      }
+  }
+}
+
+void launch_gemm2(const GemmJob* d_jobs, const int* d_tmap, int64_t ntiles, cudaStream_t st) {
+  k_gemm2<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, d_tmap);
+}
+
 // ------------------------------------------------------------------ TRSM
 // Triangular solve through the H-structure on one thin panel per CTA (host
 // step lists, see kernels.h): (a) V[r0:r0+m, :] <- T^-1 V with T a dense

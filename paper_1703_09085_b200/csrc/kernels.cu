@@ -11,6 +11,8 @@
 
 #include <atomic>
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace hm {
@@ -133,10 +135,14 @@ void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t 
   k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, nullptr);
 }
 
+void launch_gemm2(const GemmJob* d_jobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);   // eval.cu (DMMA)
+
 void launch_gemm_mapped(const GemmJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
   count_launch();
-  k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, d_tmap);
+  static const bool old = std::getenv("HM_GEMM_OLD") != nullptr;
+  if (old || !d_tmap) k_gemm<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, d_tmap);
+  else launch_gemm2(d_jobs, d_tmap, ntiles, st);
 }
 
 // ------------------------------------------------------------------ QR
