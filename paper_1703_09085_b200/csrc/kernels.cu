@@ -328,10 +328,17 @@ __global__ void __launch_bounds__(256, 3) k_applyq(const ApplyQJob* __restrict__
   }
 }
 
-void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st) {
+void launch_applyq2(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);   // eval.cu (DMMA)
+
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st, bool all_T) {
   if (njobs <= 0 || cmax <= 0) return;
   count_launch();
-  k_applyq<<<dim3(njobs, (cmax + 7) / 8), 256, 0, st>>>(d_jobs);
+  // k_applyq2 (DMMA, one CTA per job and 32 columns) measured slower on B200
+  // (169 vs 106 ms per cfg-4 product: one dependent DMMA chain per warp over
+  // all rows, fewer CTAs); opt in with HM_APPLYQ2=1
+  static const bool use2 = std::getenv("HM_APPLYQ2") != nullptr;
+  if (all_T && use2) launch_applyq2(d_jobs, njobs, cmax, st);
+  else k_applyq<<<dim3(njobs, (cmax + 7) / 8), 256, 0, st>>>(d_jobs);
 }
 
 // SVD kernels: see svd.cu

@@ -172,7 +172,8 @@ void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t 
 void launch_gemm_mapped(const GemmJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
 void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
 void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);   // rows <= 24576
-void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
+// all_T: every job carries its compact-WY T factors (then the DMMA k_applyq2 runs)
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st, bool all_T = false);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_copy_mapped(const CopyJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
