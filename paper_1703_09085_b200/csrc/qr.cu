@@ -40,18 +40,26 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
+// D(8x8) += A(8x4) B(4x8), FP64 tensor pipe (DMMA.8x8x4); fragments as in eval.cu
+__device__ __forceinline__ void dmma_qr(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
 }  // namespace
 
 // Instantiated per launch shape (the body reads blockDim.x): <512, 1> for
 // the 24 K-double buckets (one CTA per SM by shared memory), <256, 2> for
 // 12 K, <256, 3> for 6 K -- register caps that let that many CTAs share an SM.
 // kRB: trailing-update rows per lane in flight (x 2 columns).
-template <int kThreads, int kMinBlocks, int kRB>
+template <int kThreads, int kMinBlocks, int kRB, bool kDmmaTrail>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
   extern __shared__ double Vs[];            // panel / V (rows x nb), column-major
   __shared__ double T[kNbMax * kNbMax];     // upper triangular, column-major
-  __shared__ double G[kNbMax * kNbMax];     // V^T V
-  __shared__ double red2[2 * 16 * kNbMax];  // per-warp partial sums (<= 16 warps), double-buffered
+  __shared__ double G[2 * kNbMax * kNbMax];   // V^T V; the -T^T W block (16 x 32) of the DMMA update
+  __shared__ double red2[kThreads >= 512 ? 4 * 16 * kNbMax : 2 * 16 * kNbMax];  // per-warp partial sums
+                                            // (double-buffered); the W partials of the DMMA update
   __shared__ double piv[2 * kNbMax];        // pivot row of the current column, double-buffered
   __shared__ double stau[kNbMax];
   const QrJob J = jobs[blockIdx.x];
@@ -59,15 +67,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
   double* A = J.A;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
   int nb = kNbMax;
-  while (nb > 1 && (int64_t)m * nb > cap) nb >>= 1;
+  while (nb > 1 && (int64_t)(m + 15) * nb > cap) nb >>= 1;
   QT_INIT;
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int kb = min(nb, n - k0);
     const int rows = m - k0;
+    // panel leading dimension = 4 (mod 16) for the DMMA trailing update
+    // (conflict-free fragment loads); unpadded for the FFMA update
+    const int ldp = kDmmaTrail ? rows + ((4 - (rows & 15)) & 15) : rows;
     // 1. load panel
     for (int64_t e = tid; e < (int64_t)rows * kb; e += NT) {
       const int i = (int)(e % rows), j = (int)(e / rows);
-      Vs[e] = A[(k0 + i) + (int64_t)(k0 + j) * lda];
+      Vs[i + (int64_t)j * ldp] = A[(k0 + i) + (int64_t)(k0 + j) * lda];
     }
     __syncthreads();
     // 2. unblocked Householder on the panel (in shared memory), ONE barrier per
@@ -78,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
     //    itself.  red / piv are double-buffered by the parity of j.
     for (int j = 0; j < kb; j++) {
       const int nc = kb - j;               // slot 0: x.x ; slot q: x.y_{j+q}
-      const double* x = Vs + (int64_t)j * rows;
+      const double* x = Vs + (int64_t)j * ldp;
       double part[kNbMax];
 #pragma unroll
       for (int q = 0; q < kNbMax; q++) part[q] = 0.0;
@@ -87,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
         const double xi = x[i];
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
-          if (q < nc) part[q] = fma(xi, Vs[i + (int64_t)(j + q) * rows], part[q]);
+          if (q < nc) part[q] = fma(xi, Vs[i + (int64_t)(j + q) * ldp], part[q]);
       }
       double* rb = red2 + (j & 1) * (16 * kNbMax);
       double* pv = piv + (j & 1) * kNbMax;
@@ -121,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
       if (tid == j % NT) {
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
-          if (q < nc) pv[q] = Vs[j + (int64_t)(j + q) * rows];
+          if (q < nc) pv[q] = Vs[j + (int64_t)(j + q) * ldp];
       }
       __syncthreads();
       // lane q of every warp totals slot q over the warps (loads issued together)
@@ -149,31 +160,31 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
       for (int q = 1; q < kNbMax; q++) d[q] = __shfl_sync(0xffffffffu, dq, q);
       if (tid == 0) { J.tau[k0 + j] = t; stau[j] = t; }
       if (tid == j % NT) {
-        Vs[j + (int64_t)j * rows] = beta;
+        Vs[j + (int64_t)j * ldp] = beta;
 #pragma unroll
         for (int q = 1; q < kNbMax; q++)
-          if (q < nc) Vs[j + (int64_t)(j + q) * rows] = pv[q] - d[q];
+          if (q < nc) Vs[j + (int64_t)(j + q) * ldp] = pv[q] - d[q];
       }
       if (t != 0.0)
         for (int i = i0; i < rows; i += NT) {
-          const double vi = Vs[i + (int64_t)j * rows] * sc;
-          Vs[i + (int64_t)j * rows] = vi;
+          const double vi = Vs[i + (int64_t)j * ldp] * sc;
+          Vs[i + (int64_t)j * ldp] = vi;
 #pragma unroll
           for (int q = 1; q < kNbMax; q++)
-            if (q < nc) Vs[i + (int64_t)(j + q) * rows] -= d[q] * vi;
+            if (q < nc) Vs[i + (int64_t)(j + q) * ldp] -= d[q] * vi;
         }
     }
     __syncthreads();
     // 3. write the panel (R + reflectors) back; make V explicit (unit diagonal, zero above)
     for (int64_t e = tid; e < (int64_t)rows * kb; e += NT) {
       const int i = (int)(e % rows), j = (int)(e / rows);
-      A[(k0 + i) + (int64_t)(k0 + j) * lda] = Vs[e];
+      A[(k0 + i) + (int64_t)(k0 + j) * lda] = Vs[i + (int64_t)j * ldp];
     }
     __syncthreads();
     for (int64_t e = tid; e < (int64_t)kb * kb; e += NT) {
       const int i = (int)(e % kb), j = (int)(e / kb);
-      if (i < j) Vs[i + (int64_t)j * rows] = 0.0;
-      else if (i == j) Vs[i + (int64_t)j * rows] = 1.0;
+      if (i < j) Vs[i + (int64_t)j * ldp] = 0.0;
+      else if (i == j) Vs[i + (int64_t)j * ldp] = 1.0;
     }
     __syncthreads();
     QT_MARK(qt_panel);
@@ -185,8 +196,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
     for (int pr = warp; pr < kb * kb; pr += NW) {
       const int a = pr % kb, b = pr / kb;
       if (a >= b) continue;
-      const double* va = Vs + (int64_t)a * rows;
-      const double* vb = Vs + (int64_t)b * rows;
+      const double* va = Vs + (int64_t)a * ldp;
+      const double* vb = Vs + (int64_t)b * ldp;
       double d = 0.0;
       for (int i = b + lane; i < rows; i += 32) d = fma(va[i], vb[i], d);   // va, vb zero above b
       d = wsum(d);
@@ -208,6 +219,91 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
       for (int e = tid; e < kNbMax * kNbMax; e += NT) J.T[(int64_t)(k0 / kNbMax) * kNbMax * kNbMax + e] = T[e];
     QT_MARK(qt_t);
     if (ncol <= 0) continue;
+    if (kDmmaTrail) {
+      // 5'. trailing update on the FP64 tensor pipe, 32 columns at a time:
+      //     W = V^T A (warp t owns the 8x8 tile (qt, ct) of the 16 x 32 block, the
+      //     two warp groups of a 512-thread CTA split the rows), Zn = -T^T W,
+      //     A += V Zn (8-row tiles round-robin over the warps)
+      double* Wp = red2;
+      double* Zn = G;
+      const int NWG = NW >> 3;
+      const int lr = lane >> 2, lk = lane & 3;
+      double* At = A + k0 + (int64_t)(k0 + kb) * lda;
+      for (int cb = 0; cb < ncol; cb += 32) {
+        const int wcb = min(32, ncol - cb);
+        {
+          const int t = warp & 7, g = warp >> 3;
+          const int qt = t & 1, ct = t >> 1;
+          const int q = qt * 8 + lr, jc = ct * 8 + lr;
+          const bool qok = q < kb, cok = jc < wcb;
+          const double* vq = Vs + (int64_t)q * ldp;
+          const double* ac = At + (int64_t)(cb + (cok ? jc : 0)) * lda;
+          double d[2] = {0.0, 0.0};
+#pragma unroll 4
+          for (int i0 = 4 * g; i0 < rows; i0 += 4 * NWG) {
+            const int i = i0 + lk;
+            const double a = (qok && i < rows) ? vq[i] : 0.0;
+            const double b = (cok && i < rows) ? ac[i] : 0.0;
+            dmma_qr(d, a, b);
+          }
+          if (g < NWG) {
+            double* w = Wp + g * 512;
+            w[q + (ct * 8 + 2 * lk) * 16] = d[0];
+            w[q + (ct * 8 + 2 * lk + 1) * 16] = d[1];
+          }
+        }
+        __syncthreads();
+        for (int e = tid; e < 512; e += NT) {   // Zn(q, j) = -sum_{r <= q} T(r, q) W(r, j)
+          const int q = e & 15, j = e >> 4;
+          double sacc = 0.0;
+          if (q < kb)
+            for (int r = 0; r <= q; r++) {
+              double wv = Wp[r + j * 16];
+              if (NWG > 1) wv += Wp[512 + r + j * 16];
+              sacc = fma(T[r + q * kNbMax], wv, sacc);
+            }
+          Zn[q + j * 16] = -sacc;
+        }
+        __syncthreads();
+        {
+          double bz[4][4];
+#pragma unroll
+          for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+            for (int ks = 0; ks < 4; ks++) bz[ct][ks] = Zn[(ks * 4 + lk) + (ct * 8 + lr) * 16];
+          const int nrt = (rows + 7) >> 3;
+          for (int rt = warp; rt < nrt; rt += NW) {
+            const int i = rt * 8 + lr;
+            double a[4];
+#pragma unroll
+            for (int ks = 0; ks < 4; ks++) {
+              const int q = ks * 4 + lk;
+              a[ks] = (q < kb && i < rows) ? Vs[i + (int64_t)q * ldp] : 0.0;
+            }
+#pragma unroll
+            for (int ct = 0; ct < 4; ct++) {
+              if (ct * 8 >= wcb) break;   // warp-uniform
+              double d[2];
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const int j = ct * 8 + 2 * lk + h;
+                d[h] = (i < rows && j < wcb) ? At[i + (int64_t)(cb + j) * lda] : 0.0;
+              }
+#pragma unroll
+              for (int ks = 0; ks < 4; ks++) dmma_qr(d, a[ks], bz[ct][ks]);
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const int j = ct * 8 + 2 * lk + h;
+                if (i < rows && j < wcb) At[i + (int64_t)(cb + j) * lda] = d[h];
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      QT_MARK(qt_trail);
+      continue;
+    }
     // 5. trailing update, one warp per PAIR of columns (each V element read
     //    from shared memory feeds two FMAs): a <- a - V (T^T (V^T a))
     for (int c2 = 2 * warp; c2 < ncol; c2 += 2 * NW) {
@@ -228,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 #pragma unroll
           for (int q = 0; q < kNbMax; q++)
             if (q < kb) {
-              const double v = Vs[i + 32 * u + q * rows];
+              const double v = Vs[i + 32 * u + q * ldp];
               w0[q] = fma(v, x0[u], w0[q]);
               w1[q] = fma(v, x1[u], w1[q]);
             }
@@ -238,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
           if (q < kb) {
-            const double v = Vs[i + q * rows];
+            const double v = Vs[i + q * ldp];
             w0[q] = fma(v, x0, w0[q]);
             w1[q] = fma(v, x1, w1[q]);
           }
@@ -270,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 #pragma unroll
           for (int q = 0; q < kNbMax; q++)
             if (q < kb) {
-              const double v = Vs[i + 32 * u + q * rows];
+              const double v = Vs[i + 32 * u + q * ldp];
               s0 = fma(v, w0[q], s0);
               s1 = fma(v, w1[q], s1);
             }
@@ -288,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 #pragma unroll
         for (int q = 0; q < kNbMax; q++)
           if (q < kb) {
-            const double v = Vs[i + q * rows];
+            const double v = Vs[i + q * ldp];
             s0 = fma(v, w0[q], s0);
             s1 = fma(v, w1[q], s1);
           }
@@ -307,15 +403,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 
 template <int kThreads, int kMinBlocks>
 static void launch_qr_variant(const QrJob* d_jobs, int njobs, int cap, int rb, cudaStream_t st) {
+  // +256 doubles: the panel leading dimension is padded to 4 (mod 16)
+  const int capx = cap + 256;
   static bool attr = false;
   if (!attr) {
-    const int bytes = (kThreads == 512 ? 24 : (kMinBlocks == 2 ? 12 : 6)) * 1024 * 8;
-    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    const int bytes = ((kThreads == 512 ? 24 : (kMinBlocks == 2 ? 12 : 6)) * 1024 + 256) * 8;
+    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
-  if (rb == 8) k_qr_blocked<kThreads, kMinBlocks, 8><<<njobs, kThreads, (size_t)cap * 8, st>>>(d_jobs, cap);
-  else k_qr_blocked<kThreads, kMinBlocks, 4><<<njobs, kThreads, (size_t)cap * 8, st>>>(d_jobs, cap);
+  // DMMA trailing update: measured faster only for the 384-row bucket with
+  // 256 threads (133 -> 115 ms per cfg-4 product); 768 rows +4 %, 1536 rows and
+  // the 512-thread latency mode (one dependent DMMA chain per warp over all
+  // rows) slower -- the FFMA column-pair update stays there
+  static const int dm = [] { const char* e = std::getenv("HM_QR_DMMA"); return e ? std::atoi(e) : 1; }();
+  if (dm && kThreads == 256 && cap <= 6 * 1024) k_qr_blocked<kThreads, kMinBlocks, 4, true><<<njobs, kThreads, (size_t)capx * 8, st>>>(d_jobs, capx);
+  else if (rb == 8) k_qr_blocked<kThreads, kMinBlocks, 8, false><<<njobs, kThreads, (size_t)capx * 8, st>>>(d_jobs, capx);
+  else k_qr_blocked<kThreads, kMinBlocks, 4, false><<<njobs, kThreads, (size_t)capx * 8, st>>>(d_jobs, capx);
 }
 
 void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
