@@ -49,7 +49,7 @@ FACTOR_RUNS = [
 # profile class -> kernel (for the ncu traffic lookup)
 CLASS_KERNEL = {"eval": "k_eval2", "apply_q": "k_applyq", "copy": "k_copy", "memset": None,
                 "trunc_fused": "k_trunc_small", "gemm_M": "k_gemm", "dense_add": "k_gemm",
-                "qr_blk384": "k_qr_blocked<256, 2, 4>", "qr_blk768": "k_qr_blocked<256, 2, 4>", "qr_blk1536": "k_qr_blocked<512, 1, 4>",
+                "qr_blk384": "k_qr_blocked<256, 2, 4, 1>", "qr_blk768": "k_qr_blocked<256, 2, 4, 0>", "qr_blk1536": "k_qr_blocked<512, 1, 4, 0>",
                 "svd_smem26k": "k_svd", "svd_global": "k_svd", "svd_smem8k": "k_svd", "svd_smem3k": "k_svd"}
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA: SMs x FMA/clk x 2 x max clock
 
