@@ -57,9 +57,11 @@ template <int kThreads, int kMinBlocks, int kRB, bool kDmmaTrail>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob* __restrict__ jobs, int cap) {
   extern __shared__ double Vs[];            // panel / V (rows x nb), column-major
   __shared__ double T[kNbMax * kNbMax];     // upper triangular, column-major
-  __shared__ double G[2 * kNbMax * kNbMax];   // V^T V; the -T^T W block (16 x 32) of the DMMA update
-  __shared__ double red2[kThreads >= 512 ? 4 * 16 * kNbMax : 2 * 16 * kNbMax];  // per-warp partial sums
-                                            // (double-buffered); the W partials of the DMMA update
+  // (the DMMA variant needs more: G holds the -T^T W block (16 x 32), red2 the
+  // W partials; the FFMA variants keep the smaller footprint -> more L1)
+  __shared__ double G[kDmmaTrail ? 2 * kNbMax * kNbMax : kNbMax * kNbMax];   // V^T V
+  __shared__ double red2[kDmmaTrail && kThreads >= 512 ? 4 * 16 * kNbMax : 2 * 16 * kNbMax];  // per-warp
+                                            // partial sums (<= 16 warps), double-buffered
   __shared__ double piv[2 * kNbMax];        // pivot row of the current column, double-buffered
   __shared__ double stau[kNbMax];
   const QrJob J = jobs[blockIdx.x];
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
   double* A = J.A;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
   int nb = kNbMax;
-  while (nb > 1 && (int64_t)(m + 15) * nb > cap) nb >>= 1;
+  while (nb > 1 && (int64_t)(m + (kDmmaTrail ? 15 : 0)) * nb > cap) nb >>= 1;
   QT_INIT;
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int kb = min(nb, n - k0);
@@ -403,8 +405,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 
 template <int kThreads, int kMinBlocks>
 static void launch_qr_variant(const QrJob* d_jobs, int njobs, int cap, int rb, cudaStream_t st) {
-  // +256 doubles: the panel leading dimension is padded to 4 (mod 16)
-  const int capx = cap + 256;
+  static const int dm = [] { const char* e = std::getenv("HM_QR_DMMA"); return e ? std::atoi(e) : 1; }();
+  const bool use_dmma = dm && kThreads == 256 && cap <= 6 * 1024;
+  // +256 doubles: the DMMA variant pads the panel leading dimension to 4 (mod 16)
+  const int capx = cap + (use_dmma ? 256 : 0);
   static bool attr = false;
   if (!attr) {
     const int bytes = ((kThreads == 512 ? 24 : (kMinBlocks == 2 ? 12 : 6)) * 1024 + 256) * 8;
@@ -417,8 +421,7 @@ static void launch_qr_variant(const QrJob* d_jobs, int njobs, int cap, int rb, c
   // 256 threads (133 -> 115 ms per cfg-4 product); 768 rows +4 %, 1536 rows and
   // the 512-thread latency mode (one dependent DMMA chain per warp over all
   // rows) slower -- the FFMA column-pair update stays there
-  static const int dm = [] { const char* e = std::getenv("HM_QR_DMMA"); return e ? std::atoi(e) : 1; }();
-  if (dm && kThreads == 256 && cap <= 6 * 1024) k_qr_blocked<kThreads, kMinBlocks, 4, true><<<njobs, kThreads, (size_t)capx * 8, st>>>(d_jobs, capx);
+  if (use_dmma) k_qr_blocked<kThreads, kMinBlocks, 4, true><<<njobs, kThreads, (size_t)capx * 8, st>>>(d_jobs, capx);
   else if (rb == 8) k_qr_blocked<kThreads, kMinBlocks, 8, false><<<njobs, kThreads, (size_t)capx * 8, st>>>(d_jobs, capx);
   else k_qr_blocked<kThreads, kMinBlocks, 4, false><<<njobs, kThreads, (size_t)capx * 8, st>>>(d_jobs, capx);
 }
