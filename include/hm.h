@@ -15,8 +15,18 @@
  *     tree position -> original point index.
  *   - Device pointers passed in are BORROWED (caller-owned, e.g. a torch
  *     tensor's data_ptr()) and must stay valid until the stream passes the
- *     call.  Every hm_mat and all internal pools are OWNED by the context
- *     and released by hm_free / hm_ctx_destroy.
+ *     call.  Every hm_mat and all internal pools are OWNED by the context:
+ *     an hm_mat is released by hm_free, and hm_ctx_destroy releases every
+ *     hm_mat still alive in the context (their handles become invalid).
+ *     All device memory of the library comes from the allocator hook, or,
+ *     without one, from a PRIVATE stream-ordered pool of the context (the
+ *     device's default pool is not modified); hm_ctx_destroy returns it.
+ *   - Truncation (TRUNC_eps): the rank k is the smallest k with
+ *     sum_{i>k} s_i^2 <= eps^2 sum_i s_i^2 (relative Frobenius, local to the
+ *     block, no rank cap; k = 0 for a zero matrix).  Of the two returned
+ *     factors exactly ONE is orthonormal: the one on the SHORT side of the
+ *     matrix the SVD runs on (see hm_test_trunc_batched); the other carries
+ *     the singular values.  Only the represented matrix A B^T is specified.
  *   - Calls are stream-ordered on the context's stream.  Calls that return
  *     host data (hm_build, hm_import, hm_export, hm_stats, hm_addmul's rank
  *     bookkeeping) synchronize the stream.
@@ -130,7 +140,8 @@ typedef struct {
   int32_t count;
 } hm_prof_t;
 
-/* Device memory hook; NULL -> cudaMallocAsync/cudaFreeAsync on the stream. */
+/* Device memory hook (stream-ordered: alloc/free are called with the
+ * context's stream); NULL -> a private cudaMemPool of the context. */
 typedef struct {
   void* (*alloc)(size_t bytes, void* stream, void* user);
   void (*free)(void* ptr, size_t bytes, void* stream, void* user);
@@ -215,9 +226,15 @@ hm_status hm_profile_get(hm_ctx ctx, hm_prof_t* out);
  * Test-only export: batched TRUNC_eps of independent stacks (kernel-level
  * parity).  For job i: A_i (m_i x l_i, ld m_i) at a_dev + a_off[i],
  * B_i (n_i x l_i) at b_dev + b_off[i] (device, CONSUMED: overwritten);
- * results U_k (m_i x k) at ua_dev + o_off[i] (ld m_i) and V_k S_k
- * (n_i x k) at ub_dev + p_off[i] (ld n_i) with capacity min(m,n,l)
- * columns; ranks_host[i] = k.  Offsets are host arrays in doubles.
+ * results A'_i (m_i x k) at ua_dev + o_off[i] (ld m_i) and B'_i (n_i x k)
+ * at ub_dev + p_off[i] (ld n_i), capacity min(m,n,l) columns, with
+ * A'_i B'_i^T = the eps-truncated SVD of A_i B_i^T; ranks_host[i] = k,
+ * sigma_host (optional) the singular values.  Which factor is orthonormal:
+ * the SVD runs on M = R_A R_B^T (or A R_B^T / R_A B^T when only one side is
+ * QR'd), stored in its tall orientation; the factor belonging to the short
+ * side of M is orthonormal (U_k on the A side if M has fewer rows than
+ * columns, V_k on the B side otherwise), the other one is scaled by the
+ * singular values (reading R7c).  Offsets are host arrays in doubles.
  */
 hm_status hm_test_trunc_batched(hm_ctx ctx, int njobs, const int32_t* m, const int32_t* n,
                                 const int32_t* l, double* a_dev, const int64_t* a_off,

@@ -6,7 +6,7 @@ area area_i).  Config 3 (Cholesky) uses (G + G^T)/2.
 The paper's own matrices are Galerkin SLP/DLP via HCA (P:L1571-1585, §7);
 this collocation matrix stands in for them.
 
-Pinned by tests/test_oracle_basic.py (hand-computed entries, symmetry of the
+Pinned by tests/test_oracle_inputs_trees.py (hand-computed entries, symmetry of the
 symmetrised variant, diagonal formula).
 """
 from __future__ import annotations

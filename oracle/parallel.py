@@ -112,7 +112,7 @@ def addmul_s2_parallel(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps, workers=N
 
     descend(acc, ZReal(Z, root), frontier_depth)
     _G.update(items=items, X=X, Y=Y, Z=Z, eps=eps)
-    count, cols, near, addp = ctx.count, ctx.cols, list(ctx.near), alg.st.addproduct
+    count, cols, near, addp = ctx.count, ctx.cols, [(n[1], n[2]) for n in ctx.near], alg.st.addproduct
     with mp.get_context("fork").Pool(workers) as pool:
         for i, out, c, l, nr, ap in pool.imap_unordered(_flush_worker, range(len(items))):
             for bid, v in out.items():
@@ -124,4 +124,5 @@ def addmul_s2_parallel(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps, workers=N
             cols += l
             near += nr
             addp += ap
+    # near: (tag, k) of every near-threshold truncation (tags carry the (t, r) cluster ids)
     return Z, dict(truncations=count, trunc_cols=cols, near=near, addproduct=addp, frontier=len(items))

@@ -13,7 +13,7 @@ algorithms", P:L252):
 Ids are assigned in breadth-first order, so every level is contiguous and
 the sons of a node are consecutive.
 
-Pinned by tests/test_oracle_trees.py: hand-executed bisection of collinear
+Pinned by tests/test_oracle_inputs_trees.py: hand-executed bisection of collinear
 points, brute-force classification of every (t,s) pair, partition /
 tiling invariants, eq. blocktree_admissible, product-tree membership.
 """

@@ -468,103 +468,6 @@ void launch_gemm2(const GemmJob* d_jobs, const int* d_tmap, int64_t ntiles, cuda
   k_gemm2<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, d_tmap);
 }
 
-// ------------------------------------------------------------------ apply Q
-// X <- Q X, Q = prod_p (I - Y_p T_p Y_p^T) (compact-WY panels of 16 reflectors
-// from k_qr_blocked, last panel first), one CTA per (job, 32 columns of X):
-// W = Y_p^T X and X -= Y_p (T_p W) on the FP64 tensor pipe.  The reflector
-// panel is read once per CTA and panel (the warp-per-column k_applyq reads it
-// once per column); Y_p is the unit lower-trapezoidal panel below row j0.
-__device__ __forceinline__ double yref(const double* Vp, int ldv, int i, int q, int j0, int kb, int m) {
-  if (q >= kb || i >= m || i < j0 + q) return 0.0;
-  return i == j0 + q ? 1.0 : Vp[i + (int64_t)q * ldv];
-}
-
-__global__ void __launch_bounds__(256) k_applyq2(const ApplyQJob* __restrict__ jobs) {
-  __shared__ double Ws[16 * 32];
-  __shared__ double Ts[256];
-  const ApplyQJob J = jobs[blockIdx.x];
-  const int c = J.cdyn ? *J.cdyn : J.c;
-  const int c0 = blockIdx.y * 32;
-  if (c0 >= c) return;
-  const int wc = min(32, c - c0);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lr = lane >> 2, lk = lane & 3;
-  const int m = J.m, ldv = J.ldv, ldx = J.ldx;
-  double* X = J.X + (int64_t)c0 * ldx;
-  for (int p = (J.r + 15) / 16 - 1; p >= 0; p--) {
-    const int j0 = p * 16, kb = min(16, J.r - j0);
-    const double* Vp = J.V + (int64_t)j0 * ldv;
-    Ts[tid] = J.T[256 * p + tid];
-    // pass 1: W (16 x 32) = Y^T X, warp (qt, ct) owns the 8 x 8 tile (qt, ct)
-    {
-      const int qt = warp & 1, ct = warp >> 1;
-      const int q = qt * 8 + lr, jc = ct * 8 + lr;
-      const bool cok = jc < wc;
-      const double* xc = X + (int64_t)(cok ? jc : 0) * ldx;
-      double d[2] = {0.0, 0.0};
-#pragma unroll 4
-      for (int i0 = j0; i0 < m; i0 += 4) {
-        const int i = i0 + lk;
-        const double a = yref(Vp, ldv, i, q, j0, kb, m);
-        const double b = (cok && i < m) ? xc[i] : 0.0;
-        dmma(d, a, b);
-      }
-      Ws[(qt * 8 + lr) + (ct * 8 + 2 * lk) * 16] = d[0];
-      Ws[(qt * 8 + lr) + (ct * 8 + 2 * lk + 1) * 16] = d[1];
-    }
-    __syncthreads();
-    // Z = -T W (T upper: Z(q, j) = -sum_{r >= q} T(q, r) W(r, j)), 2 entries per thread
-    double z[2];
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int q = tid & 15, j = (tid >> 4) + 16 * h;
-      double s = 0.0;
-      for (int r = q; r < kb; r++) s = fma(Ts[q + r * 16], Ws[r + j * 16], s);
-      z[h] = q < kb ? -s : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int h = 0; h < 2; h++) Ws[(tid & 15) + ((tid >> 4) + 16 * h) * 16] = z[h];
-    __syncthreads();
-    // pass 2: X += Y Z over row tiles of 8 rows from j0, warps round-robin
-    {
-      double bz[4][4];
-#pragma unroll
-      for (int ct = 0; ct < 4; ct++)
-#pragma unroll
-        for (int ks = 0; ks < 4; ks++) bz[ct][ks] = Ws[(ks * 4 + lk) + (ct * 8 + lr) * 16];
-      const int nrt = (m - j0 + 7) >> 3;
-      for (int rt = warp; rt < nrt; rt += 8) {
-        const int i = j0 + rt * 8 + lr;
-        double a[4];
-#pragma unroll
-        for (int ks = 0; ks < 4; ks++) a[ks] = yref(Vp, ldv, j0 + rt * 8 + lr, ks * 4 + lk, j0, kb, m);
-#pragma unroll
-        for (int ct = 0; ct < 4; ct++) {
-          if (ct * 8 >= wc) break;   // warp-uniform
-          double d[2];
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int j = ct * 8 + 2 * lk + h;
-            d[h] = (i < m && j < wc) ? X[i + (int64_t)j * ldx] : 0.0;
-          }
-#pragma unroll
-          for (int ks = 0; ks < 4; ks++) dmma(d, a[ks], bz[ct][ks]);
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int j = ct * 8 + 2 * lk + h;
-            if (i < m && j < wc) X[i + (int64_t)j * ldx] = d[h];
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-void launch_applyq2(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st) {
-  k_applyq2<<<dim3(njobs, (cmax + 31) / 32), 256, 0, st>>>(d_jobs);
-}
-
 // ------------------------------------------------------------------ TRSM
 // Triangular solve through the H-structure on one thin panel per CTA (host
 // step lists, see kernels.h): (a) V[r0:r0+m, :] <- T^-1 V with T a dense
@@ -651,22 +554,14 @@ __global__ void __launch_bounds__(kNT) k_trsm2(const TrsmJob* __restrict__ jobs,
 
 void launch_trsm2(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, const LeafDesc* leaves, cudaStream_t st) {
   if (njobs <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_trsm2, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmShared * 8);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_trsm2, kTrsmShared * 8);
   count_launch();
   k_trsm2<<<njobs, kNT, (size_t)kTrsmShared * 8, st>>>(d_jobs, d_steps, leaves);
 }
 
 void launch_eval2(const EvalJob* d_jobs, int njobs, cudaStream_t st) {
   if (njobs <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_eval2, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem * 8);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_eval2, kSmem * 8);
   count_launch();
   k_eval2<<<njobs, kNT, (size_t)kSmem * 8, st>>>(d_jobs);
 }

@@ -459,8 +459,7 @@ struct Planner {
     };
     auto flush_eval = [&]() {
       if (ej.empty()) return;
-      static const bool old_eval = std::getenv("HM_EVAL_OLD") != nullptr;
-      if (!old_eval) split_evals(ej);
+      split_evals(ej);
       // largest first (index sort: the jobs themselves are moved once)
       std::vector<int> order(ej.size());
       std::iota(order.begin(), order.end(), 0);
@@ -486,8 +485,7 @@ struct Planner {
       ProfScope ps(c, PC_EVAL, fl_eval - fl_eval0, by_eval - by_eval0);
       fl_eval0 = fl_eval;
       by_eval0 = by_eval;
-      if (old_eval) launch_eval(scratch.upload(sorted), (int)sorted.size(), c->stream);
-      else launch_eval2(scratch.upload(sorted), (int)sorted.size(), c->stream);
+      launch_eval2(scratch.upload(sorted), (int)sorted.size(), c->stream);
       HM_CHECK_LAUNCH();
     };
     for (auto& s : stacks) {
@@ -850,9 +848,7 @@ struct Planner {
 // goes through the Planner above, triangular solves through the H-structure
 // run as one k_trsm CTA per panel, dense diagonal leaves as k_leaf_factor.
 static void trsm_launch(const TrsmJob* j, int n, const TrsmStep* st, const LeafDesc* lv, cudaStream_t s) {
-  static const bool old_trsm = std::getenv("HM_TRSM_OLD") != nullptr;
-  if (old_trsm) launch_trsm(j, n, st, lv, s);
-  else launch_trsm2(j, n, st, lv, s);
+  launch_trsm2(j, n, st, lv, s);
 }
 
 struct Factorizer {
@@ -1305,6 +1301,12 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
   const Tree& T = *G->tree;
   if (T.bl_kind[0] != HM_BLOCK_SUB && T.bl_kind[0] != HM_BLOCK_DENSE)
     throw Error(HM_ESTRUCT, "hm_lr/hm_chol: the root block must not be admissible");
+  // k_leaf_factor keeps a diagonal leaf in shared memory (m^2 doubles <= 200 KB)
+  for (int t = 0; t < T.nclusters(); t++)
+    if (T.cl_nsons[t] == 0 && T.cl_size[t] > kMaxLeafFactor)
+      throw Error(HM_EUNSUPPORTED, "hm_lr/hm_chol: leaf cluster " + std::to_string(t) + " has " +
+                                       std::to_string(T.cl_size[t]) + " rows (diagonal leaf factorization supports <= " +
+                                       std::to_string(kMaxLeafFactor) + ")");
   if (shift != 0.0) {
     Arena ar(c);
     std::vector<CopyJob> cj;

@@ -163,13 +163,20 @@ hm_status hm_ctx_create(int device, void* cuda_stream, const hm_allocator* alloc
     int major = 0;
     HM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
     if (major != 10) throw Error(HM_EUNSUPPORTED, "libhm is built for sm_100a (B200) only");
-    // keep freed stream-ordered allocations cached in the pool: every level of
-    // hm_addmul allocates and frees its stacks, and re-mapping tens of GB per
-    // level would dominate the run time.
-    cudaMemPool_t pool;
-    HM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    HM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // a PRIVATE stream-ordered pool that keeps freed allocations cached: every
+    // level of hm_addmul allocates and frees its stacks, and re-mapping tens of
+    // GB per level would dominate the run time.  The device's default pool (the
+    // one torch and other cudaMallocAsync users see) is left untouched; the
+    // private pool's memory is returned by hm_ctx_destroy.
+    if (!c->c.has_alloc) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      HM_CUDA(cudaMemPoolCreate(&c->c.pool, &props));
+      uint64_t thr = UINT64_MAX;
+      HM_CUDA(cudaMemPoolSetAttribute(c->c.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
   });
   if (s != HM_OK) {
     delete c;
@@ -181,9 +188,18 @@ hm_status hm_ctx_create(int device, void* cuda_stream, const hm_allocator* alloc
 
 hm_status hm_ctx_destroy(hm_ctx ctx) {
   if (!ctx) return HM_EINVAL;
+  cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   ctx->c.prof_collect();
   for (auto e : ctx->c.free_events) cudaEventDestroy(e);
+  // every hm_mat of the context is released here (include/hm.h): handles
+  // become invalid
+  for (void* p : ctx->c.live) {
+    auto* m = static_cast<hm_mat_s*>(p);
+    m->m.free_all(&ctx->c);
+    delete m;
+  }
+  ctx->c.live.clear();
   delete ctx;
   return HM_OK;
 }
@@ -208,6 +224,7 @@ hm_status hm_import(hm_ctx ctx, const hm_host_desc* d, hm_mat* out) {
       delete M;
       throw;
     }
+    ctx->c.live.insert(M);
     *out = M;
   });
 }
@@ -365,6 +382,7 @@ hm_status hm_clone(hm_ctx ctx, hm_mat src, hm_mat* out) {
         M->m.pA[b] = dp + (S.pA[b] - d0);
       }
     }
+    ctx->c.live.insert(M);
     *out = M;
   });
 }
@@ -372,6 +390,7 @@ hm_status hm_clone(hm_ctx ctx, hm_mat src, hm_mat* out) {
 hm_status hm_free(hm_ctx ctx, hm_mat m) {
   if (!ctx || !m) return HM_EINVAL;
   return guard(ctx, [&] {
+    if (!ctx->c.live.erase(m)) throw Error(HM_EINVAL, "hm_free: matrix does not belong to this context");
     m->m.free_all(&ctx->c);
     delete m;
   });
@@ -397,6 +416,7 @@ hm_status hm_build(hm_ctx ctx, const double* pts_host, const double* area_host, 
     auto* H = new hm_mat_s;
     H->m = std::move(*M);
     delete M;
+    ctx->c.live.insert(H);
     *out = H;
   });
 }

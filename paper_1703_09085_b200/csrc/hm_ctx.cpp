@@ -36,22 +36,21 @@ void* Ctx::pinned(size_t bytes) {
 }
 
 Ctx::~Ctx() {
+  cudaSetDevice(device);
+  if (ws) dfree(ws, ws_cap * sizeof(double));
+  if (sp) dfree(sp, sp_cap);
+  cudaStreamSynchronize(stream);
   if (pin) cudaFreeHost(pin);
-  if (ws) cudaFree(ws);
-  if (sp) cudaFree(sp);
+  if (pool) cudaMemPoolDestroy(pool);
 }
 
 double* Ctx::stack_ws(size_t ndoubles) {
   if (ndoubles > ws_cap) {
-    if (ws) cudaFreeAsync(ws, stream);
+    if (ws) dfree(ws, ws_cap * sizeof(double));
     ws = nullptr;
+    ws_cap = 0;
     const size_t cap = std::max(ndoubles + ndoubles / 8, (size_t)1 << 24);
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), cap * sizeof(double), stream);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      ws_cap = 0;
-      throw Error(HM_ENOMEM, "stack workspace (" + std::to_string(cap * 8) + " B): " + cudaGetErrorString(e));
-    }
+    ws = static_cast<double*>(dmalloc(cap * sizeof(double)));   // throws HM_ENOMEM
     ws_cap = cap;
   }
   return ws;
@@ -65,7 +64,7 @@ void* Ctx::dmalloc(size_t bytes) {
     if (!p) throw Error(HM_ENOMEM, "device allocation hook failed (" + std::to_string(bytes) + " B)");
     return p;
   }
-  cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, bytes, pool, stream) : cudaMallocAsync(&p, bytes, stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Error(HM_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
@@ -125,12 +124,16 @@ void Ctx::prof_collect() {
 
 void Ctx::sp_prepare() {
   if (sp_hwm > sp_cap) {
-    if (sp) cudaFreeAsync(sp, stream);
+    if (sp) dfree(sp, sp_cap);
     sp = nullptr;
     sp_cap = 0;
     const size_t cap = sp_hwm + sp_hwm / 8;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&sp), cap, stream) == cudaSuccess) sp_cap = cap;
-    else cudaGetLastError();
+    try {
+      sp = static_cast<char*>(dmalloc(cap));
+      sp_cap = cap;
+    } catch (const Error&) {   // the arenas fall back to per-chunk allocations
+      sp = nullptr;
+    }
   }
   sp_top = 0;
   sp_hwm = 0;

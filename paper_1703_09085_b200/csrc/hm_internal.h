@@ -4,6 +4,7 @@
 
 #include <cstring>
 #include <memory>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -48,6 +49,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   hm_allocator alloc{};
   bool has_alloc = false;
+  cudaMemPool_t pool = nullptr;   // private stream-ordered pool (no allocator hook)
+  std::set<void*> live;            // hm_mat handles owned by this context
   std::string err;
   hm_stats_t last{};
   // profiling
@@ -79,6 +82,8 @@ struct Ctx {
   void sp_prepare();   // call when no stack-mode arena is live
   ~Ctx();
 
+  // every device allocation of the library goes through these two (allocator
+  // hook if given, else the private pool)
   void* dmalloc(size_t bytes);
   void dfree(void* p, size_t bytes);
   cudaEvent_t get_event();

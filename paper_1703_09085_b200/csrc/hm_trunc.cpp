@@ -416,17 +416,12 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   }
   {
     ProfScope ps(c, PC_APPLYQ, 0, 0);
-    auto allT = [](const std::vector<ApplyQJob>& v) {
-      for (const ApplyQJob& j : v)
-        if (!j.T) return false;
-      return true;
-    };
     auto cmax = [](const std::vector<ApplyQJob>& v) {
       int m = 0;
       for (const ApplyQJob& j : v) m = std::max(m, j.c);
       return m;
     };
-    if (!aq1.empty()) launch_applyq(ar.upload(aq1), (int)aq1.size(), cmax(aq1), st, allT(aq1));
+    if (!aq1.empty()) launch_applyq(ar.upload(aq1), (int)aq1.size(), cmax(aq1), st);
     if (!ts.empty()) {
       // TSQR: X_top[0:l] = output[0:l] (the SVD's factor), zeros below; then per
       // level (top down) X_j <- blockdiag(Q_j) X_j and scatter its l-row blocks
@@ -459,11 +454,11 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
             add_copy(cj, tiles, D.X + r0, D.ldx, U.X + (size_t)ch * P.l, U.ldx, P.l, P.kcap, 0);
           }
         }
-        launch_applyq(ar.upload(tq), (int)tq.size(), cmax(tq), st, allT(tq));
+        launch_applyq(ar.upload(tq), (int)tq.size(), cmax(tq), st);
         launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
       }
     }
-    if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), cmax(aq), st, allT(aq));
+    if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), cmax(aq), st);
     HM_CHECK_LAUNCH();
   }
 }

@@ -10,6 +10,11 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <tuple>
 
 #include <cstdlib>
 
@@ -21,6 +26,22 @@ static constexpr double kU = 1.1102230246251565e-16;  // unit roundoff 2^-53
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void ensure_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;   // (function, device, bytes)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(func, dev, bytes);
+  if (done.count(key)) return;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error(std::string("cudaFuncSetAttribute(MaxDynamicSharedMemorySize): ") + cudaGetErrorString(e));
+  }
+  done.insert(key);
+}
 int64_t launch_count() { return g_launches.load(); }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -213,14 +234,9 @@ int qr_smem_capacity() { return 24 * 1024; }
 
 void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st) {
   if (njobs <= 0) return;
-  static bool attr = false;
   if (cap > qr_smem_capacity()) cap = qr_smem_capacity();
   const size_t bytes = (size_t)cap * sizeof(double);
-  if (!attr) {
-    cudaFuncSetAttribute(k_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         qr_smem_capacity() * 8);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_qr, qr_smem_capacity() * 8);
   count_launch();
   k_qr<<<njobs, 256, bytes, st>>>(d_jobs, cap);
 }
@@ -328,17 +344,10 @@ __global__ void __launch_bounds__(256, 3) k_applyq(const ApplyQJob* __restrict__
   }
 }
 
-void launch_applyq2(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);   // eval.cu (DMMA)
-
-void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st, bool all_T) {
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st) {
   if (njobs <= 0 || cmax <= 0) return;
   count_launch();
-  // k_applyq2 (DMMA, one CTA per job and 32 columns) measured slower on B200
-  // (169 vs 106 ms per cfg-4 product: one dependent DMMA chain per warp over
-  // all rows, fewer CTAs); opt in with HM_APPLYQ2=1
-  static const bool use2 = std::getenv("HM_APPLYQ2") != nullptr;
-  if (all_T && use2) launch_applyq2(d_jobs, njobs, cmax, st);
-  else k_applyq<<<dim3(njobs, (cmax + 7) / 8), 256, 0, st>>>(d_jobs);
+  k_applyq<<<dim3(njobs, (cmax + 7) / 8), 256, 0, st>>>(d_jobs);
 }
 
 // SVD kernels: see svd.cu
@@ -382,193 +391,6 @@ void launch_copy_mapped(const CopyJob* d_jobs, int njobs, const int* d_tmap, int
 }
 
 // ------------------------------------------------------------------ eval
-// CTA-wide out[0:M,0:N] += coef * opA(M x K) * opB(K x N), 32x32 tiles,
-// 256 threads, operands staged through shared memory.  bid: opB = I.
-struct Op {
-  const double* p;
-  int ld, tr;
-  __device__ __forceinline__ double at(int i, int j) const {
-    return tr ? p[j + (int64_t)i * ld] : p[i + (int64_t)j * ld];
-  }
-};
-
-__device__ void cta_gemm_acc(double* out, int ldo, int M, int N, int K, double coef, Op A, Op B,
-                             double* sA, double* sB) {
-  const int tid = threadIdx.x;
-  const int ri = tid & 31, cj = tid >> 5;  // rows ri, cols cj + 8*x
-  for (int i0 = 0; i0 < M; i0 += 32) {
-    for (int j0 = 0; j0 < N; j0 += 32) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int p0 = 0; p0 < K; p0 += 32) {
-        for (int e = tid; e < 1024; e += 256) {
-          int a, b;
-          if (!A.tr) { a = e & 31; b = e >> 5; } else { b = e & 31; a = e >> 5; }
-          const int gi = i0 + a, gp = p0 + b;
-          sA[a * 33 + b] = (gi < M && gp < K) ? A.at(gi, gp) : 0.0;
-          int c2, d2;
-          if (!B.tr) { d2 = e & 31; c2 = e >> 5; } else { c2 = e & 31; d2 = e >> 5; }
-          const int gq = p0 + d2, gj = j0 + c2;
-          sB[d2 * 33 + c2] = (gq < K && gj < N) ? B.at(gq, gj) : 0.0;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int pp = 0; pp < 32; pp++) {
-          const double av = sA[ri * 33 + pp];
-#pragma unroll
-          for (int x = 0; x < 4; x++) acc[x] = fma(av, sB[pp * 33 + cj + 8 * x], acc[x]);
-        }
-        __syncthreads();
-      }
-      const int gi = i0 + ri;
-      if (gi < M) {
-#pragma unroll
-        for (int x = 0; x < 4; x++) {
-          const int gj = j0 + cj + 8 * x;
-          if (gj < N) out[gi + (int64_t)gj * ldo] += coef * acc[x];
-        }
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// out += coef * op(H) V over the leaves [lb, le) of J's table (Fig. 1 addeval /
-// addevaltrans flattened over a DFS leaf range); one CTA, results accumulate in
-// place (each CTA owns its output panel).
-__device__ void eval_leaves(const EvalJob& J, int lb, int le, double* sA, double* sB, double* sT) {
-  const int tid = threadIdx.x;
-  for (int li = lb; li < le; li++) {
-    const LeafDesc L = J.leaves[li];
-    const int ro = L.row0 - J.t0, co = L.col0 - J.s0;   // offsets inside block (t,s)
-    // non-trans: out rows ro.., V rows co.. ; trans: out rows co.., V rows ro..
-    const int orow = J.trans ? co : ro;
-    const int vrow = J.trans ? ro : co;
-    const int mo = J.trans ? L.n : L.m;   // rows of op(L)
-    const int ko = J.trans ? L.m : L.n;   // cols of op(L)
-    if (J.videntity) {
-      // out[orow + i, vrow + p] += coef * op(L)(i, p)
-      double* o = J.out + orow + (int64_t)vrow * J.ldo;
-      if (L.kind == 2) {
-        for (int64_t e = tid; e < (int64_t)mo * ko; e += 256) {
-          const int i = (int)(e % mo), p = (int)(e / mo);
-          const double v = J.trans ? L.A[p + (int64_t)i * L.m] : L.A[i + (int64_t)p * L.m];
-          o[i + (int64_t)p * J.ldo] += J.coef * v;
-        }
-        __syncthreads();
-      } else if (L.k > 0) {
-        // op(L) = A B^T (or B A^T): out += coef * X Y^T with X,Y the factors
-        const Op X{J.trans ? L.B : L.A, J.trans ? L.n : L.m, 0};
-        const Op Yt{J.trans ? L.A : L.B, J.trans ? L.m : L.n, 1};
-        cta_gemm_acc(o, J.ldo, mo, ko, L.k, J.coef, X, Yt, sA, sB);
-      }
-      continue;
-    }
-    const Op V{J.V + (J.vtrans ? (int64_t)vrow * J.ldv : (int64_t)vrow), J.ldv, J.vtrans};
-    double* o = J.out + orow;
-    if (L.kind == 2) {
-      const Op N{L.A, L.m, J.trans};
-      cta_gemm_acc(o, J.ldo, mo, J.w, ko, J.coef, N, V, sA, sB);
-    } else if (L.k > 0) {
-      // tmp (k x 32 chunk) = F2^T V ; out += coef * F1 tmp, F1 = A (B for trans)
-      const double* F1 = J.trans ? L.B : L.A;
-      const int ld1 = J.trans ? L.n : L.m;
-      const double* F2 = J.trans ? L.A : L.B;
-      const int ld2 = J.trans ? L.m : L.n;
-      for (int j0 = 0; j0 < J.w; j0 += 32) {
-        const int wc = min(32, J.w - j0);
-        const Op Vc{J.vtrans ? V.p + j0 : V.p + (int64_t)j0 * V.ld, V.ld, V.tr};
-        for (int q0 = 0; q0 < L.k; q0 += 32) {
-          const int kc = min(32, L.k - q0);
-          for (int e = tid; e < 32 * 33; e += 256) sT[e] = 0.0;
-          __syncthreads();
-          const Op F2t{F2 + (int64_t)q0 * ld2, ld2, 1};
-          cta_gemm_acc(sT, 33, kc, wc, ko, 1.0, F2t, Vc, sA, sB);
-          const Op F1o{F1 + (int64_t)q0 * ld1, ld1, 0};
-          const Op T{sT, 33, 0};
-          cta_gemm_acc(o + (int64_t)j0 * J.ldo, J.ldo, mo, wc, kc, J.coef, F1o, T, sA, sB);
-        }
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) k_eval(const EvalJob* __restrict__ jobs) {
-  __shared__ double sA[32 * 33];
-  __shared__ double sB[32 * 33];
-  __shared__ double sT[32 * 33];
-  const EvalJob J = jobs[blockIdx.x];
-  eval_leaves(J, J.leaf_begin, J.leaf_end, sA, sB, sT);
-}
-
-// ------------------------------------------------------------------ TRSM
-// Triangular solve through the H-structure on one thin panel per CTA: a host
-// prepared step list of (a) dense triangular solves on leaf clusters and (b)
-// addeval / addevaltrans updates over leaf ranges (alpha = -1), e.g.
-// TRSM_L(t, V): TRSM_L(t1, V1); V2 -= L_(t2,t1) V1; TRSM_L(t2, V2).
-__global__ void __launch_bounds__(256) k_trsm(const TrsmJob* __restrict__ jobs,
-                                              const TrsmStep* __restrict__ steps,
-                                              const LeafDesc* __restrict__ leaves) {
-  __shared__ double tri[64 * 65];   // solve steps; eval steps reuse it as 3 tiles
-  double* sA = tri;
-  double* sB = tri + 32 * 33;
-  double* sT = tri + 2 * 32 * 33;
-  const TrsmJob J = jobs[blockIdx.x];
-  const int tid = threadIdx.x;
-  for (int si = J.step0; si < J.step1; si++) {
-    const TrsmStep S = steps[si];
-    if (S.kind == 0) {
-      // V[r0:r0+m, :] <- T^{-1} V, T lower triangular: T(i,j) = trans ? P[j + i ld] : P[i + j ld]
-      const int m = S.m;
-      double* v = J.V + S.r0;
-      if (m <= 64) {
-        for (int e = tid; e < m * m; e += 256) {
-          const int i = e % m, j = e / m;
-          tri[i + j * 65] = S.trans ? S.P[j + (int64_t)i * S.ld] : S.P[i + (int64_t)j * S.ld];
-        }
-        __syncthreads();
-      }
-      for (int col = tid; col < J.ncols; col += 256) {
-        double* x = v + (int64_t)col * J.ldv;
-        for (int i = 0; i < m; i++) {
-          double s = x[i];
-          for (int p = 0; p < i; p++) {
-            const double tip = (m <= 64) ? tri[i + p * 65]
-                                         : (S.trans ? S.P[p + (int64_t)i * S.ld] : S.P[i + (int64_t)p * S.ld]);
-            s = fma(-tip, x[p], s);
-          }
-          if (!S.unit) {
-            const double d = (m <= 64) ? tri[i + i * 65] : S.P[i + (int64_t)i * S.ld];
-            s /= d;
-          }
-          x[i] = s;
-        }
-      }
-      __syncthreads();
-    } else {
-      EvalJob E{};
-      E.leaves = leaves;
-      E.trans = S.trans;
-      E.t0 = J.panel0;
-      E.s0 = J.panel0;
-      E.coef = -1.0;
-      E.out = J.V;
-      E.ldo = J.ldv;
-      E.w = J.ncols;
-      E.V = J.V;
-      E.ldv = J.ldv;
-      eval_leaves(E, S.lb, S.le, sA, sB, sT);
-      __syncthreads();
-    }
-  }
-}
-
-void launch_trsm(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, const LeafDesc* leaves,
-                 cudaStream_t st) {
-  if (njobs <= 0) return;
-  count_launch();
-  k_trsm<<<njobs, 256, 0, st>>>(d_jobs, d_steps, leaves);
-}
-
 // ------------------------------------------------------------------ dense leaf factorizations
 // In-place LU without pivoting (unit L) or Cholesky (lower) of one diagonal
 // leaf per CTA (m <= 128 in shared memory).  Pivot breakdown (|p| <= 1e-300,
@@ -622,19 +444,9 @@ __global__ void __launch_bounds__(256) k_leaf_factor(const LeafFactorJob* __rest
 void launch_leaf_factor(const LeafFactorJob* d_jobs, int njobs, int chol, int* fail, double* minpiv,
                         int maxm, cudaStream_t st) {
   if (njobs <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_leaf_factor, 200 * 1024);
   count_launch();
   k_leaf_factor<<<njobs, 256, (size_t)maxm * maxm * 8, st>>>(d_jobs, chol, fail, minpiv);
-}
-
-void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st) {
-  if (njobs <= 0) return;
-  count_launch();
-  k_eval<<<njobs, 256, 0, st>>>(d_jobs);
 }
 
 // ------------------------------------------------------------------ entries

@@ -147,7 +147,9 @@ struct TrsmJob {
   int step0, step1;
 };
 
-// In-place dense LU (no pivoting, unit L) or Cholesky of a diagonal leaf.
+// In-place dense LU (no pivoting, unit L) or Cholesky of a diagonal leaf
+// (whole leaf in shared memory: m <= kMaxLeafFactor).
+constexpr int kMaxLeafFactor = 160;
 struct LeafFactorJob {
   double* N;
   int m, ld;
@@ -172,17 +174,13 @@ void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t 
 void launch_gemm_mapped(const GemmJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
 void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
 void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);   // rows <= 24576
-// all_T: every job carries its compact-WY T factors (then the DMMA k_applyq2 runs)
-void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st, bool all_T = false);
+void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_copy_mapped(const CopyJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
-void launch_eval(const EvalJob* d_jobs, int njobs, cudaStream_t st);
 void launch_eval2(const EvalJob* d_jobs, int njobs, cudaStream_t st);   // eval.cu (shared-memory tiles)
 void launch_trsm2(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, const LeafDesc* leaves,
                   cudaStream_t st);   // eval.cu (shared-memory substitution + eval tiles)
-void launch_trsm(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, const LeafDesc* leaves,
-                 cudaStream_t st);
 void launch_leaf_factor(const LeafFactorJob* d_jobs, int njobs, int chol, int* fail, double* minpiv,
                         int maxm, cudaStream_t st);
 void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x,
@@ -193,6 +191,10 @@ void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double
                           const double* x, int64_t ldx, double* y, int64_t ldy, int ncols,
                           int part, cudaStream_t st);
 void launch_scale(double* y, int64_t ldy, int64_t rows, int cols, double beta, cudaStream_t st);
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the CURRENT device,
+// set once per (function, device) under a mutex; throws (HM_ECUDA) on failure.
+void ensure_smem_attr(const void* func, int bytes);
 
 int64_t launch_count();     // process-wide number of kernel launches
 void count_launch();        // called by every launcher

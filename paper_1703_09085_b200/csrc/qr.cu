@@ -409,13 +409,11 @@ static void launch_qr_variant(const QrJob* d_jobs, int njobs, int cap, int rb, c
   const bool use_dmma = dm && kThreads == 256 && cap <= 6 * 1024;
   // +256 doubles: the DMMA variant pads the panel leading dimension to 4 (mod 16)
   const int capx = cap + (use_dmma ? 256 : 0);
-  static bool attr = false;
-  if (!attr) {
+  {
     const int bytes = ((kThreads == 512 ? 24 : (kMinBlocks == 2 ? 12 : 6)) * 1024 + 256) * 8;
-    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_qr_blocked<kThreads, kMinBlocks, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr = true;
+    ensure_smem_attr((const void*)k_qr_blocked<kThreads, kMinBlocks, 4, true>, bytes);
+    ensure_smem_attr((const void*)k_qr_blocked<kThreads, kMinBlocks, 4, false>, bytes);
+    ensure_smem_attr((const void*)k_qr_blocked<kThreads, kMinBlocks, 8, false>, bytes);
   }
   // DMMA trailing update: measured faster only for the 384-row bucket with
   // 256 threads (133 -> 115 ms per cfg-4 product); 768 rows +4 %, 1536 rows and

@@ -871,11 +871,7 @@ __global__ void __launch_bounds__(512) k_trunc_small(const TruncSmallJob* __rest
 
 void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
   if (njobs <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_trunc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 26 * 1024 * 8);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_trunc_small, 26 * 1024 * 8);
   count_launch();
   // small stacks: one warp per stack (barriers of a 1-warp CTA are nearly
   // free, and many stacks share an SM); larger: 128 / 256 threads
@@ -896,11 +892,7 @@ int svd_smem_capacity() { return 26 * 1024; }
 
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
   if (njobs <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, svd_smem_capacity() * 8);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_svd, svd_smem_capacity() * 8);
   if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
   static const int tg = [] { const char* e = std::getenv("HM_SVDG_THREADS"); return e ? std::atoi(e) : 512; }();
   int threads = (cap == 0 || cap > 8 * 1024 || njobs < 296) ? 512 : 256;

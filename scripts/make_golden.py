@@ -2,20 +2,31 @@
 """Write oracle golden data for full-size parity tests (calls only oracle/ and
 hm_inputs/; nothing from the CUDA path).
 
-    python scripts/make_golden.py product 4     # BASELINE configs[3]: n=81920 product
+    python scripts/make_golden.py product 1     # BASELINE configs[0]: n=1280 product
+    python scripts/make_golden.py product 4     # configs[3]: n=81920 product
     python scripts/make_golden.py lr 2          # configs[1]: n=5120 H-LR
     python scripts/make_golden.py chol 3        # configs[2]: n=20480 H-Cholesky
+    python scripts/make_golden.py lr 4          # "config 4'": H-LR of configs[3]'s matrix (metric, n=81920)
+    python scripts/make_golden.py lr 5          # configs[4]: n=327680 H-LR
+    [workers]  (default: all host cores)
 
-Stored in tests/golden/<name>.npz:
-  ranks      per block rank of the result (-1 for non-admissible blocks)
-  fro        per leaf block Frobenius norm of the result
-  sample     ids of sampled leaf blocks; sketch_<id> = Z_b Omega_b with
-             Omega_b = default_rng([1703, 9085, 99, id]).standard_normal((n_b, 4))
-  probes     result applied to 2 probe vectors (tree order)
-  meta       json (config, truncation counts, near-threshold list, timings)
+The built H-matrix and the oracle's result are also pickled under
+.golden_raw/ (git- and gpurun-ignored) so summaries can be recomputed and
+config 4 / 4' share one build.
+
+tests/golden/<what>_cfg<cfg>.npz (oracle/summary.py):
+  leaf_ids, ranks, fro, sk     summary of the RESULT for every leaf block:
+                               rank, exact ||Z_b||_F, two-sided sketch
+                               Omega_L[t]^T Z_b Omega_R[r] (sketch_k x sketch_k)
+  b_ranks, b_fro               summary of the BUILT input (build parity)
+  probes                       result applied to 2 probe vectors (tree order;
+                               H-LR: L(R v), Cholesky: L(L^T v))
+  near                         (t, r) cluster ids of near-threshold truncations
+  meta                         json: config, truncation counts, timings
 """
 import json
 import os
+import pickle
 import sys
 import time
 
@@ -29,41 +40,37 @@ from hm_inputs import probe_vectors, sphere_points  # noqa: E402
 from oracle import kernel as K  # noqa: E402
 from oracle.hmatrix import Problem, matvec  # noqa: E402
 from oracle.parallel import addmul_s2_parallel, build_parallel  # noqa: E402
+from oracle.summary import summarise_hmatrix  # noqa: E402
 
+# cfg -> (icosphere level, leaf, eps); BASELINE.json configs[cfg-1]; 4 = configs[3]'s matrix
 CONFIGS = {1: (3, 32, 1e-4), 2: (4, 32, 1e-4), 3: (5, 32, 1e-5), 4: (6, 64, 1e-6), 5: (7, 64, 1e-4)}
+RAW = os.path.join(ROOT, ".golden_raw")
 
 
-def omega(bid, n):
-    return np.random.default_rng([1703, 9085, 99, int(bid)]).standard_normal((n, 4))
+def near_tags(near):
+    """(t, r) cluster ids of near-threshold truncations; tags are
+    (kind, t_id, r_id) (oracle/product.py, oracle/factor.py)."""
+    out = []
+    for tag in near:
+        if tag is not None and len(tag) >= 3:
+            out.append((int(tag[1]), int(tag[2])))
+    return sorted(set(out))
 
 
-def summarise(P, H, nsample=400, max_rows=300):
-    bt = P.bt
-    nb = len(bt.blocks)
-    ranks = np.full(nb, -1, np.int32)
-    fro = np.zeros(nb)
-    for b in bt.leaves():
-        if b.kind == 1:
-            A, B = H.A[b.id], H.B[b.id]
-            ranks[b.id] = A.shape[1]
-            _, Ra = np.linalg.qr(A)
-            _, Rb = np.linalg.qr(B)
-            fro[b.id] = np.linalg.norm(Ra @ Rb.T) if A.shape[1] else 0.0
-        else:
-            fro[b.id] = np.linalg.norm(H.N[b.id])
-    rng = np.random.default_rng([1703, 9085, 98])
-    cand = [b for b in bt.leaves() if b.t.size <= max_rows and b.s.size <= max_rows]
-    pick = rng.choice(len(cand), size=min(nsample, len(cand)), replace=False)
-    sample = np.array(sorted(cand[i].id for i in pick), np.int64)
-    sk = {}
-    for bid in sample:
-        b = bt.blocks[bid]
-        Om = omega(bid, b.s.size)
-        if b.kind == 1:
-            sk[f"sketch_{bid}"] = H.A[bid] @ (H.B[bid].T @ Om)
-        else:
-            sk[f"sketch_{bid}"] = H.N[bid] @ Om
-    return ranks, fro, sample, sk
+def get_build(P, eps, kernel, L, leaf, workers):
+    os.makedirs(RAW, exist_ok=True)
+    path = os.path.join(RAW, f"build_L{L}_leaf{leaf}_eps{eps:g}_k{kernel}.pkl")
+    if os.path.exists(path):
+        with open(path, "rb") as f:
+            G, t_build = pickle.load(f)
+        print(f"build loaded from {path}", flush=True)
+        return G, t_build
+    t0 = time.time()
+    G = build_parallel(P, eps, workers)
+    t_build = time.time() - t0
+    with open(path, "wb") as f:
+        pickle.dump((G, t_build), f, protocol=pickle.HIGHEST_PROTOCOL)
+    return G, t_build
 
 
 def main():
@@ -73,40 +80,53 @@ def main():
     x, w = sphere_points(L)
     kernel = K.KERNEL_SLP_SYM if what == "chol" else K.KERNEL_SLP
     P = Problem(x, w, leaf, 2.0, kernel=kernel)
-    t0 = time.time()
-    G = build_parallel(P, eps, workers)
-    t_build = time.time() - t0
+    G, t_build = get_build(P, eps, kernel, L, leaf, workers)
     print(f"build n={P.ct.n}: {t_build:.1f}s", flush=True)
-    meta = dict(what=what, config=cfg, L=L, leaf=leaf, eps=eps, n=int(P.ct.n), build_s=t_build)
+    meta = dict(what=what, config=cfg, L=L, leaf=leaf, eps=eps, n=int(P.ct.n), kernel=kernel, build_s=t_build)
+    sk_k = 2 if cfg == 5 else 4
+    bsum = summarise_hmatrix(G, sk_k)
     t0 = time.time()
+    v2 = probe_vectors(P.ct.n, 2)[P.perm]
     if what == "product":
-        Z, info = addmul_s2_parallel(1.0, G.clone(), G.clone(), G.clone(), eps, workers)
-        meta.update({k: (v if k != "near" else [list(map(str, x)) for x in v]) for k, v in info.items()})
+        Z, info = addmul_s2_parallel(1.0, G.clone(), G.clone(), G.clone(), eps, workers, frontier_depth=4)
+        near = near_tags(t for t, _ in info["near"])
+        meta.update(truncations=info["truncations"], trunc_cols=info["trunc_cols"],
+                    addproduct=info["addproduct"], frontier=info["frontier"], schedule="S2 (oracle.parallel)")
         out = Z
+        meta["op_s"] = time.time() - t0
+        pr = np.zeros_like(v2)
+        matvec(out, 1.0, v2, pr)
     else:
-        from oracle.factor import chol_with_restart, lr, probe_residual
+        from oracle.factor import apply_factor, chol_with_restart, lr, probe_residual
         from oracle.lowrank import TruncCtx
         ctx = TruncCtx(eps)
         G0 = G.clone()
+        Gw = G.clone()
         if what == "lr":
-            out, F = lr(G, eps, ctx=ctx)
+            out, F = lr(Gw, eps, ctx=ctx)
             shift = 0.0
         else:
-            out, F, shift = chol_with_restart(G, eps, lambda: TruncCtx(eps))
+            out, F, shift = chol_with_restart(Gw, eps, lambda: TruncCtx(eps))
             ctx = F.ctx
-        v = probe_vectors(P.ct.n)[P.perm]
-        meta.update(truncations=ctx.count, trunc_cols=ctx.cols, near=[str(x[1]) for x in ctx.near],
-                    min_pivot=F.min_pivot, shift=shift,
-                    probe_residual=probe_residual(G0, out, v, what, shift))
-    meta["op_s"] = time.time() - t0
-    print(f"{what}: {meta['op_s']:.1f}s truncations {meta['truncations']}", flush=True)
-    ranks, fro, sample, sk = summarise(P, out)
-    v = probe_vectors(P.ct.n, 2)[P.perm]
-    pr = np.zeros_like(v)
-    matvec(out, 1.0, v, pr)
+        meta["op_s"] = time.time() - t0
+        near = near_tags(x[1] for x in ctx.near)
+        v8 = probe_vectors(P.ct.n)[P.perm]
+        meta.update(truncations=ctx.count, trunc_cols=ctx.cols, min_pivot=F.min_pivot, shift=shift,
+                    probe_residual=probe_residual(G0, out, v8, what, shift), schedule="O8/O9 (oracle.factor)")
+        if what == "lr":
+            pr = apply_factor(out, "L", apply_factor(out, "R", v2))
+        else:
+            pr = apply_factor(out, "Lc", apply_factor(out, "LcT", v2))
+    meta["near_count"] = len(near)
+    print(f"{what} cfg{cfg}: {meta['op_s']:.1f}s truncations {meta['truncations']} near {len(near)}", flush=True)
+    with open(os.path.join(RAW, f"{what}_cfg{cfg}_result.pkl"), "wb") as f:
+        pickle.dump((out, meta, near), f, protocol=pickle.HIGHEST_PROTOCOL)
+    rsum = summarise_hmatrix(out, sk_k)
     os.makedirs(os.path.join(ROOT, "tests", "golden"), exist_ok=True)
     path = os.path.join(ROOT, "tests", "golden", f"{what}_cfg{cfg}.npz")
-    np.savez_compressed(path, ranks=ranks, fro=fro, sample=sample, probes=pr, meta=json.dumps(meta), **sk)
+    np.savez_compressed(path, leaf_ids=rsum["leaf_ids"], ranks=rsum["ranks"], fro=rsum["fro"], sk=rsum["sk"],
+                        b_ranks=bsum["ranks"], b_fro=bsum["fro"], probes=pr,
+                        near=np.array(near, np.int64).reshape(-1, 2), meta=json.dumps(meta))
     print("wrote", path, os.path.getsize(path) // 1024, "KiB", flush=True)
 
 

@@ -46,9 +46,29 @@ def lowrank_norm(A, B):
     return float(np.linalg.norm(Ra @ Rb.T))
 
 
+def near_tags(octx):
+    """(t, r) cluster ids of the oracle's near-threshold truncations
+    (TruncCtx.near entries (idx, tag, k, s), tag = (kind, t_id, r_id))."""
+    out = set()
+    for e in octx.near:
+        tag = e[1]
+        if tag is not None and len(tag) >= 3:
+            out.add((int(tag[1]), int(tag[2])))
+    return sorted(out)
+
+
+def near_block_set(d, octx):
+    """Leaf blocks inside a near-threshold truncation's (t, r) block: the only
+    blocks whose rank may differ (north star exemption)."""
+    from oracle.summary import near_blocks
+    return near_blocks(d, near_tags(octx))
+
+
 def compare(dg, do, near_blocks=(), tol=1e-9):
-    """Per-block parity (north star): identical ranks (except flagged blocks) and
-    relative Frobenius difference <= tol.  Returns a report dict."""
+    """Per-block parity (north star): identical ranks except on near-flagged
+    blocks (rank_mismatch must be a subset of near_blocks: see
+    `unexplained_mismatch`) and relative Frobenius difference <= tol on every
+    other block.  Returns a report dict."""
     pg, po = leaf_payloads(dg), leaf_payloads(do)
     assert pg.keys() == po.keys()
     total = 0.0
@@ -70,4 +90,6 @@ def compare(dg, do, near_blocks=(), tol=1e-9):
             continue
         if rel > worst:
             worst, worst_b = rel, b
-    return dict(rank_mismatch=rank_mis, worst=worst, worst_block=worst_b, znorm=znorm)
+    near_blocks = set(near_blocks)
+    return dict(rank_mismatch=rank_mis, unexplained_mismatch=[b for b in rank_mis if b not in near_blocks],
+                worst=worst, worst_block=worst_b, znorm=znorm)

@@ -1,14 +1,21 @@
 """Full-size GPU <-> oracle parity on BASELINE.json's configurations (pytest -m gpu).
 
-Golden data come from `scripts/make_golden.py` (calls only oracle/):
-per-block ranks and Frobenius norms of the oracle's result, sketches
-Z_b Omega_b of ~400 sampled leaf blocks, and the result applied to two probe
-vectors.  The device side builds the same H-matrix with hm_build (trees
-bit-identical, admissible blocks certified to 1e-12 against the exact SVD),
-runs the operation in the launch configuration bench.py uses, and is
-compared on: identical ranks (blocks flagged near-threshold by the oracle
-excepted), per-block norms and sampled sketches within 1e-9 relative, probes
-within 1e-9 relative.
+Golden data come from `scripts/make_golden.py` (calls only oracle/; summary
+format in oracle/summary.py): for EVERY leaf block of the oracle's result its
+rank, exact Frobenius norm and a two-sided Gaussian sketch
+Omega_L[t]^T Z_b Omega_R[r]; the built input's ranks and norms; the result
+applied to two probe vectors; the (t, r) clusters of near-threshold
+truncations.  The device side builds the same H-matrix with hm_build (trees
+bit-identical, admissible blocks certified to 1e-12 against the exact SVD;
+its ranks and per-block norms are checked against the oracle build first),
+runs the operation in the launch configuration bench.py uses, exports the
+result and summarises it with the same oracle/summary.py code.  Checks
+(north star, BASELINE.json):
+  * identical ranks on every block outside a near-threshold truncation's
+    (t, r) block (mismatches must be a subset of the near-flagged blocks),
+  * per-block difference estimate ||S_gpu - S_oracle||_F / k <= 1e-9 of
+    max(||Z_b||_F, 1e-12 ||Z||_F) on every other block,
+  * probes within 1e-9 relative.
 """
 import json
 import os
@@ -45,75 +52,70 @@ def _load(name):
     return g, json.loads(str(g["meta"]))
 
 
-def _payloads(d):
-    from tests.hm_compare import leaf_payloads
-    return leaf_payloads(d)
+def _check_build(G, g):
+    """Device build vs the oracle build: ranks identical, norms <= 1e-9."""
+    from oracle.summary import summarise_desc
+    s = summarise_desc(G.export(), k=1)
+    assert np.array_equal(s["ranks"], g["b_ranks"]), int(np.sum(s["ranks"] != g["b_ranks"]))
+    znorm = np.sqrt(np.sum(g["b_fro"] ** 2))
+    rel = np.abs(s["fro"] - g["b_fro"]) / np.maximum(g["b_fro"], 1e-12 * znorm)
+    assert rel.max() <= TOL, rel.max()
 
 
-def _fro(v):
-    if v[0] == "dense":
-        return float(np.linalg.norm(v[1]))
-    A, B = v[1], v[2]
-    if A.shape[1] == 0:
-        return 0.0
-    return float(np.sqrt(max(np.sum((A.T @ A) * (B.T @ B)), 0.0)))
-
-
-def _check(hm, ctx, out, g, meta):
+def _check_result(out, g, meta):
+    from oracle.summary import compare_summaries, near_blocks, summarise_desc
     d = out.export()
-    pay = _payloads(d)
-    ranks = g["ranks"]
-    nearb = set()
-    mism = [b for b, v in pay.items() if v[0] == "adm" and v[1].shape[1] != ranks[b]]
-    assert not mism or meta.get("near"), (len(mism), mism[:10])
-    fro = g["fro"]
-    znorm = np.sqrt(np.sum(fro ** 2))
-    worst = 0.0
-    for b, v in pay.items():
-        if b in mism:
-            continue
-        worst = max(worst, abs(_fro(v) - fro[b]) / max(fro[b], 1e-12 * znorm))
-    assert worst <= TOL, worst
-    ws = 0.0
-    for bid in g["sample"]:
-        if int(bid) in mism:
-            continue
-        v = pay[int(bid)]
-        n_b = (v[1].shape[1] if v[0] == "dense" else v[2].shape[0])
-        Om = np.random.default_rng([1703, 9085, 99, int(bid)]).standard_normal((n_b, 4))
-        s = v[1] @ Om if v[0] == "dense" else v[1] @ (v[2].T @ Om)
-        ref = g[f"sketch_{int(bid)}"]
-        ws = max(ws, np.linalg.norm(s - ref) / max(np.linalg.norm(ref), 1e-12 * znorm))
-    assert ws <= TOL, ws
-    return worst, ws
+    k = g["sk"].shape[1]
+    got = summarise_desc(d, k=k)
+    ref = {key: g[key] for key in ("leaf_ids", "ranks", "fro", "sk")}
+    allowed = near_blocks(d, [tuple(x) for x in g["near"]])
+    rep = compare_summaries(got, ref, TOL, allowed, eps_bound=20 * meta["eps"])
+    print(f"{meta['what']} cfg{meta['config']}: {rep['nleaves']} leaves, worst block diff {rep['worst']:.2e} "
+          f"(block {rep['worst_block']}), near-flagged {len(allowed)}, rank mismatches {len(rep['rank_mismatch'])}")
+    assert not rep["unexplained_mismatch"], rep["unexplained_mismatch"][:20]
+    assert rep["worst"] <= TOL, rep
+    assert rep["worst_allowed"] <= 20 * meta["eps"], rep
+    return rep
+
+
+def _probe(hm, M, n, perm, what):
+    import torch
+    v = probe_vectors(n, 2)[perm]
+    xv = torch.from_numpy(v.T.copy()).cuda().T
+    y = torch.zeros_like(xv)
+    if what == "product":
+        hm.matvec(M, xv, y)
+    else:
+        t = torch.zeros_like(xv)
+        hm.matvec(M, xv, t, op=3 if what == "lr" else 5)   # R v | L^T v
+        hm.matvec(M, t, y, op=2 if what == "lr" else 4)    # L (.)
+    return y.cpu().numpy()
 
 
 @pytest.mark.parametrize("cfg", [1, 4])
 def test_product_golden(hm, ctx, cfg):
-    import torch
     g, meta = _load(f"product_cfg{cfg}.npz")
     x, w = sphere_points(meta["L"])
     G = ctx.build(x, w, meta["leaf"], 2.0, meta["eps"])
+    _check_build(G, g)
     X, Y, Z = G.clone(), G.clone(), G.clone()
     hm.addmul(1.0, X, Y, Z, meta["eps"])
     st = ctx.last_stats()
     assert st["truncations"] == meta["truncations"]
     assert st["addproduct_calls"] == meta["addproduct"]
-    _check(hm, ctx, Z, g, meta)
-    n = len(w)
-    v = probe_vectors(n, 2)[G.perm]
-    xv = torch.from_numpy(v.T.copy()).cuda().T
-    yv = torch.zeros_like(xv)
-    hm.matvec(Z, xv, yv)
-    pr = yv.cpu().numpy()
+    _check_result(Z, g, meta)
+    pr = _probe(hm, Z, len(w), G.perm, "product")
     assert np.linalg.norm(pr - g["probes"]) <= TOL * np.linalg.norm(g["probes"])
 
 
-@pytest.mark.parametrize("kind,cfg", [("lr", 2), ("chol", 3)])
+@pytest.mark.parametrize("kind,cfg", [("lr", 2), ("chol", 3), ("lr", 4), ("lr", 5)])
 def test_factor_golden(hm, ctx, kind, cfg):
+    """configs[1] (n=5120 H-LR), configs[2] (n=20480 H-Cholesky), the metric's
+    n=81920 H-LR of configs[3]'s matrix and configs[4] (n=327680 H-LR)."""
     g, meta = _load(f"{kind}_cfg{cfg}.npz")
     x, w = sphere_points(meta["L"])
     G = ctx.build(x, w, meta["leaf"], 2.0, meta["eps"], kernel=0 if kind == "lr" else 1)
+    _check_build(G, g)
     if kind == "lr":
         hm.lr(G, meta["eps"])
     else:
@@ -121,7 +123,9 @@ def test_factor_golden(hm, ctx, kind, cfg):
     st = ctx.last_stats()
     assert st["truncations"] == meta["truncations"]
     assert abs(st["min_pivot"] - meta["min_pivot"]) <= 1e-9 * meta["min_pivot"]
-    _check(hm, ctx, G, g, meta)
+    _check_result(G, g, meta)
+    pr = _probe(hm, G, len(w), G.perm, kind)
+    assert np.linalg.norm(pr - g["probes"]) <= TOL * np.linalg.norm(g["probes"])
 
 
 def _probe_residual_gpu(hm, G0, F, n, perm, kind):
@@ -147,7 +151,6 @@ def _probe_residual_gpu(hm, G0, F, n, perm, kind):
     ("lr", 4, 32, 1e-4),     # configs[1]
     ("chol", 5, 32, 1e-5),   # configs[2]
     ("lr", 6, 64, 1e-6),     # the metric's n = 81920 H-LR
-    ("lr", 7, 64, 1e-4),     # configs[4]: n = 327680, fully HBM resident
 ])
 def test_factor_probe_residual(hm, ctx, kind, L, leaf, eps):
     """Property valid at any size (north star check 4): probe residual of the
