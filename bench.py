@@ -12,8 +12,15 @@ FP64 GFLOP/s of the batched low-rank update work over the
 device-timed region; `e2e` = same flops with host descriptions uploaded /
 the result downloaded through the C-ABI inside the timed region.
 
+The line also carries (BASELINE.json metric, first half): H-LR / H-Cholesky
+setup seconds and convention GFLOP/s at configs[1], configs[2], the metric's
+n = 81920 H-LR ("config 4'") and configs[4] (n = 327680); the standalone
+batched flush (captured in situ + synthetic prescribed-sigma stacks); the
+roofline of the top kernel functions; the standard (S0) product next to the
+accumulated one when available; the CPU oracle on all host cores.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 4|1] [--no-cpu-baseline]
+                    [--config 4|1] [--no-cpu-baseline] [--no-factor] [--no-flush]
 
 `--impl reference` times the CPU oracle (oracle/, the reference arm of this
 tier) on a bounded sample of the same workload; it is test infrastructure,
@@ -24,6 +31,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,13 +53,25 @@ FACTOR_RUNS = [
     ("cfg2_hlr_n5120", 4, 32, 1e-4, 0, "lr", 2),
     ("cfg3_hchol_n20480", 5, 32, 1e-5, 1, "chol", 1),
     ("cfg4p_hlr_n81920", 6, 64, 1e-6, 0, "lr", 1),
+    ("cfg5_hlr_n327680", 7, 64, 1e-4, 0, "lr", 1),
 ]
-# profile class -> kernel (for the ncu traffic lookup)
-CLASS_KERNEL = {"eval": "k_eval2", "apply_q": "k_applyq", "copy": "k_copy", "memset": None,
-                "trunc_fused": "k_trunc_small", "gemm_M": "k_gemm", "dense_add": "k_gemm",
-                "qr_blk384": "k_qr_blocked<256, 2, 4, 1>", "qr_blk768": "k_qr_blocked<256, 2, 4, 0>", "qr_blk1536": "k_qr_blocked<512, 1, 4, 0>",
-                "svd_smem26k": "k_svd", "svd_global": "k_svd", "svd_smem8k": "k_svd", "svd_smem3k": "k_svd"}
-NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA: SMs x FMA/clk x 2 x max clock
+# profile class -> (kernel function, bound, what the class's convention work measures)
+CLASS_FUNCTION = {
+    "qr": ("k_qr_blocked+k_qr (Householder QR of the stacks, incl. TSQR)", "alu"),
+    "jacobi_svd": ("k_svd (QRCP + one-sided Jacobi)", "alu"),
+    "trunc_fused": ("k_trunc_small (fused TRUNC)", "alu"),
+    "eval": ("k_eval2 (H x thin dense, addeval)", "hbm"),
+    "apply_q": ("k_applyq (reform A' = Q_A U)", "alu"),
+    "gemm_M": ("k_gemm2 (M = R_A R_B^T)", "alu"),
+    "dense_add": ("k_gemm2 (dense flush N += A B^T)", "alu"),
+    "copy": ("k_copy (stack gathers)", "hbm"),
+    "pre_qr_M": ("k_qr_blocked (pre-QR of large M)", "alu"),
+}
+NCU_NAME = {"qr": "k_qr_blocked", "jacobi_svd": "k_svd", "trunc_fused": "k_trunc_small", "eval": "k_eval2",
+            "apply_q": "k_applyq", "gemm_M": "k_gemm2", "dense_add": "k_gemm2", "copy": "k_copy",
+            "pre_qr_M": "k_qr_blocked"}
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA/DMMA: SMs x FMA/clk x 2 x max clock
+CPU_SAMPLE_LEVEL = 5   # oracle sample: icosphere L5 (n = 20480) with config 4's leaf / eta / eps
 
 
 def dist_env():
@@ -152,43 +172,64 @@ def load_peaks():
         return {}
 
 
+def trunc_flops(m, n, l, k):
+    """SURVEY §8(d) convention flops of one truncation (same formula as libhm's
+    trunc_flops and oracle/flops.py)."""
+    if l <= 0:
+        return 0.0
+    if l < min(m, n):
+        return 2.0 * (m + n) * l * l - (4.0 / 3.0) * l ** 3 + l ** 3 / 3.0 + 22.0 * l ** 3 + 2.0 * (m + n) * l * k
+    p, q = max(m, n), min(m, n)
+    return 2.0 * m * n * l + 14.0 * p * q * q + 8.0 * q ** 3
+
+
 # ---------------------------------------------------------------- CPU leg
-def oracle_sample(cfg, seconds_hint=20.0):
-    """The oracle (as it stands) on a bounded sample of the same workload:
-    the S2 accumulated product on the level-4 icosphere (n = 5120) with the
-    config's leaf size, eta and eps.  Returns (GFLOP/s, seconds, sample text,
-    convention GFLOP)."""
+def oracle_sample(cfg, cores, level=CPU_SAMPLE_LEVEL, prebuilt=None):
+    """The oracle (as it stands) on a bounded sample of the same workload: the
+    S2 accumulated product (oracle.parallel.addmul_s2_parallel: the serial
+    oracle's arithmetic, independent subtrees on a process pool, pinned
+    bit-identical to oracle.product.addmul_s2 by tests/test_oracle_parallel.py)
+    on the level-`level` icosphere with the config's leaf size, eta and eps, on
+    `cores` host cores.  Returns (GFLOP/s, seconds, sample text, GFLOP, build)."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from hm_inputs import sphere_points
-    from oracle.hmatrix import Problem, build
-    from oracle.lowrank import TruncCtx
-    from oracle.product import addmul_s2
-    from oracle.flops import ConventionCounter
+    from oracle.hmatrix import Problem
+    from oracle.parallel import addmul_s2_parallel, build_parallel
 
-    L = min(cfg["level"], 4)
-    x, w = sphere_points(L)
-    P = Problem(x, w, cfg["leaf"], cfg["eta"])
-    G = build(P, cfg["eps"])
-    X, Y, Z = G.clone(), G.clone(), G.clone()
-    cc = ConventionCounter()
+    L = min(cfg["level"], level)
+    if prebuilt is None:
+        x, w = sphere_points(L)
+        P = Problem(x, w, cfg["leaf"], cfg["eta"])
+        G = build_parallel(P, cfg["eps"], cores)
+        prebuilt = (P, G)
+    P, G = prebuilt
     t0 = time.perf_counter()
-    addmul_s2(1.0, X, Y, Z, cfg["eps"], ctx=TruncCtx(cfg["eps"], log_near=False), counter=cc)
+    Z, info = addmul_s2_parallel(1.0, G.clone(), G.clone(), G.clone(), cfg["eps"], workers=cores, frontier_depth=4)
     dt = time.perf_counter() - t0
-    gf = cc.total_flops() / 1e9
-    sample = (f"oracle S2 product (oracle/product.py addmul_s2, NumPy/OpenBLAS, 1 thread) on the n={P.ct.n} "
-              f"icosphere (L={L}) with leaf {cfg['leaf']}, eta {cfg['eta']}, eps {cfg['eps']:g}: "
-              f"{gf:.2f} convention GFLOP in {dt:.1f} s")
-    return gf / dt, dt, sample, gf
+    gf = info["conv_gflop"]   # SURVEY §8(d) convention work (oracle/flops.py), printed-branch widths
+    sample = (f"oracle S2 product (oracle.parallel.addmul_s2_parallel, NumPy/OpenBLAS 1 thread per worker, "
+              f"{cores} worker processes) on the n={P.ct.n} icosphere (L={L}) with leaf {cfg['leaf']}, "
+              f"eta {cfg['eta']}, eps {cfg['eps']:g}: {gf:.1f} convention GFLOP in {dt:.1f} s")
+    return gf / dt, dt, sample, gf, prebuilt
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
+    cores = host_cores()
     times, rates = [], []
     sample = ""
+    pre = None
     for i in range(args.warmup + args.steps):
-        rate, dt, sample, gf = oracle_sample(cfg)
+        rate, dt, sample, gf, pre = oracle_sample(cfg, cores, prebuilt=pre)
         if i >= args.warmup:
             times.append(dt)
             rates.append(rate)
@@ -198,7 +239,7 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["name"], "sample": "bounded oracle sample (see cpu_baseline)"},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -206,6 +247,121 @@ def run_reference(args, cfg):
 
 
 # ---------------------------------------------------------------- GPU leg
+def roofline_report(prof, dgemm_tf, peaks, traffic_file):
+    """Top kernel functions by device time in the timed region (per-class CUDA
+    events on the library's stream), achieved convention rate vs the measured
+    DGEMM peak and the nominal FP64 peak (alu) or the measured HBM copy peak
+    (hbm), and the ncu DRAM bytes per launch vs the algorithmic ones."""
+    hbm = peaks.get("hbm_gbs", 6553.6)
+    tj = {}
+    if traffic_file:
+        try:
+            tj = json.load(open(traffic_file)).get("functions", {})
+        except Exception:
+            tj = {}
+    total_ms = sum(v["ms"] for k, v in prof.items() if k in CLASS_FUNCTION)
+    rows = []
+    for k, (fn, bound) in CLASS_FUNCTION.items():
+        p = prof.get(k)
+        if not p or not p["launches"] or p["ms"] <= 0:
+            continue
+        sec = p["ms"] * 1e-3
+        if bound == "hbm":
+            achieved = p["bytes"] / sec / 1e9
+            peak, unit = hbm, "GB/s"
+            frac_nom = achieved / hbm
+        else:
+            achieved = p["flops"] / sec / 1e12
+            peak, unit = dgemm_tf or NOMINAL_FP64_TFLOPS, "TFLOP/s"
+            frac_nom = achieved / NOMINAL_FP64_TFLOPS
+        nc = tj.get(NCU_NAME.get(k, ""), {})
+        algo_per_launch = p["bytes"] / p["launches"] if p["bytes"] else None
+        rows.append({"class": k, "kernel": fn, "bound": bound, "ms": round(p["ms"], 3),
+                     "share": round(p["ms"] / total_ms, 4) if total_ms else None, "launches": p["launches"],
+                     "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak if peak else None,
+                     "frac_nominal": frac_nom, "gflop": p["flops"] / 1e9, "gb_algorithmic": p["bytes"] / 1e9,
+                     "ncu_dram_bytes_per_launch": nc.get("dram_bytes_per_launch"),
+                     "algorithmic_bytes_per_launch": algo_per_launch})
+    rows.sort(key=lambda r: -r["ms"])
+    return rows
+
+
+def standalone_flush(hm, ctx, torch, dev, X, Y, G, eps, top=3):
+    """SURVEY §8(d) config 4 standalone batched flush.  (1) Captured in situ:
+    one extra (untimed) product records every level's TRUNC batch; the `top`
+    levels by convention flops keep their stacked factors on the device and
+    are replayed alone (CUDA events around the TRUNC batch only); the replay
+    must reproduce the in-situ ranks.  (2) Synthetic: the captured shape list
+    of the largest level, every stack filled with prescribed singular values
+    sigma_i = 10^(-i/2) on random orthonormal bases split into 1-8 terms
+    (seed [1703, 9085, 4, level]), through hm_test_trunc_batched."""
+    import numpy as np
+    hm.flush_capture(ctx, 0)
+    Z = G.clone()
+    hm.addmul(1.0, X, Y, Z, eps)
+    Z.free()
+    info = hm.flush_capture_info(ctx)
+    fl = [sum(trunc_flops(int(a), int(b), int(c), int(d)) for a, b, c, d in zip(L["m"], L["n"], L["l"], L["k"]))
+          for L in info]
+    order = sorted(range(len(info)), key=lambda i: -fl[i])[:top]
+    mask = 0
+    for i in order:
+        mask |= 1 << i
+    hm.flush_capture(ctx, mask)
+    Z = G.clone()
+    hm.addmul(1.0, X, Y, Z, eps)
+    Z.free()
+    levels = []
+    tot_fl = tot_ms = 0.0
+    for i in sorted(order):
+        ms, rs = hm.flush_replay(ctx, i, eps, reps=3)
+        L = info[i]
+        ok = rs == int(L["k"].sum())
+        levels.append({"batch": i, "truncations": len(L["m"]), "gflop": fl[i] / 1e9, "ms": ms,
+                       "gflops": fl[i] / (ms * 1e-3) / 1e9, "sum_l": int(L["l"].sum()),
+                       "max_m": int(max(L["m"].max(), L["n"].max())), "max_l": int(L["l"].max()),
+                       "ranks_reproduced": ok})
+        tot_fl += fl[i]
+        tot_ms += ms
+    hm.flush_capture_free(ctx)
+    out = {"captured": {"levels": levels, "gflops": tot_fl / (tot_ms * 1e-3) / 1e9 if tot_ms else None,
+                        "all_level_gflop": sum(fl) / 1e9,
+                        "note": "TRUNC batches of the top levels by convention flops, replayed from captured stacks"}}
+    # synthetic prescribed-sigma stacks on the largest level's shapes (sampled)
+    big = order[0]
+    L = info[big]
+    rng = np.random.default_rng([1703, 9085, 4, big])
+    idx = rng.choice(len(L["m"]), size=min(2048, len(L["m"])), replace=False)
+    stacks = []
+    for j in idx:
+        m, n, l = int(L["m"][j]), int(L["n"][j]), int(L["l"][j])
+        q = max(1, min(m, n, l) // 2)
+        s = 10.0 ** (-np.arange(q) / 2.0)
+        U, _ = np.linalg.qr(rng.standard_normal((m, q)))
+        V, _ = np.linalg.qr(rng.standard_normal((n, q)))
+        nt = int(rng.integers(1, 9))
+        cuts = np.sort(rng.choice(np.arange(1, q), size=min(nt - 1, q - 1), replace=False)) if q > 1 else []
+        As, Bs = [], []
+        for blk in np.split(np.arange(q), cuts):
+            As.append(U[:, blk] * s[blk])
+            Bs.append(V[:, blk])
+        A, B = np.hstack(As), np.hstack(Bs)
+        pad = l - A.shape[1]                      # widen to the captured stack width with exact zero columns
+        if pad > 0:
+            A = np.hstack([A, np.zeros((m, pad))])
+            B = np.hstack([B, np.zeros((n, pad))])
+        stacks.append((A, B))
+    sfl = sum(trunc_flops(a.shape[0], b.shape[0], a.shape[1], 0) for a, b in stacks)
+    hm.test_trunc_batched(ctx, stacks, eps)          # warm-up
+    # device time of the batched TRUNC only (the upload happens before e0)
+    _, ranks, _, ms = hm.test_trunc_batched(ctx, stacks, eps, timed=True)
+    out["synthetic"] = {"level_batch": big, "stacks": len(stacks), "gflop": sfl / 1e9, "ms": ms,
+                        "gflops": sfl / (ms * 1e-3) / 1e9, "seed": [1703, 9085, 4, int(big)],
+                        "recipe": "sigma_i = 10^(-i/2), q = min(m,n,l)/2, random orthonormal bases, 1-8 terms, "
+                                  "zero columns up to the captured width l"}
+    return out
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -260,6 +416,9 @@ def run_ours(args, cfg):
     ms = max_over_ranks(ms, dev)
     ms_step = ms / args.steps
     value = whole_job_value(ws, flops, ms_step)
+    # per-class times are summed over the timed steps: per step
+    prof_step = {k: {kk: (vv / args.steps if kk in ("ms", "flops", "bytes", "launches") else vv)
+                     for kk, vv in v.items()} for k, v in prof.items()}
 
     # ---- end to end through the C-ABI with host buffers
     dX, dY, dZ = X.export(), Y.export(), G.export()
@@ -280,7 +439,7 @@ def run_ours(args, cfg):
     for _ in range(e2e_steps):
         Xh, Yh, Zh = ctx.import_desc(dX), ctx.import_desc(dY), ctx.import_desc(dZ)
         hm.addmul(1.0, Xh, Yh, Zh, cfg["eps"])
-        out = Zh.export()
+        out = Zh.export(pinned=True)
         d2h = int(out["factors"].nbytes + out["dense"].nbytes)
         for m_ in (Xh, Yh, Zh):
             m_.free()
@@ -288,52 +447,52 @@ def run_ours(args, cfg):
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     e2e_value = ws * flops / (e2e_ms * 1e-3) / 1e9
 
-    # ---- roofline of the dominant kernel class
+    # ---- roofline of the top kernel functions
     peaks = load_peaks()
     dgemm = measure_dgemm_tflops(torch, dev) if rank == 0 else None
-    # dominant single kernel class ("qr" / "jacobi_svd" are aggregates of the bucketed launches)
-    top = max(((k, v) for k, v in prof.items() if k not in ("qr", "jacobi_svd")), key=lambda kv: kv[1]["ms"])
-    name, p = top
-    hbm = peaks.get("hbm_gbs", 6553.6)
-    if name in ("eval", "copy", "memset", "apply_q"):
-        bound, unit = "hbm", "GB/s"
-        achieved = p["bytes"] / (p["ms"] * 1e-3) / 1e9 if p["ms"] else 0.0
-        peak = hbm
-        peak_src = "MEASURED_PEAKS.json hbm_gbs (copy)"
-    else:
-        bound, unit = "alu", "TFLOP/s"
-        achieved = p["flops"] / (p["ms"] * 1e-3) / 1e12 if p["ms"] else 0.0
-        peak = NOMINAL_FP64_TFLOPS
-        peak_src = "FP64 DFMA nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6); tcgen05 has no f64 kind"
-    # dram traffic per launch of the class's kernel: the committed ncu launch
-    # list of one bench step (scripts/ncu_traffic.py -> profiles/*_traffic.json)
-    traffic, traffic_src = None, None
-    kern = CLASS_KERNEL.get(name)
     tfiles = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic.json"))
-    if kern and tfiles:
-        try:
-            tj = json.load(open(os.path.join(ROOT, "profiles", tfiles[-1])))
-            if kern in tj["kernels"]:
-                traffic = tj["kernels"][kern]["dram_bytes_per_launch"]
-                traffic_src = f"profiles/{tfiles[-1]} ({kern}, ncu dram__bytes_read+write per launch)"
-        except Exception:
-            pass
-    roof = {"bound": bound, "kernel": name, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_source": traffic_src,
-            "algorithmic_per_launch": (p["bytes"] if bound == "hbm" else p["flops"]) / max(p["launches"], 1),
-            "per_launch_ms": p["ms"] / max(p["launches"], 1), "launches": p["launches"], "peak_source": peak_src,
-            "dgemm_cublas_tflops_measured": dgemm,
+    traffic_file = os.path.join(ROOT, "profiles", tfiles[-1]) if tfiles else None
+    rows = roofline_report(prof_step, dgemm, peaks, traffic_file)
+    top = rows[0] if rows else {}
+    algo = top.get("gflop", 0) * 1e9 / max(top.get("launches", 1), 1) if top.get("bound") == "alu" else \
+        top.get("gb_algorithmic", 0) * 1e9 / max(top.get("launches", 1), 1)
+    roof = {"bound": top.get("bound"), "kernel": top.get("kernel"), "achieved": top.get("achieved"),
+            "peak": top.get("peak"), "unit": top.get("unit"), "frac": top.get("frac"),
+            "frac_nominal": top.get("frac_nominal"),
+            "traffic": top.get("ncu_dram_bytes_per_launch"),
+            "traffic_source": (f"{os.path.relpath(traffic_file, ROOT)} (ncu dram__bytes_read+write per launch, "
+                               f"function {NCU_NAME.get(top.get('class'), '?')})") if traffic_file else None,
+            "algorithmic_per_launch": algo, "per_launch_ms": top.get("ms", 0) / max(top.get("launches", 1), 1),
+            "launches_per_step": top.get("launches"), "share_of_step": top.get("share"),
+            "peak_source": ("measured cuBLAS DGEMM 8192^3 on this box (FP64 has no tcgen05 kind: DMMA/DFMA "
+                            f"nominal {NOMINAL_FP64_TFLOPS:.1f} TFLOP/s)") if top.get("bound") == "alu"
+            else "MEASURED_PEAKS.json hbm_gbs (copy)",
+            "dgemm_cublas_tflops_measured": dgemm, "nominal_fp64_tflops": NOMINAL_FP64_TFLOPS,
+            "top_functions": rows[:3],
             "classes": {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                             "gflop": round(v["flops"] / 1e9, 3), "gb": round(v["bytes"] / 1e9, 3)}
-                        for k, v in prof.items() if v["launches"]}}
+                        for k, v in prof_step.items() if v["launches"]}}
 
-    # ---- H-LR / H-Cholesky setup seconds (BASELINE configs[1], [2] and the
+    # ---- standalone batched flush (captured + synthetic)
+    flush = None
+    if rank == 0 and not args.no_flush:
+        try:
+            flush = standalone_flush(hm, ctx, torch, dev, X, Y, G, cfg["eps"])
+        except Exception as e:   # reported, never fatal for the main line
+            flush = {"error": repr(e)}
+
+    # ---- H-LR / H-Cholesky setup seconds (BASELINE configs[1], [2], [4] and the
     # metric's n = 81920 H-LR, "config 4'"), device time with CUDA events
     factor = {}
     if rank == 0 and not args.no_factor:
+        X.free(), Y.free(), G.free()
         for key, L, leaf, eps, kern, op, reps in FACTOR_RUNS:
+            if cfg["level"] < 6 and L > 5:
+                continue
             xf, wf = sphere_points(L)
+            tb = time.time()
             G0 = ctx.build(xf, wf, leaf, 2.0, eps, kernel=kern)
+            tb = time.time() - tb
             times = []
             for r in range(reps):
                 Gf = G0.clone()
@@ -348,13 +507,17 @@ def run_ours(args, cfg):
                 fst = ctx.last_stats()
                 Gf.free()
             G0.free()
+            fgf = (fst["flops_trunc"] + fst["flops_eval"] + fst["flops_dense"]) / 1e9
             factor[key] = {"setup_s": min(times), "runs": len(times), "n": len(wf), "leaf": leaf, "eps": eps,
-                           "truncations": fst["truncations"], "min_pivot": fst["min_pivot"]}
+                           "truncations": fst["truncations"], "trunc_cols": fst["trunc_cols"],
+                           "convention_gflop": fgf, "gflops": fgf / min(times), "min_pivot": fst["min_pivot"],
+                           "build_s": tb}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, dt, sample, gf = oracle_sample(cfg)
-        cpu = {"value": rate, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample}
+        cores = host_cores()
+        rate, dt, sample, gf, _ = oracle_sample(cfg, cores)
+        cpu = {"value": rate, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
 
     if rank == 0:
         line = {
@@ -372,6 +535,7 @@ def run_ours(args, cfg):
                         "mean_rank": gstats["mean_rank"], "max_rank": gstats["max_rank"], "build_s": build_s},
             "roofline": roof,
             "hlr_hchol_setup": factor,
+            "standalone_flush": flush,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -385,6 +549,14 @@ def run_ours(args, cfg):
     return 0
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -394,7 +566,13 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-factor", action="store_true", help="skip the H-LR / H-Cholesky setup timings")
+    ap.add_argument("--no-flush", action="store_true", help="skip the standalone batched-flush timing")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # replicas only (the path does not shard): spawn one rank per GPU
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)

@@ -242,6 +242,49 @@ hm_status hm_test_trunc_batched(hm_ctx ctx, int njobs, const int32_t* m, const i
                                 const int64_t* o_off, double* ub_dev, const int64_t* p_off,
                                 double eps, int32_t* ranks_host, double* sigma_host);
 
+/*
+ * Test-only export: batched H x thin-dense products (Fig. 1 addeval /
+ * addevaltrans) through the launch path of hm_addmul's A2 step
+ * (DFS leaf ranges of the block, row-group splitting of large jobs, one
+ * k_eval2 batch).  For job i with block b = blk[i] = (t, s) of H:
+ *   trans[i] = 0: out_i += coef[i] * H|_{t x s} V_i   (V_i: #s x w[i], out_i: #t x w[i])
+ *   trans[i] = 1: out_i += coef[i] * H|_{t x s}^T V_i (V_i: #t x w[i], out_i: #s x w[i])
+ * V_i at v_dev + v_off[i] (ld ldv[i]), out_i at out_dev + o_off[i] (ld
+ * ldo[i]), device, column-major; outputs of different jobs must not overlap.
+ * split_threshold > 0 forces the row-group split of every job whose cost
+ * estimate exceeds it (exercises the split path); <= 0: production rule.
+ * Synchronizes.
+ */
+hm_status hm_test_eval_batched(hm_ctx ctx, hm_mat H, int njobs, const int32_t* blk, const int32_t* trans,
+                               const double* coef, double* v_dev, const int64_t* v_off, const int32_t* ldv,
+                               double* out_dev, const int64_t* o_off, const int32_t* ldo, const int32_t* w,
+                               double split_threshold);
+
+/*
+ * Standalone batched flush (BASELINE configs[3]: "also timed
+ * as standalone batched flush"): the TRUNC_eps batches of the flush of Fig. 7
+ * captured in situ during an hm_addmul and replayed alone.
+ *   hm_flush_capture(ctx, mask): the NEXT hm_addmul of the context records,
+ *     per block-tree level (batch index 0, 1, ... in execution order), the
+ *     shapes (m, n, l) and resulting ranks of its TRUNC batch (T1 reduces and
+ *     T2/T3 flushes; rkmerge batches excluded), and for the levels whose bit
+ *     is set in `mask` a device copy of the stacked factors (up to tens of GB
+ *     per level, owned by the context until hm_flush_capture_free).
+ *   hm_flush_capture_info(ctx, level, njobs, m, n, l, k, has_data): level < 0:
+ *     *njobs = number of captured levels; else *njobs = batch size and, for
+ *     non-NULL host arrays of njobs entries, the shapes and ranks.
+ *   hm_flush_replay(ctx, level, eps, reps, ms_out, rank_sum): restores the
+ *     captured stacks (not timed) and runs the level's TRUNC batch `reps`
+ *     times; *ms_out = mean device time of the TRUNC batch (CUDA events on
+ *     the context stream), *rank_sum = sum of the resulting ranks (equal to
+ *     the in-situ ranks' sum: same inputs, same kernels).  Synchronizes.
+ */
+hm_status hm_flush_capture(hm_ctx ctx, uint64_t level_mask);
+hm_status hm_flush_capture_info(hm_ctx ctx, int level, int64_t* njobs, int32_t* m, int32_t* n, int32_t* l,
+                                int32_t* k, int* has_data);
+hm_status hm_flush_replay(hm_ctx ctx, int level, double eps, int reps, double* ms_out, int64_t* rank_sum);
+hm_status hm_flush_capture_free(hm_ctx ctx);
+
 #ifdef __cplusplus
 }
 #endif

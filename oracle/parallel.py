@@ -78,8 +78,10 @@ def _subtree_leaves(b):
 def _flush_worker(i):
     acc, zb = _G["items"][i]
     X, Y, Z, eps = _G["X"], _G["Y"], _G["Z"], _G["eps"]
+    from .flops import ConventionCounter
     ctx = TruncCtx(eps)
-    alg = S2(X, Y, ctx, Stats())
+    cc = ConventionCounter()
+    alg = S2(X, Y, ctx, Stats(), counter=cc)
     b = Z.bt.blocks[zb]
     alg.flush(acc, ZReal(Z, b))
     out = {}
@@ -88,14 +90,16 @@ def _flush_worker(i):
             out[leaf.id] = ("A", Z.A[leaf.id], Z.B[leaf.id])
         else:
             out[leaf.id] = ("N", Z.N[leaf.id])
-    return i, out, ctx.count, ctx.cols, [(n[1], n[2]) for n in ctx.near], alg.st.addproduct
+    return i, out, ctx.count, ctx.cols, [(n[1], n[2]) for n in ctx.near], alg.st.addproduct, cc.total_flops()
 
 
 def addmul_s2_parallel(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps, workers=None, frontier_depth=3):
     """Z <- blocktrunc(Z + alpha X Y), S2 schedule, identical to addmul_s2."""
+    from .flops import ConventionCounter
     workers = workers or os.cpu_count()
     ctx = TruncCtx(eps)
-    alg = S2(X, Y, ctx, Stats())
+    cc = ConventionCounter()   # SURVEY §8(d) convention work (timing reports only)
+    alg = S2(X, Y, ctx, Stats(), counter=cc)
     root = Z.bt.root
     acc = Acc2(root.t, root.s)
     alg.addproduct(acc, alpha, X.bt.root, Y.bt.root)
@@ -114,7 +118,9 @@ def addmul_s2_parallel(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps, workers=N
     _G.update(items=items, X=X, Y=Y, Z=Z, eps=eps)
     count, cols, near, addp = ctx.count, ctx.cols, [(n[1], n[2]) for n in ctx.near], alg.st.addproduct
     with mp.get_context("fork").Pool(workers) as pool:
-        for i, out, c, l, nr, ap in pool.imap_unordered(_flush_worker, range(len(items))):
+        conv = cc.total_flops()
+        for i, out, c, l, nr, ap, fl in pool.imap_unordered(_flush_worker, range(len(items))):
+            conv += fl
             for bid, v in out.items():
                 if v[0] == "A":
                     Z.A[bid], Z.B[bid] = v[1], v[2]
@@ -125,4 +131,5 @@ def addmul_s2_parallel(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps, workers=N
             near += nr
             addp += ap
     # near: (tag, k) of every near-threshold truncation (tags carry the (t, r) cluster ids)
-    return Z, dict(truncations=count, trunc_cols=cols, near=near, addproduct=addp, frontier=len(items))
+    return Z, dict(truncations=count, trunc_cols=cols, near=near, addproduct=addp, frontier=len(items),
+                   conv_gflop=conv / 1e9)

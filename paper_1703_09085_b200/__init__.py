@@ -248,9 +248,11 @@ def matvec(G: HMatrix, x, y, alpha=1.0, beta=0.0, op=0):
                                      float(beta), C.c_void_p(y.data_ptr()), ldy, ncols))
 
 
-def test_trunc_batched(ctx: Context, stacks, eps):
+def test_trunc_batched(ctx: Context, stacks, eps, timed=False):
     """Kernel-level parity export: list of (A (m x l), B (n x l)) numpy arrays ->
-    list of (U_k, V_k S_k) numpy arrays, ranks, sigmas (hm_test_trunc_batched)."""
+    list of (U_k, V_k S_k) numpy arrays, ranks, sigmas (hm_test_trunc_batched);
+    timed=True also returns the device ms of the C-ABI call (CUDA events on the
+    context stream, after the stacks are uploaded)."""
     import torch
     nj = len(stacks)
     m = np.array([a.shape[0] for a, b in stacks], np.int32)
@@ -284,11 +286,20 @@ def test_trunc_batched(ctx: Context, stacks, eps):
     ranks = np.zeros(nj, np.int32)
     qs = [int(min(mm, nn, ll)) for mm, nn, ll in zip(m, n, l)]
     sig = np.zeros(max(sum(qs), 1))
+    if timed:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
     ctx.check(lib().hm_test_trunc_batched(
         ctx.h, nj, _ptr(m, C.c_int32), _ptr(n, C.c_int32), _ptr(l, C.c_int32),
         C.c_void_p(A.data_ptr()), _ptr(a_off, C.c_int64), C.c_void_p(B.data_ptr()), _ptr(b_off, C.c_int64),
         C.c_void_p(UA.data_ptr()), _ptr(o_off, C.c_int64), C.c_void_p(UB.data_ptr()), _ptr(p_off, C.c_int64),
         float(eps), _ptr(ranks, C.c_int32), _ptr(sig, C.c_double)))
+    ms = None
+    if timed:
+        e1.record(ctx.stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
     ua = UA.cpu().numpy()
     ub = UB.cpu().numpy()
     out, sigmas, o = [], [], 0
@@ -299,7 +310,87 @@ def test_trunc_batched(ctx: Context, stacks, eps):
         out.append((U, V))
         sigmas.append(sig[o:o + qs[i]].copy())
         o += qs[i]
+    if timed:
+        return out, ranks, sigmas, ms
     return out, ranks, sigmas
 
 
-__all__ = ["Context", "HMatrix", "HMError", "addmul", "chol", "lr", "matvec", "lib", "test_trunc_batched"]
+def test_eval_batched(H: HMatrix, jobs, split_threshold=0.0):
+    """Kernel-level parity export of the A2 step (hm_test_eval_batched):
+    jobs = list of (block id, trans, coef, V numpy (rows x w)) -> list of
+    out numpy arrays (zero-initialised, out += coef op(H|_b) V)."""
+    import torch
+    ctx = H.ctx
+    dev = torch.device("cuda", ctx.device)
+    nj = len(jobs)
+    vs, outs = [], []
+    blk = np.array([j[0] for j in jobs], np.int32)
+    tr = np.array([1 if j[1] else 0 for j in jobs], np.int32)
+    coef = np.array([j[2] for j in jobs], np.float64)
+    d = H.export()
+    cz = d["cl_size"]
+    ldv = np.zeros(nj, np.int32)
+    ldo = np.zeros(nj, np.int32)
+    w = np.zeros(nj, np.int32)
+    v_off = np.zeros(nj, np.int64)
+    o_off = np.zeros(nj, np.int64)
+    tv = to = 0
+    for i, (b, t, c, V) in enumerate(jobs):
+        rows_out = int(cz[d["bl_col"][b]] if t else cz[d["bl_row"][b]])
+        assert V.shape[0] == int(cz[d["bl_row"][b]] if t else cz[d["bl_col"][b]])
+        ldv[i], ldo[i], w[i] = V.shape[0], rows_out, V.shape[1]
+        v_off[i], o_off[i] = tv, to
+        tv += V.size + 1
+        to += rows_out * V.shape[1] + 1
+    hv = np.zeros(max(tv, 1))
+    for i, j in enumerate(jobs):
+        hv[v_off[i]:v_off[i] + j[3].size] = np.asarray(j[3], np.float64).ravel(order="F")
+    Vd = torch.from_numpy(hv).to(dev)
+    Od = torch.zeros(max(to, 1), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    ctx.check(lib().hm_test_eval_batched(ctx.h, H.h, nj, _ptr(blk, C.c_int32), _ptr(tr, C.c_int32),
+                                         _ptr(coef, C.c_double), C.c_void_p(Vd.data_ptr()), _ptr(v_off, C.c_int64),
+                                         _ptr(ldv, C.c_int32), C.c_void_p(Od.data_ptr()), _ptr(o_off, C.c_int64),
+                                         _ptr(ldo, C.c_int32), _ptr(w, C.c_int32), float(split_threshold)))
+    ho = Od.cpu().numpy()
+    for i in range(nj):
+        outs.append(ho[o_off[i]:o_off[i] + int(ldo[i]) * int(w[i])].reshape((int(ldo[i]), int(w[i])), order="F"))
+    return outs
+
+
+def flush_capture(ctx: Context, level_mask):
+    """Record the TRUNC batches of the next addmul (hm_flush_capture)."""
+    ctx.check(lib().hm_flush_capture(ctx.h, C.c_uint64(int(level_mask))))
+
+
+def flush_capture_info(ctx: Context):
+    """List of per-level dicts (m, n, l, k arrays, has_data) of the capture."""
+    nl = C.c_int64()
+    ctx.check(lib().hm_flush_capture_info(ctx.h, -1, C.byref(nl), None, None, None, None, None))
+    out = []
+    for lev in range(nl.value):
+        nj = C.c_int64()
+        ctx.check(lib().hm_flush_capture_info(ctx.h, lev, C.byref(nj), None, None, None, None, None))
+        a = {k: np.zeros(nj.value, np.int32) for k in ("m", "n", "l", "k")}
+        hd = C.c_int()
+        ctx.check(lib().hm_flush_capture_info(ctx.h, lev, C.byref(nj), _ptr(a["m"], C.c_int32), _ptr(a["n"], C.c_int32),
+                                              _ptr(a["l"], C.c_int32), _ptr(a["k"], C.c_int32), C.byref(hd)))
+        a["has_data"] = bool(hd.value)
+        out.append(a)
+    return out
+
+
+def flush_replay(ctx: Context, level, eps, reps=1):
+    """Replay one captured level's TRUNC batch: (mean device ms, rank sum)."""
+    ms = C.c_double()
+    rs = C.c_int64()
+    ctx.check(lib().hm_flush_replay(ctx.h, int(level), float(eps), int(reps), C.byref(ms), C.byref(rs)))
+    return ms.value, rs.value
+
+
+def flush_capture_free(ctx: Context):
+    ctx.check(lib().hm_flush_capture_free(ctx.h))
+
+
+__all__ = ["Context", "HMatrix", "HMError", "addmul", "chol", "lr", "matvec", "lib", "test_trunc_batched",
+           "test_eval_batched", "flush_capture", "flush_capture_info", "flush_replay", "flush_capture_free"]

@@ -66,7 +66,8 @@ EXPORTS = [
     "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_build",
     "hm_import", "hm_export", "hm_export_sizes", "hm_export_into", "hm_clone", "hm_free", "hm_addmul", "hm_lr", "hm_chol",
     "hm_matvec_thin", "hm_stats", "hm_profile_enable", "hm_profile_reset", "hm_profile_get",
-    "hm_test_trunc_batched",
+    "hm_test_trunc_batched", "hm_test_eval_batched",
+    "hm_flush_capture", "hm_flush_capture_info", "hm_flush_replay", "hm_flush_capture_free",
 ]
 
 
@@ -102,6 +103,12 @@ def load(path: str = LIB_PATH):
         "hm_profile_get": (C.c_int, [vp, C.POINTER(Prof)]),
         "hm_test_trunc_batched": (C.c_int, [vp, C.c_int, P_i32, P_i32, P_i32, vp, P_i64, vp, P_i64,
                                             vp, P_i64, vp, P_i64, C.c_double, P_i32, P_f64]),
+        "hm_test_eval_batched": (C.c_int, [vp, vp, C.c_int, P_i32, P_i32, P_f64, vp, P_i64, P_i32, vp, P_i64,
+                                           P_i32, P_i32, C.c_double]),
+        "hm_flush_capture": (C.c_int, [vp, C.c_uint64]),
+        "hm_flush_capture_info": (C.c_int, [vp, C.c_int, P_i64, P_i32, P_i32, P_i32, P_i32, C.POINTER(C.c_int)]),
+        "hm_flush_replay": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, P_f64, P_i64]),
+        "hm_flush_capture_free": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

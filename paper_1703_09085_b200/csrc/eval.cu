@@ -371,14 +371,18 @@ __device__ void eval_range(const EvalJob& J, int lb, int le, double* sm) {
 
 __global__ void __launch_bounds__(kNT, 3) k_eval2(const EvalJob* __restrict__ jobs) {
   extern __shared__ double sm[];
-  const EvalJob J = jobs[blockIdx.x];
-  if (J.nrng == 0) {
-    eval_range(J, J.leaf_begin, J.leaf_end, sm);
-  } else {
-    for (int g = 0; g < J.nrng; g++) {
-      const int2 r = J.rng[g];
-      eval_range(J, r.x, r.y, sm);
+  const EvalJob* jp = &jobs[blockIdx.x];
+  while (jp) {
+    const EvalJob J = *jp;
+    if (J.nrng == 0) {
+      eval_range(J, J.leaf_begin, J.leaf_end, sm);
+    } else {
+      for (int g = 0; g < J.nrng; g++) {
+        const int2 r = J.rng[g];
+        eval_range(J, r.x, r.y, sm);
+      }
     }
+    jp = J.next;   // eval_range ends with a barrier: the chained job sees this one's writes
   }
 }
 

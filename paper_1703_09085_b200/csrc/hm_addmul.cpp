@@ -38,7 +38,10 @@ struct FP {            // device factor pair; rows relative to clusters starting
   int k;
 };
 
-struct Term { int bx, by, br, w; };
+struct Term {
+  int bx, by, br, w;
+  bool xd = false, yd = false;   // X|ts / Y|sr is a dense leaf (identity branches 0 / 2 available)
+};
 struct Pend { int bx, by; };
 
 struct Node {
@@ -91,6 +94,8 @@ struct Planner {
     const int t = T.bl_row[bx], s = T.bl_col[bx], r = T.bl_col[by];
     out.bx = bx;
     out.by = by;
+    out.xd = kx == HM_BLOCK_DENSE;
+    out.yd = ky == HM_BLOCK_DENSE;
     if (kx == HM_BLOCK_DENSE) {
       if (csize(t) <= csize(s)) { out.br = 0; out.w = csize(t); }
       else { out.br = 1; out.w = csize(s); }
@@ -176,6 +181,7 @@ struct Planner {
   // (yside = true); trans: out += coef H|_blk^T V instead of H|_blk V.
   struct EvalMeta { double cost; int blk, yside; };
   std::vector<EvalMeta> emeta;   // host-side companions of the level's EvalJobs
+  double split_thr = -1;         // > 0: fixed split threshold (hm_test_eval_batched)
   std::vector<int2> erng;        // leaf-range table of split jobs (uploaded with the jobs)
 
   void add_eval(std::vector<EvalJob>& ej, bool yside, int blk, int trans, double coef, double* out,
@@ -225,7 +231,7 @@ struct Planner {
     for (auto& m : emeta) total += m.cost;
     static const double div = [] { const char* e = std::getenv("HM_EVAL_SPLIT"); return e ? std::atof(e) : 1184.0; }();
     if (div <= 0) return;
-    const double thr = std::max(total / div, 2e5);
+    const double thr = split_thr > 0 ? split_thr : std::max(total / div, 2e5);
     std::vector<EvalJob> out;
     std::vector<EvalMeta> mout;
     out.reserve(ej.size());
@@ -233,7 +239,7 @@ struct Planner {
     for (size_t ji = 0; ji < ej.size(); ji++) {
       const EvalJob& e = ej[ji];
       const EvalMeta& em = emeta[ji];
-      if (em.cost <= thr) { out.push_back(e); mout.push_back(em); continue; }
+      if (em.cost <= thr || e.next) { out.push_back(e); mout.push_back(em); continue; }
       const std::vector<double>& pm = em.yside ? ly_mat : lx_mat;
       const std::vector<double>& pn = em.yside ? ly_mn : lx_mn;
       auto bcost = [&](int b) {
@@ -291,6 +297,38 @@ struct Planner {
     emeta.swap(mout);
   }
 
+  // Split (load balance), sort largest-first and launch one k_eval2 batch.
+  void launch_evals(std::vector<EvalJob>& ej, Arena& scratch, double fl, double by) {
+    if (ej.empty()) return;
+    split_evals(ej);
+    std::vector<int> order(ej.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return emeta[a].cost > emeta[b].cost; });
+    const int2* drng = erng.empty() ? nullptr : scratch.upload(erng);
+    EvalJob* dtail = nullptr;
+    if (!etail.empty()) {
+      dtail = static_cast<EvalJob*>(scratch.alloc_bytes(etail.size() * sizeof(EvalJob)));
+      for (auto& t : etail)
+        if (t.next) t.next = dtail + (reinterpret_cast<intptr_t>(t.next) - 1);
+      void* h = c->pinned(etail.size() * sizeof(EvalJob));
+      std::memcpy(h, etail.data(), etail.size() * sizeof(EvalJob));
+      HM_CUDA(cudaMemcpyAsync(dtail, h, etail.size() * sizeof(EvalJob), cudaMemcpyHostToDevice, c->stream));
+    }
+    std::vector<EvalJob> sorted(ej.size());
+    for (size_t i = 0; i < order.size(); i++) {
+      sorted[i] = ej[order[i]];
+      if (sorted[i].nrng > 0) sorted[i].rng = drng + reinterpret_cast<intptr_t>(sorted[i].rng);
+      if (sorted[i].next) sorted[i].next = dtail + (reinterpret_cast<intptr_t>(sorted[i].next) - 1);
+    }
+    emeta.clear();
+    erng.clear();
+    ej.clear();
+    etail.clear();
+    ProfScope ps(c, PC_EVAL, fl, by);
+    launch_eval2(scratch.upload(sorted), (int)sorted.size(), c->stream);
+    HM_CHECK_LAUNCH();
+  }
+
   // Emit the A2 realisation of one evaluated term into stack columns [col, col+w).
   void emit_term(const Term& tm, double* SA, int m, double* SB, int n, int col,
                  std::vector<CopyJob>& cj, int64_t& ctiles, std::vector<EvalJob>& ej) {
@@ -333,6 +371,93 @@ struct Planner {
     }
   }
 
+  // Identity pre-summing (exact; reading R7d): every term of one
+  // accumulator (t, r) whose X|ts is a dense leaf may take Fig. 5's branch
+  // A_hat = alpha I_t, and sum_i alpha I_t B_hat_i^T = alpha I_t (sum_i B_hat_i)^T
+  // is ONE column block of width #t; likewise B_hat = I_r for dense Y|sr.  The
+  // exact matrix the accumulator truncates is unchanged -- only the stack gets
+  // narrower (the same argument as the narrowest-branch reading R7b).
+  struct Groups {
+    std::vector<char> role;   // per term: 0 own columns, 1 I_t group, 2 I_r group
+    int wt = 0, wr = 0, width = 0;
+  };
+  bool presum = [] { const char* e = std::getenv("HM_NO_PRESUM"); return !(e && e[0] == '1'); }();
+
+  Groups plan_groups(const Node& nd) const {
+    Groups best;
+    const int nterm = (int)nd.terms.size();
+    best.role.assign(nterm, 0);
+    for (auto& tm : nd.terms) best.width += tm.w;
+    if (!presum || nterm < 2) return best;
+    const int gwid[3] = {0, csize(nd.t), csize(nd.r)};
+    for (int first = 1; first <= 2; first++) {
+      Groups g;
+      g.role.assign(nterm, 0);
+      for (int pass = 0; pass < 2; pass++) {
+        const int which = pass == 0 ? first : 3 - first;
+        int s = 0, cnt = 0;
+        for (int i = 0; i < nterm; i++)
+          if (!g.role[i] && (which == 1 ? nd.terms[i].xd : nd.terms[i].yd)) { s += nd.terms[i].w; cnt++; }
+        if (cnt < 2 || s <= gwid[which]) continue;
+        for (int i = 0; i < nterm; i++)
+          if (!g.role[i] && (which == 1 ? nd.terms[i].xd : nd.terms[i].yd)) g.role[i] = (char)which;
+        (which == 1 ? g.wt : g.wr) = gwid[which];
+      }
+      g.width = g.wt + g.wr;
+      for (int i = 0; i < nterm; i++)
+        if (!g.role[i]) g.width += nd.terms[i].w;
+      if (g.width < best.width) best = std::move(g);
+    }
+    return best;
+  }
+
+  // chained continuation jobs of the current eval batch (identity groups)
+  std::vector<EvalJob> etail;
+  void add_eval_chained(std::vector<EvalJob>& ej, int& head, int& last, bool yside, int blk, int trans,
+                        double coef, double* out, int ldo, int w, const double* V, int ldv, int vtrans) {
+    add_eval(ej, yside, blk, trans, coef, out, ldo, w, V, ldv, vtrans, 0);
+    if (head < 0) {
+      head = (int)ej.size() - 1;
+      last = -1;
+      return;
+    }
+    EvalJob e = ej.back();
+    ej.pop_back();
+    emeta[head].cost += emeta.back().cost;
+    emeta.pop_back();
+    e.next = nullptr;
+    etail.push_back(e);
+    const intptr_t idx = (intptr_t)etail.size();   // 1-based link, resolved at upload
+    if (last < 0) ej[head].next = reinterpret_cast<const EvalJob*>(idx);
+    else etail[last].next = reinterpret_cast<const EvalJob*>(idx);
+    last = (int)idx - 1;
+  }
+
+  // one identity group: which = 1 (A = alpha I_t, B = sum_i Y|s_i r^T N_X(t,s_i)^T)
+  // or 2 (B = I_r, A = sum_i alpha X|t s_i N_Y(s_i,r))
+  void emit_group(const Node& nd, const Groups& g, int which, double* SA, int m, double* SB, int n, int col,
+                  std::vector<CopyJob>& cj, int64_t& ctiles, std::vector<EvalJob>& ej) {
+    double* a = SA + (size_t)col * m;
+    double* b = SB + (size_t)col * n;
+    const int nt = csize(nd.t), nr = csize(nd.r);
+    int head = -1, last = -1;
+    if (which == 1) add_copy(cj, ctiles, a, m, nullptr, 0, nt, nt, 0, 1, alpha);
+    else add_copy(cj, ctiles, b, n, nullptr, 0, nr, nr, 0, 1, 1.0);
+    for (size_t i = 0; i < nd.terms.size(); i++) {
+      if (g.role[i] != which) continue;
+      const Term& tm = nd.terms[i];
+      const int bx = tm.bx, by = tm.by, ybk = yb(by);
+      const int ns = csize(T.bl_col[bx]);
+      if (which == 1) {
+        add_eval_chained(ej, head, last, true, ybk, ytrans ? 0 : 1, 1.0, b, n, nt, X->pA[bx], nt, 1);
+      } else if (ytrans) {
+        add_eval_chained(ej, head, last, false, bx, 0, alpha, a, m, nr, Y->pA[ybk], nr, 1);
+      } else {
+        add_eval_chained(ej, head, last, false, bx, 0, alpha, a, m, nr, Y->pA[by], ns, 0);
+      }
+    }
+  }
+
   void copy_view(const FP& f, int t, int r, double* SA, int m, double* SB, int n, int col,
                  std::vector<CopyJob>& cj, int64_t& ctiles) {
     if (f.k <= 0) return;
@@ -365,12 +490,16 @@ struct Planner {
     int* d_ranks = nullptr;
     std::vector<TruncReq> tr;
     std::vector<int> tr_fp;
+    int cap_level = -1;
   };
+  bool capture = false;   // hm_addmul with ctx->cap_on: record every level's TRUNC batch
 
   void run_level(std::vector<Node>& nodes) { run_level_finish(run_level_enqueue(nodes)); }
 
   void run_level_finish(LevelTail lt) {
     sync_ranks(lt.d_ranks, lt.tr_fp);
+    if (lt.cap_level >= 0)
+      for (size_t i = 0; i < lt.tr.size(); i++) c->cap[lt.cap_level].k.push_back(fps[lt.tr_fp[i]].k);
     for (size_t i = 0; i < lt.tr.size(); i++) {
       const double k = fps[lt.tr_fp[i]].k;
       fl_trunc += trunc_flops(lt.tr[i].m, lt.tr[i].n, lt.tr[i].l, k);
@@ -387,13 +516,14 @@ struct Planner {
     lt.scratch.reset(new Arena(c));
     Arena& scratch = *lt.scratch;
     std::vector<Stack> stacks;
+    std::vector<Groups> groups(nodes.size());
     for (int i = 0; i < (int)nodes.size(); i++) {
       Node& nd = nodes[i];
       const int m = csize(nd.t), n = csize(nd.r);
       int kind = 0, l = 0;
       const int kb = nd.base >= 0 ? fps[nd.base].k : 0;
-      int wt = 0;
-      for (auto& tm : nd.terms) wt += tm.w;
+      groups[i] = plan_groups(nd);
+      const int wt = groups[i].width;
       if (!nd.pend.empty() || nd.force_split) {
         if (nd.zt == ZD && !nd.force_split)
           throw Error(HM_ESTRUCT, "flush: pending products into an inadmissible leaf");
@@ -459,34 +589,9 @@ struct Planner {
     };
     auto flush_eval = [&]() {
       if (ej.empty()) return;
-      split_evals(ej);
-      // largest first (index sort: the jobs themselves are moved once)
-      std::vector<int> order(ej.size());
-      std::iota(order.begin(), order.end(), 0);
-      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return emeta[a].cost > emeta[b].cost; });
-      if (const char* dump = std::getenv("HM_DUMP_EVAL")) {   // diagnostics: job cost spread per batch
-        if (FILE* f = std::fopen(dump, "a")) {
-          double sum = 0;
-          for (auto& m : emeta) sum += m.cost;
-          std::fprintf(f, "jobs %zu sum %.4g max %.4g p50 %.4g ranges %zu\n", ej.size(), sum,
-                       emeta[order[0]].cost, emeta[order[order.size() / 2]].cost, erng.size());
-          std::fclose(f);
-        }
-      }
-      const int2* drng = erng.empty() ? nullptr : scratch.upload(erng);
-      std::vector<EvalJob> sorted(ej.size());
-      for (size_t i = 0; i < order.size(); i++) {
-        sorted[i] = ej[order[i]];
-        if (sorted[i].nrng > 0) sorted[i].rng = drng + reinterpret_cast<intptr_t>(sorted[i].rng);
-      }
-      emeta.clear();
-      erng.clear();
-      ej.clear();
-      ProfScope ps(c, PC_EVAL, fl_eval - fl_eval0, by_eval - by_eval0);
+      launch_evals(ej, scratch, fl_eval - fl_eval0, by_eval - by_eval0);
       fl_eval0 = fl_eval;
       by_eval0 = by_eval;
-      launch_eval2(scratch.upload(sorted), (int)sorted.size(), c->stream);
-      HM_CHECK_LAUNCH();
     };
     for (auto& s : stacks) {
       Node& nd = nodes[s.node];
@@ -500,9 +605,19 @@ struct Planner {
         copy_view(fps[nd.base], nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
         col += fps[nd.base].k;
       }
-      for (auto& tm : nd.terms) {
-        emit_term(tm, s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
-        col += tm.w;
+      const Groups& g = groups[s.node];
+      if (g.wt) {
+        emit_group(nd, g, 1, s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
+        col += g.wt;
+      }
+      if (g.wr) {
+        emit_group(nd, g, 2, s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
+        col += g.wr;
+      }
+      for (size_t ti = 0; ti < nd.terms.size(); ti++) {
+        if (g.role[ti]) continue;
+        emit_term(nd.terms[ti], s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
+        col += nd.terms[ti].w;
       }
       if (ej.size() >= kChunk) flush_eval();
       if (cj.size() >= kChunk) flush_copy();
@@ -551,6 +666,24 @@ struct Planner {
     }
     double t3 = now_s();
     t_c += t3 - t2;
+    if (capture) {
+      const int lev = (int)c->cap.size();
+      c->cap.emplace_back();
+      Ctx::CapLevel& L = c->cap.back();
+      for (const TruncReq& q : tr) {
+        L.m.push_back(q.m);
+        L.n.push_back(q.n);
+        L.l.push_back(q.l);
+        L.aoff.push_back((size_t)(q.A - buf));
+        L.boff.push_back((size_t)(q.B - buf));
+      }
+      if (lev < 64 && ((c->cap_mask >> lev) & 1) && total > 0) {
+        L.ndoubles = total;
+        L.data = static_cast<double*>(c->dmalloc(total * sizeof(double)));
+        HM_CUDA(cudaMemcpyAsync(L.data, buf, total * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      }
+      lt.cap_level = lev;
+    }
     trunc_batched(c, scratch, tr, eps);
     t_d += now_s() - t3;
     for (auto& s : stacks) {
@@ -929,6 +1062,12 @@ struct Factorizer {
 
   void flush_many(std::vector<Node> roots) {
     if (roots.empty()) return;
+    if (c->plog) {
+      int pend = 0;
+      for (auto& r : roots) pend += !r.pend.empty();
+      c->prof_note("FLUSH roots " + std::to_string(roots.size()) + " withpend " + std::to_string(pend));
+      ProfScope mark(c, PC_MEMSET, 0, 0);
+    }
     n_flush += (int64_t)roots.size();
     n_flush_calls++;
     Arena local(c, true);
@@ -983,6 +1122,10 @@ struct Factorizer {
     }
     if (batch.empty()) return;
     n_reduce_calls++;
+    if (c->plog) {
+      c->prof_note("REDUCE " + std::to_string(batch.size()));
+      ProfScope mark(c, PC_MEMSET, 0, 0);
+    }
     P.run_level(batch);
     for (size_t i = 0; i < who.size(); i++) who[i]->red = batch[i].red;
   }
@@ -1295,6 +1438,71 @@ struct Factorizer {
 
 }  // namespace
 
+// Kernel-level parity export of the batched H x thin-dense product (Fig. 1
+// addeval / addevaltrans) exactly as the product launches it.
+void eval_batched_test(Ctx* c, Mat* H, int njobs, const int* blk, const int* trans, const double* coef,
+                       const double* const* V, const int* ldv, double* const* out, const int* ldo, const int* w,
+                       double split_thr) {
+  const Tree& T = *H->tree;
+  Planner P(c, T, H, H, H, 1.0, 0.0);
+  P.setup_tables(true);
+  P.split_thr = split_thr;
+  Arena scratch(c);
+  std::vector<EvalJob> ej;
+  for (int i = 0; i < njobs; i++) {
+    if (blk[i] < 0 || blk[i] >= T.nblocks()) throw Error(HM_EINVAL, "hm_test_eval_batched: bad block id");
+    P.add_eval(ej, false, blk[i], trans[i] ? 1 : 0, coef[i], out[i], ldo[i], w[i], V[i], ldv[i], 0, 0);
+  }
+  P.launch_evals(ej, scratch, P.fl_eval, P.by_eval);
+  HM_CUDA(cudaStreamSynchronize(c->stream));
+  P.persist.release();
+}
+
+// Standalone batched flush: replay the TRUNC batch of
+// one captured level of the last hm_addmul from its captured stacks.
+void flush_replay(Ctx* c, int level, double eps, int reps, double* ms_out, int64_t* rank_sum) {
+  if (level < 0 || level >= (int)c->cap.size()) throw Error(HM_EINVAL, "hm_flush_replay: no such captured level");
+  const Ctx::CapLevel& L = c->cap[level];
+  if (!L.data) throw Error(HM_EINVAL, "hm_flush_replay: level captured without data (cap mask)");
+  const int nj = (int)L.m.size();
+  double* work = c->stack_ws(L.ndoubles + 1);
+  Arena out(c);
+  std::vector<double*> oa(nj), ob(nj);
+  for (int i = 0; i < nj; i++) {
+    const int kc = trunc_kcap(L.m[i], L.n[i], L.l[i]);
+    oa[i] = out.alloc((size_t)L.m[i] * std::max(kc, 1));
+    ob[i] = out.alloc((size_t)L.n[i] * std::max(kc, 1));
+  }
+  int* d_rank = static_cast<int*>(out.alloc_bytes(sizeof(int) * (nj + 1)));
+  cudaEvent_t e0, e1;
+  HM_CUDA(cudaEventCreate(&e0));
+  HM_CUDA(cudaEventCreate(&e1));
+  double total_ms = 0;
+  std::vector<int> hr(nj);
+  for (int r = 0; r < std::max(reps, 1); r++) {
+    HM_CUDA(cudaMemcpyAsync(work, L.data, L.ndoubles * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    std::vector<TruncReq> tr(nj);
+    for (int i = 0; i < nj; i++)
+      tr[i] = TruncReq{L.m[i], L.n[i], L.l[i], work + L.aoff[i], work + L.boff[i], oa[i], ob[i], d_rank + i, nullptr};
+    Arena scratch(c);
+    HM_CUDA(cudaEventRecord(e0, c->stream));
+    trunc_batched(c, scratch, tr, eps);
+    HM_CUDA(cudaEventRecord(e1, c->stream));
+    HM_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    HM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    total_ms += ms;
+    scratch.release();
+  }
+  HM_CUDA(cudaMemcpy(hr.data(), d_rank, sizeof(int) * nj, cudaMemcpyDeviceToHost));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  int64_t s = 0;
+  for (int i = 0; i < nj; i++) s += hr[i];
+  if (rank_sum) *rank_sum = s;
+  if (ms_out) *ms_out = total_ms / std::max(reps, 1);
+}
+
 void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_pivot) {
   if (!G) throw Error(HM_EINVAL, "hm_lr/hm_chol: null matrix");
   if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_lr/hm_chol: eps must be >= 0");
@@ -1360,7 +1568,12 @@ void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps) {
     throw Error(HM_ESTRUCT, "hm_addmul: X, Y and Z must share one block tree");
   c->sp_prepare();
   Planner P(c, T, X, Y, Z, alpha, eps);
+  if (c->cap_on) {
+    c->cap_free();
+    P.capture = true;
+  }
   P.run();
+  c->cap_on = false;
   hm_stats_t& s = c->last;
   s.addproduct_calls = P.n_addproduct;
   s.evaluated_terms = P.n_eval;

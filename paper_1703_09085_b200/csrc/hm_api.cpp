@@ -1,6 +1,7 @@
 // C-ABI entry points of libhm (include/hm.h).  Every entry point catches
 // all exceptions and converts them to hm_status + hm_last_error().
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -490,6 +491,8 @@ hm_status hm_stats(hm_ctx ctx, hm_mat m, hm_stats_t* out) {
 hm_status hm_profile_enable(hm_ctx ctx, int on) {
   if (!ctx) return HM_EINVAL;
   ctx->c.prof = on != 0;
+  if (ctx->c.prof && !ctx->c.plog)
+    if (const char* f = std::getenv("HM_PROF_LOG")) ctx->c.plog = std::fopen(f, "w");
   return HM_OK;
 }
 
@@ -562,6 +565,73 @@ hm_status hm_test_trunc_batched(hm_ctx ctx, int njobs, const int32_t* m, const i
         o += q;
       }
     }
+  });
+}
+
+hm_status hm_test_eval_batched(hm_ctx ctx, hm_mat H, int njobs, const int32_t* blk, const int32_t* trans,
+                               const double* coef, double* v_dev, const int64_t* v_off, const int32_t* ldv,
+                               double* out_dev, const int64_t* o_off, const int32_t* ldo, const int32_t* w,
+                               double split_threshold) {
+  if (!ctx || !H || njobs < 0 || (njobs > 0 && (!blk || !trans || !coef || !v_off || !ldv || !o_off || !ldo || !w)))
+    return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    std::vector<const double*> V(njobs);
+    std::vector<double*> O(njobs);
+    for (int i = 0; i < njobs; i++) {
+      if (w[i] <= 0 || ldv[i] <= 0 || ldo[i] <= 0) throw Error(HM_EINVAL, "hm_test_eval_batched: bad panel shape");
+      V[i] = v_dev + v_off[i];
+      O[i] = out_dev + o_off[i];
+    }
+    eval_batched_test(&ctx->c, &H->m, njobs, blk, trans, coef, V.data(), ldv, O.data(), ldo, w, split_threshold);
+  });
+}
+
+hm_status hm_flush_capture(hm_ctx ctx, uint64_t level_mask) {
+  if (!ctx) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    ctx->c.cap_free();
+    ctx->c.cap_on = true;
+    ctx->c.cap_mask = level_mask;
+  });
+}
+
+hm_status hm_flush_capture_info(hm_ctx ctx, int level, int64_t* njobs, int32_t* m, int32_t* n, int32_t* l,
+                                int32_t* k, int* has_data) {
+  if (!ctx || !njobs) return HM_EINVAL;
+  return guard(ctx, [&] {
+    if (level < 0) {            // number of captured levels
+      *njobs = (int64_t)ctx->c.cap.size();
+      return;
+    }
+    if (level >= (int)ctx->c.cap.size()) throw Error(HM_EINVAL, "hm_flush_capture_info: no such level");
+    const Ctx::CapLevel& L = ctx->c.cap[level];
+    *njobs = (int64_t)L.m.size();
+    if (has_data) *has_data = L.data != nullptr;
+    for (size_t i = 0; i < L.m.size(); i++) {
+      if (m) m[i] = L.m[i];
+      if (n) n[i] = L.n[i];
+      if (l) l[i] = L.l[i];
+      if (k) k[i] = i < L.k.size() ? L.k[i] : -1;
+    }
+  });
+}
+
+hm_status hm_flush_replay(hm_ctx ctx, int level, double eps, int reps, double* ms_out, int64_t* rank_sum) {
+  if (!ctx) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    flush_replay(&ctx->c, level, eps, reps, ms_out, rank_sum);
+  });
+}
+
+hm_status hm_flush_capture_free(hm_ctx ctx) {
+  if (!ctx) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    ctx->c.cap_free();
+    ctx->c.cap_on = false;
   });
 }
 

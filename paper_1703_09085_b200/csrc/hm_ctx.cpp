@@ -35,13 +35,21 @@ void* Ctx::pinned(size_t bytes) {
   return p;
 }
 
+void Ctx::cap_free() {
+  for (auto& L : cap)
+    if (L.data) dfree(L.data, L.ndoubles * sizeof(double));
+  cap.clear();
+}
+
 Ctx::~Ctx() {
   cudaSetDevice(device);
+  cap_free();
   if (ws) dfree(ws, ws_cap * sizeof(double));
   if (sp) dfree(sp, sp_cap);
   cudaStreamSynchronize(stream);
   if (pin) cudaFreeHost(pin);
   if (pool) cudaMemPoolDestroy(pool);
+  if (plog) std::fclose(plog);
 }
 
 double* Ctx::stack_ws(size_t ndoubles) {
@@ -97,13 +105,18 @@ void Ctx::prof_begin(int cls, cudaEvent_t* a) {
   if (!prof) return;
   *a = get_event();
   HM_CUDA(cudaEventRecord(*a, stream));
+  if (plog && !pbase) {
+    HM_CUDA(cudaEventCreate(&pbase));
+    HM_CUDA(cudaEventRecord(pbase, stream));
+  }
 }
 
 void Ctx::prof_end(int cls, cudaEvent_t a, double fl, double by) {
   if (!prof || !a) return;
   cudaEvent_t b = get_event();
   cudaEventRecord(b, stream);
-  pend.push_back(Pending{cls, a, b, fl, by});
+  pend.push_back(Pending{cls, a, b, fl, by, std::move(note)});
+  note.clear();
   if (pend.size() > 4096) prof_collect();
 }
 
@@ -113,6 +126,11 @@ void Ctx::prof_collect() {
     float ms_ = 0.f;
     cudaEventElapsedTime(&ms_, p.a, p.b);
     ms[p.cls] += ms_;
+    if (plog) {
+      float t0 = 0.f;
+      if (pbase) cudaEventElapsedTime(&t0, pbase, p.a);
+      std::fprintf(plog, "%d %.4f %.4f %s\n", p.cls, t0, ms_, p.note.c_str());
+    }
     launches[p.cls] += 1;
     flops[p.cls] += p.flops;
     bytes[p.cls] += p.bytes;

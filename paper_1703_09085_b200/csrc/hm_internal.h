@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -51,11 +52,30 @@ struct Ctx {
   bool has_alloc = false;
   cudaMemPool_t pool = nullptr;   // private stream-ordered pool (no allocator hook)
   std::set<void*> live;            // hm_mat handles owned by this context
+  // standalone batched-flush capture (hm_flush_capture / hm_flush_replay):
+  // per level of the next hm_addmul the TRUNC batch's shapes and ranks, and for
+  // the levels in cap_mask a device copy of the stacked factors (consumed by
+  // the TRUNC, so replays restore them from this copy)
+  struct CapLevel {
+    std::vector<int> m, n, l, k;
+    std::vector<size_t> aoff, boff;   // doubles, relative to data
+    double* data = nullptr;
+    size_t ndoubles = 0;
+  };
+  bool cap_on = false;
+  uint64_t cap_mask = 0;
+  std::vector<CapLevel> cap;
+  void cap_free();
   std::string err;
   hm_stats_t last{};
   // profiling
   bool prof = false;
-  struct Pending { int cls; cudaEvent_t a, b; double flops, bytes; };
+  struct Pending { int cls; cudaEvent_t a, b; double flops, bytes; std::string note; };
+  // HM_PROF_LOG=<file>: one line per profiled launch group (class, ms, note)
+  std::string note;            // consumed by the next prof_end
+  FILE* plog = nullptr;
+  cudaEvent_t pbase = nullptr;   // timeline origin of the log (first profiled launch)
+  void prof_note(const std::string& s) { if (prof && plog) note = s; }
   std::vector<Pending> pend;
   std::vector<cudaEvent_t> free_events;
   double ms[PC_COUNT] = {0};
@@ -201,6 +221,10 @@ double trunc_flops(double m, double n, double l, double k);
 double trunc_bytes(double m, double n, double l, double k);
 
 void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps);
+void flush_replay(Ctx* c, int level, double eps, int reps, double* ms_out, int64_t* rank_sum);
+void eval_batched_test(Ctx* c, Mat* H, int njobs, const int* blk, const int* trans, const double* coef,
+                       const double* const* V, const int* ldv, double* const* out, const int* ldo, const int* w,
+                       double split_thr);
 void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_pivot);
 Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int kernel,
                   int leaf_size, double eta, double eps, int64_t* perm_out);

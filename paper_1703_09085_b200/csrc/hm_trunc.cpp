@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "hm_internal.h"
 
@@ -75,6 +76,13 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
     fl += trunc_flops(r.m, r.n, r.l, 0.0);   // convention flops (reform term k unknown here)
     by += trunc_bytes(r.m, r.n, r.l, 0.0);
   }
+  if (c->plog) {
+    int mx = 0, ml = 0, nf = 0;
+    for (int b = 0; b < 3; b++)
+      for (auto& j : fb[b]) { mx = std::max(mx, std::max(j.m, j.n)); ml = std::max(ml, j.l); nf++; }
+    c->prof_note("fused jobs " + std::to_string(nf) + " maxmn " + std::to_string(mx) + " maxl " + std::to_string(ml) +
+                 " staged " + std::to_string(rest.size()));
+  }
   {
     ProfScope ps(c, PC_FUSED, fl, by);
     for (int b = 0; b < 3; b++)
@@ -88,6 +96,12 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   if (reqs.empty()) return;
   cudaStream_t st = c->stream;
   const int nj = (int)reqs.size();
+  std::string shapes;
+  if (c->plog) {
+    for (int i = 0; i < nj && i < 6; i++)
+      shapes += " " + std::to_string(reqs[i].m) + "x" + std::to_string(reqs[i].n) + "x" + std::to_string(reqs[i].l);
+    shapes = "jobs " + std::to_string(nj) + shapes;
+  }
   std::vector<int> p(nj), q(nj);
   std::vector<char> qa(nj), qb(nj);
   size_t tau_total = 0, m_total = 0;
@@ -226,6 +240,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     tiles += (int64_t)((rows + 31) / 32) * ((cols + 31) / 32);
     v.push_back(j);
   };
+  c->prof_note(shapes);
   {
     ProfScope ps(c, PC_QR, fl_qr, 0);
     launch_qr_set(qjobs);
@@ -290,6 +305,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     fl_m += 2.0 * p[i] * q[i] * r.l;
     gj.push_back(g);
   }
+  c->prof_note(shapes);
   {
     ProfScope ps(c, PC_GEMM_M, fl_m, 0);
     launch_gemm_mapped(ar.upload(gj), (int)gj.size(), ar.tile_map(gj, tiles), tiles, st);
@@ -365,6 +381,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     if (b == 3) s.work = ar.alloc((size_t)need);
     sj[b].push_back(s);
   }
+  c->prof_note(shapes);
   {
     ProfScope ps(c, PC_SVD, fl_svd, 0);
     for (int b = 0; b < 4; b++) {
@@ -414,6 +431,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       }
     }
   }
+  c->prof_note(shapes);
   {
     ProfScope ps(c, PC_APPLYQ, 0, 0);
     auto cmax = [](const std::vector<ApplyQJob>& v) {

@@ -127,6 +127,9 @@ struct EvalJob {
   // spread over several CTAs without atomics.
   int nrng;
   const int2* rng;
+  // chain (identity pre-summing): after this job the same CTA runs *next, which
+  // accumulates into the same output columns (sequential: no atomics)
+  const EvalJob* next;
 };
 
 // Triangular solve through the H-structure on a thin panel (one CTA per job).

@@ -44,7 +44,16 @@ def main(path, out):
         res[k] = {"launches": a["launches"], "ms": round(a["ms"], 3), "share": round(a["ms"] / tot, 4),
                   "dram_bytes_per_launch": a["dram_bytes"] / a["launches"],
                   "dram_gbs": a["dram_bytes"] / (a["ms"] * 1e-3) / 1e9 if a["ms"] else None}
-    json.dump({"source": path, "total_ms": tot, "kernels": res}, open(out, "w"), indent=1)
+    # aggregated by kernel FUNCTION (template instantiations / buckets merged)
+    fun = collections.defaultdict(lambda: {"launches": 0, "ms": 0.0, "dram_bytes": 0.0})
+    for k, a in agg.items():
+        f = fun[k.split("<")[0].strip()]
+        for key in ("launches", "ms", "dram_bytes"):
+            f[key] += a[key]
+    fres = {k: {"launches": a["launches"], "ms": round(a["ms"], 3), "share": round(a["ms"] / tot, 4),
+                "dram_bytes_per_launch": a["dram_bytes"] / a["launches"], "dram_bytes": a["dram_bytes"]}
+            for k, a in sorted(fun.items(), key=lambda kv: -kv[1]["ms"])}
+    json.dump({"source": path, "total_ms": tot, "kernels": res, "functions": fres}, open(out, "w"), indent=1)
     for k, a in res.items():
         print(f"{k:20s} {a['launches']:5d} {a['ms']:10.1f} ms {100 * a['share']:5.1f}%  "
               f"{a['dram_bytes_per_launch'] / 1e6:10.1f} MB/launch  {a['dram_gbs'] or 0:8.0f} GB/s")

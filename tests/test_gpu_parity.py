@@ -221,3 +221,77 @@ def test_matvec(hm, ctx):
         yg = torch.from_numpy(Y0.T.copy()).cuda().T
         hm.matvec(Gg, xg, yg, alpha=2.0, beta=0.5, op=op)
         np.testing.assert_allclose(yg.cpu().numpy(), ref, atol=1e-13 * np.abs(ref).max())
+
+
+def test_eval_batched_kernel(hm, ctx):
+    """hm_test_eval_batched (Fig. 1 addeval / addevaltrans) vs the
+    oracle's recursive addeval / addevaltrans on the same H-matrix, for blocks
+    of every kind (subdivided, admissible, dense), both orientations, ragged
+    widths, with and without the row-group split of large jobs: the sums run
+    over the same leaves, so the results agree to rounding (1e-13)."""
+    from oracle.hmatrix import addeval, addevaltrans
+    x, w = random_points(700, 9)
+    P = Problem(x, w, 16, 2.0)
+    G = build(P, 1e-6)
+    Gg = ctx.import_desc(export(G))
+    rng = np.random.default_rng(4)
+    blocks = [P.bt.root] + [b for b in P.bt.blocks if b.kind == 0][1:6] + \
+        [b for b in P.bt.blocks if b.kind == 1][:4] + [b for b in P.bt.blocks if b.kind == 2][:4]
+    jobs, refs = [], []
+    for i, b in enumerate(blocks):
+        for trans in (0, 1):
+            wdt = int(rng.integers(1, 40))
+            coef = float(rng.uniform(-2, 2))
+            rows_in = b.t.size if trans else b.s.size
+            V = rng.standard_normal((rows_in, wdt))
+            ref = np.zeros((b.s.size if trans else b.t.size, wdt))
+            (addevaltrans if trans else addeval)(G, b, coef, V, ref)
+            jobs.append((b.id, trans, coef, V))
+            refs.append(ref)
+    for thr in (0.0, 1e3):   # production rule / force the row-group split
+        outs = hm.test_eval_batched(Gg, jobs, split_threshold=thr)
+        for (bid, trans, _, _), o, ref in zip(jobs, outs, refs):
+            assert np.linalg.norm(o - ref) <= 1e-13 * max(np.linalg.norm(ref), 1e-300), (bid, trans, thr)
+
+
+@pytest.mark.parametrize("presum", ["1", "0"])
+def test_addmul_identity_presum_parity(hm, ctx, presum, monkeypatch):
+    """Identity pre-summing (reading R7d) on / off: same truncation count, the
+    same ranks and <= 1e-9 per-block agreement with the oracle either way
+    (the truncated exact matrices are identical)."""
+    monkeypatch.setenv("HM_NO_PRESUM", "0" if presum == "1" else "1")
+    P, G = _cfg(3, 16, 1e-6)
+    octx = TruncCtx(1e-6)
+    Zo, octx, _ = addmul_s2(1.0, G.clone(), G.clone(), G.clone(), 1e-6, ctx=octx)
+    do = export(Zo)
+    Gg = ctx.import_desc(export(G))
+    X, Y, Z = Gg.clone(), Gg.clone(), Gg.clone()
+    hm.addmul(1.0, X, Y, Z, 1e-6)
+    assert ctx.last_stats()["truncations"] == octx.count
+    rep = compare(Z.export(), do, near_block_set(do, octx))
+    assert not rep["unexplained_mismatch"], rep
+    assert rep["worst"] <= TOL, rep
+    print(f"presum={presum}: trunc_cols {ctx.last_stats()['trunc_cols']} (oracle printed-branch {octx.cols})")
+
+
+def test_flush_capture_replay(hm, ctx):
+    """Standalone batched flush (BASELINE configs[3] timing mode):
+    every captured level's TRUNC batch replayed from its captured stacks
+    reproduces the in-situ ranks (same inputs, same kernels)."""
+    P, G = _cfg(3, 32, 1e-4)
+    Gg = ctx.import_desc(export(G))
+    X, Y, Z = Gg.clone(), Gg.clone(), Gg.clone()
+    hm.flush_capture(ctx, (1 << 63) - 1)
+    hm.addmul(1.0, X, Y, Z, 1e-4)
+    info = hm.flush_capture_info(ctx)
+    assert len(info) >= 3
+    ntr = 0
+    for lev, L in enumerate(info):
+        assert L["has_data"]
+        ms, rs = hm.flush_replay(ctx, lev, 1e-4, reps=2)
+        assert rs == int(L["k"].sum()), (lev, rs, int(L["k"].sum()))
+        assert ms > 0
+        ntr += len(L["m"])
+    # level batches hold every truncation except the rkmerge ones (T4)
+    assert 0 < ntr <= ctx.last_stats()["truncations"]
+    hm.flush_capture_free(ctx)
