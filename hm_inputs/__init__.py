@@ -12,6 +12,6 @@ Workload recipe (BASELINE.json configs):
 The paper (§7) uses a refined double pyramid; the
 icosahedron is BASELINE.json's stand-in.
 """
-from .mesh import icosphere, sphere_points, probe_vectors, random_points
+from .mesh import icosphere, sphere_normals, sphere_points, probe_vectors, random_points
 
-__all__ = ["icosphere", "sphere_points", "probe_vectors", "random_points"]
+__all__ = ["icosphere", "sphere_normals", "sphere_points", "probe_vectors", "random_points"]

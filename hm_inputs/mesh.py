@@ -79,6 +79,19 @@ def sphere_points(level: int):
     return np.ascontiguousarray(x), np.ascontiguousarray(area)
 
 
+def sphere_normals(level: int):
+    """Unit normals (n,3) of the flat triangles, oriented outward
+    (n . centroid > 0) -- geometry of the double-layer matrix K (PAPER.md
+    P:L1583-1585)."""
+    v, f = icosphere(level)
+    p0, p1, p2 = v[f[:, 0]], v[f[:, 1]], v[f[:, 2]]
+    cr = np.cross(p1 - p0, p2 - p0)
+    nrm = cr / np.sqrt(cr[:, 0] * cr[:, 0] + cr[:, 1] * cr[:, 1] + cr[:, 2] * cr[:, 2])[:, None]
+    x = (p0 + p1 + p2) / 3.0
+    sgn = np.where(np.sum(nrm * x, axis=1) < 0.0, -1.0, 1.0)
+    return np.ascontiguousarray(nrm * sgn[:, None])
+
+
 def random_points(n: int, seed: int):
     """Seeded random points on the unit sphere with random positive weights
     (small structural test inputs: ragged trees, odd n)."""

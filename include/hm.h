@@ -59,7 +59,8 @@ typedef enum {
   HM_EUNSUPPORTED = -6   /* operation not available in this build */
 } hm_status;
 
-enum { HM_KERNEL_SLP = 0, HM_KERNEL_SLP_SYM = 1 };   /* G, (G + G^T)/2 */
+/* G (single layer), (G + G^T)/2, K + I/2 (double layer) */
+enum { HM_KERNEL_SLP = 0, HM_KERNEL_SLP_SYM = 1, HM_KERNEL_DLP = 2 };
 /* hm_matvec_thin operators: G, G^T, and (after hm_lr / hm_chol, in place)
  * the unit lower factor L, the upper factor R, the Cholesky factor L and L^T. */
 enum { HM_OP_G = 0, HM_OP_GT = 1, HM_OP_L = 2, HM_OP_R = 3, HM_OP_LC = 4, HM_OP_LCT = 5 };
@@ -172,6 +173,14 @@ const char* hm_version(void);
 hm_status hm_build(hm_ctx ctx, const double* pts_host, const double* area_host, int64_t n,
                    int kernel, int leaf_size, double eta, double eps,
                    hm_mat* out, int64_t* perm_host);
+/* hm_build_nrm: as hm_build with unit normals nrm_host (n x 3 row-major,
+ * outward, host, read during the call; NULL allowed except for
+ * HM_KERNEL_DLP): K_ij = area_j ((x_j - x_i) . n_j) / (4 pi |x_i - x_j|^3),
+ * K_ii = 1/2 -- the double-layer matrix plus 1/2 I of PAPER.md P:L1583-1585
+ * (sign: DESIGN.md reading R20, K 1 ~ 1/2 on a closed surface). */
+hm_status hm_build_nrm(hm_ctx ctx, const double* pts_host, const double* area_host, const double* nrm_host,
+                       int64_t n, int kernel, int leaf_size, double eta, double eps, hm_mat* out,
+                       int64_t* perm_host);
 
 /* hm_import: upload a flat host description (trees + payloads). */
 hm_status hm_import(hm_ctx ctx, const hm_host_desc* d, hm_mat* out);
@@ -203,10 +212,46 @@ hm_status hm_free(hm_ctx ctx, hm_mat m);
  */
 hm_status hm_addmul(hm_ctx ctx, double alpha, hm_mat X, hm_mat Y, hm_mat Z, double eps);
 
+/*
+ * hm_addmul_std: the STANDARD (immediate-update) product Z <- Z + alpha X Y of
+ * PAPER.md §4 -- the paper's baseline the accumulated product
+ * is compared against (Fig. 9): every evaluated elementary
+ * product is truncated into each admissible Z leaf below its block at once
+ * (rkupdate, Fig. 3), temporaries + rkmerge below admissible leaves
+ * (P:L871-875).  Same arguments, trees and errors as hm_addmul; the result
+ * differs from hm_addmul's by truncation error only (same exact product).
+ * hm_stats reports its truncation count (the paper's point: S0 truncates far
+ * more often) and `levels` = number of dependent TRUNC rounds.
+ */
+hm_status hm_addmul_std(hm_ctx ctx, double alpha, hm_mat X, hm_mat Y, hm_mat Z, double eps);
+
 /* H-LR (unit lower L, upper R, in place) and H-Cholesky (lower L, in place,
  * G + shift*I factored) with accumulated updates. */
 hm_status hm_lr(hm_ctx ctx, hm_mat G, double eps);
 hm_status hm_chol(hm_ctx ctx, hm_mat G, double eps, double shift);
+
+/*
+ * hm_solve_thin: X <- op(F)^{-1} X in place, F = an hm_lr / hm_chol result,
+ * X: n x ncols device panel in tree order (ld ldx >= n).  op:
+ *   HM_SOLVE_L (unit lower L), HM_SOLVE_R (upper R), HM_SOLVE_LT (L^T),
+ *   HM_SOLVE_RT (R^T), HM_SOLVE_LC (Cholesky L), HM_SOLVE_LCT (L^T).
+ * Block substitution through the cluster tree (dense leaf substitutions +
+ * Fig. 1 addeval updates); (L R)^{-1} x = two calls (L then R).  The
+ * preconditioner of PAPER.md P:L1628-1629.  Synchronizes.
+ */
+enum { HM_SOLVE_L = 0, HM_SOLVE_R = 1, HM_SOLVE_LT = 2, HM_SOLVE_RT = 3, HM_SOLVE_LC = 4, HM_SOLVE_LCT = 5 };
+hm_status hm_solve_thin(hm_ctx ctx, hm_mat F, int op, double* x_dev, int64_t ldx, int ncols);
+
+/*
+ * hm_precond_error: the paper's preconditioner error ||I - F^{-1} G||_2
+ * ("estimate the spectral norm ... using a power iteration"),
+ * F = L R (kind 0, after hm_lr) or L L^T (kind 1, after hm_chol), G the
+ * unfactored matrix (e.g. an hm_clone taken before factorizing): `iters`
+ * power steps on E^T E from a seeded Gaussian start (device generator,
+ * `seed`); *out = ||E v|| of the last step (a lower bound converging to
+ * ||E||_2).  All vector work on the device; synchronizes.
+ */
+hm_status hm_precond_error(hm_ctx ctx, hm_mat G, hm_mat F, int kind, int iters, uint64_t seed, double* out);
 
 /*
  * hm_matvec_thin: Y <- alpha op(G) X + beta Y (Fig. 1 addeval/addevaltrans,

@@ -307,7 +307,28 @@ def chol_with_restart(G: HMatrix, eps, ctx_factory=None):
 
 def apply_factor(F: HMatrix, part, V):
     """Y = op(F) V for part in {'L' (unit lower), 'R' (upper), 'Lc' (lower, non-unit),
-    'LcT' (transpose of Lc)} using the leaves of the in-place factorization."""
+    'LcT' (transpose of Lc), 'LT' (transpose of L), 'RT' (transpose of R)} using
+    the leaves of the in-place factorization."""
+    if part in ("LT", "RT"):
+        # op(F)^T V = (op(F)^T applied by rows): Y = (M^T) V with M = apply_factor(part[0])
+        base = part[0]
+        Y = np.zeros_like(V)
+        for b in F.bt.leaves():
+            t, s = b.t, b.s
+            rt = slice(t.start, t.start + t.size)
+            rs = slice(s.start, s.start + s.size)
+            if t is s:
+                N = F.N[b.id]
+                M = np.tril(N, -1) + np.eye(t.size) if base == "L" else np.triu(N)
+                Y[rt] += M.T @ V[rt]
+                continue
+            lower = t.start > s.start
+            if (base == "L") == lower:
+                if b.kind == DENSE:
+                    Y[rs] += F.N[b.id].T @ V[rt]
+                else:
+                    Y[rs] += F.B[b.id] @ (F.A[b.id].T @ V[rt])
+        return Y
     Y = np.zeros_like(V)
     for b in F.bt.leaves():
         t, s = b.t, b.s
@@ -353,3 +374,91 @@ def probe_residual(G0: HMatrix, F: HMatrix, probes, kind="lr", shift=0.0):
     else:
         LRv = apply_factor(F, "Lc", apply_factor(F, "LcT", probes))
     return float(np.linalg.norm(Gv - LRv) / np.linalg.norm(Gv))
+
+
+# ------------------------------------------------------------ solving with the factors
+
+def solve_factor(F: HMatrix, part, V):
+    """V <- op(F)^{-1} V (in place) by block substitution through the cluster
+    tree: the inverse of apply_factor's operators, part in
+      'L'   unit lower L (H-LR)        'R'   upper R (H-LR)
+      'LT'  L^T (unit upper)           'RT'  R^T (lower)
+      'Lc'  Cholesky factor L (lower)  'LcT' L^T (upper)
+    Forward substitution for the lower operators (solve the t1 rows, subtract
+    the (t2,t1) block's contribution with addeval / addevaltrans, solve t2),
+    backward for the upper ones; dense diagonal leaves with
+    scipy.linalg.solve_triangular.  Used for (L R)^{-1} in the preconditioner
+    error of PAPER.md P:L1628-1629 (power iteration).
+    Pinned by tests/test_oracle_factor.py against numpy.linalg.solve of the
+    dense operator apply_factor(F, part, I)."""
+    lower = part in ("L", "RT", "Lc")
+    unit = part in ("L", "LT")
+    G = F
+
+    def rec(t, W):
+        if t.leaf:
+            N = G.N[_diag(G, t).id]
+            if part in ("L", "Lc"):
+                W[:] = sla.solve_triangular(N, W, lower=True, unit_diagonal=unit)
+            elif part == "R":
+                W[:] = sla.solve_triangular(N, W, lower=False)
+            elif part == "RT":
+                W[:] = sla.solve_triangular(N, W, lower=False, trans="T")
+            else:   # LT, LcT: (lower N)^T
+                W[:] = sla.solve_triangular(N, W, lower=True, trans="T", unit_diagonal=unit)
+            return
+        t1, t2 = t.sons
+        W1, W2 = W[_rows(t, t1)], W[_rows(t, t2)]
+        if lower:
+            rec(t1, W1)
+            if part == "RT":                       # (R^T)_(t2,t1) = R_(t1,t2)^T
+                addevaltrans(G, G.bt.find(t1, t2), -1.0, W1, W2)
+            else:                                  # L_(t2,t1)
+                addeval(G, G.bt.find(t2, t1), -1.0, W1, W2)
+            rec(t2, W2)
+        else:
+            rec(t2, W2)
+            if part == "R":                        # R_(t1,t2)
+                addeval(G, G.bt.find(t1, t2), -1.0, W2, W1)
+            else:                                  # (L^T)_(t1,t2) = L_(t2,t1)^T
+                addevaltrans(G, G.bt.find(t2, t1), -1.0, W2, W1)
+            rec(t1, W1)
+
+    rec(G.bt.root.t, V)
+    return V
+
+
+def precond_error(G0: HMatrix, F: HMatrix, kind="lr", iters=30, seed=0, v0=None):
+    """Spectral norm estimate of E = I - (F)^{-1} G0 (the paper's
+    "preconditioner error" ||I - G~^{-1} G||_2) by power
+    iteration on E^T E: v <- E^T E v / ||.||, estimate ||E v|| (||v|| = 1).
+    F = the in-place H-LR (kind 'lr': F = L R) or H-Cholesky (kind 'chol':
+    F = L L^T of the symmetric G0).  E^T = I - G0^T F^{-T}.
+    Pinned by tests/test_oracle_factor.py against numpy.linalg.norm(E, 2)."""
+    from .hmatrix import matvec
+    n = G0.n
+    v = np.random.default_rng([1703, 9085, 5, seed]).standard_normal(n) if v0 is None else np.array(v0, float)
+    v = v / np.linalg.norm(v)
+    est = 0.0
+    for _ in range(iters):
+        gv = np.zeros(n)
+        matvec(G0, 1.0, v, gv)
+        if kind == "lr":
+            solve_factor(F, "R", solve_factor(F, "L", gv))
+        else:
+            solve_factor(F, "LcT", solve_factor(F, "Lc", gv))
+        w = v - gv
+        est = float(np.linalg.norm(w))
+        y = w.copy()
+        if kind == "lr":                           # F^{-T} = L^{-T} R^{-T}
+            solve_factor(F, "LT", solve_factor(F, "RT", y))
+        else:
+            solve_factor(F, "LcT", solve_factor(F, "Lc", y))
+        z = np.zeros(n)
+        matvec(G0, 1.0, y, z, trans=True)
+        u = w - z
+        nu = np.linalg.norm(u)
+        if nu == 0.0:
+            return 0.0
+        v = u / nu
+    return est

@@ -92,9 +92,10 @@ class HMatrix:
 class Problem:
     """Trees + geometry of one configuration (no matrix data)."""
 
-    def __init__(self, x, w, leaf_size, eta, kernel=K.KERNEL_SLP):
+    def __init__(self, x, w, leaf_size, eta, kernel=K.KERNEL_SLP, nrm=None):
         self.x = np.asarray(x, np.float64)
         self.w = np.asarray(w, np.float64)
+        self.nrm = None if nrm is None else np.asarray(nrm, np.float64)
         self.kernel = kernel
         self.ct = build_cluster_tree(self.x, leaf_size)
         self.bt = build_block_tree(self.ct, self.ct, eta)
@@ -108,10 +109,10 @@ class Problem:
     def block_entries(self, b):
         p = self.ct.perm
         return K.entries(self.x, self.w, p[b.t.start:b.t.start + b.t.size],
-                         p[b.s.start:b.s.start + b.s.size], self.kernel)
+                         p[b.s.start:b.s.start + b.s.size], self.kernel, self.nrm)
 
     def dense(self):
-        return K.dense_matrix(self.x, self.w, self.ct.perm, self.kernel)
+        return K.dense_matrix(self.x, self.w, self.ct.perm, self.kernel, self.nrm)
 
     def arrays(self):
         return tree_arrays(self.ct, self.bt)

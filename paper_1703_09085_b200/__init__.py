@@ -76,14 +76,17 @@ class Context:
         self.check(lib().hm_sync(self.h))
 
     # ---- construction
-    def build(self, points, areas, leaf_size, eta, eps, kernel=0):
+    def build(self, points, areas, leaf_size, eta, eps, kernel=0, normals=None):
+        """kernel 0: single layer G, 1: (G+G^T)/2, 2: double layer K + I/2 (needs normals)."""
         pts = np.ascontiguousarray(points, dtype=np.float64)
         ar = np.ascontiguousarray(areas, dtype=np.float64)
+        nr = None if normals is None else np.ascontiguousarray(normals, dtype=np.float64)
         n = len(ar)
         perm = np.empty(n, np.int64)
         h = C.c_void_p()
-        self.check(lib().hm_build(self.h, _ptr(pts, C.c_double), _ptr(ar, C.c_double), n, int(kernel),
-                                  int(leaf_size), float(eta), float(eps), C.byref(h), _ptr(perm, C.c_int64)))
+        self.check(lib().hm_build_nrm(self.h, _ptr(pts, C.c_double), _ptr(ar, C.c_double),
+                                      _ptr(nr, C.c_double) if nr is not None else None, n, int(kernel),
+                                      int(leaf_size), float(eta), float(eps), C.byref(h), _ptr(perm, C.c_int64)))
         m = HMatrix(self, h)
         m.perm = perm
         return m
@@ -220,6 +223,11 @@ def addmul(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps):
     Z.ctx.check(lib().hm_addmul(Z.ctx.h, float(alpha), X.h, Y.h, Z.h, float(eps)))
 
 
+def addmul_std(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps):
+    """Standard immediate-update product (hm_addmul_std)."""
+    Z.ctx.check(lib().hm_addmul_std(Z.ctx.h, float(alpha), X.h, Y.h, Z.h, float(eps)))
+
+
 def lr(G: HMatrix, eps):
     """In-place H-LR with accumulated updates (hm_lr): strict lower part = L
     (unit diagonal), upper part = R."""
@@ -246,6 +254,29 @@ def matvec(G: HMatrix, x, y, alpha=1.0, beta=0.0, op=0):
         ldx = ldy = n
     G.ctx.check(lib().hm_matvec_thin(G.ctx.h, G.h, int(op), float(alpha), C.c_void_p(x.data_ptr()), ldx,
                                      float(beta), C.c_void_p(y.data_ptr()), ldy, ncols))
+
+
+SOLVE_OPS = {"L": 0, "R": 1, "LT": 2, "RT": 3, "Lc": 4, "LcT": 5}
+
+
+def solve(F: HMatrix, x, op):
+    """x <- op(F)^{-1} x in place (hm_solve_thin); x: torch CUDA float64 n x c
+    column-major (or 1-D); op in 'L', 'R', 'LT', 'RT', 'Lc', 'LcT'."""
+    import torch
+    assert x.is_cuda and x.dtype == torch.float64
+    ncols = 1 if x.dim() == 1 else x.shape[1]
+    ldx = x.shape[0] if x.dim() == 1 else x.stride(1)
+    if x.dim() == 2:
+        assert x.stride(0) == 1, "panels must be column-major (stride(0) == 1)"
+    F.ctx.check(lib().hm_solve_thin(F.ctx.h, F.h, SOLVE_OPS[op], C.c_void_p(x.data_ptr()), ldx, ncols))
+
+
+def precond_error(G: HMatrix, F: HMatrix, kind="lr", iters=30, seed=1703):
+    """||I - F^{-1} G||_2 by power iteration (hm_precond_error)."""
+    out = C.c_double()
+    G.ctx.check(lib().hm_precond_error(G.ctx.h, G.h, F.h, 0 if kind == "lr" else 1, int(iters),
+                                       C.c_uint64(int(seed)), C.byref(out)))
+    return out.value
 
 
 def test_trunc_batched(ctx: Context, stacks, eps, timed=False):
@@ -392,5 +423,5 @@ def flush_capture_free(ctx: Context):
     ctx.check(lib().hm_flush_capture_free(ctx.h))
 
 
-__all__ = ["Context", "HMatrix", "HMError", "addmul", "chol", "lr", "matvec", "lib", "test_trunc_batched",
+__all__ = ["Context", "HMatrix", "HMError", "addmul", "addmul_std", "solve", "precond_error", "chol", "lr", "matvec", "lib", "test_trunc_batched",
            "test_eval_batched", "flush_capture", "flush_capture_info", "flush_replay", "flush_capture_free"]

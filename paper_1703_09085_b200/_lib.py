@@ -63,9 +63,10 @@ class Prof(C.Structure):
 
 
 EXPORTS = [
-    "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_build",
-    "hm_import", "hm_export", "hm_export_sizes", "hm_export_into", "hm_clone", "hm_free", "hm_addmul", "hm_lr", "hm_chol",
-    "hm_matvec_thin", "hm_stats", "hm_profile_enable", "hm_profile_reset", "hm_profile_get",
+    "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_build", "hm_build_nrm",
+    "hm_import", "hm_export", "hm_export_sizes", "hm_export_into", "hm_clone", "hm_free", "hm_addmul", "hm_addmul_std",
+    "hm_lr", "hm_chol",
+    "hm_matvec_thin", "hm_solve_thin", "hm_precond_error", "hm_stats", "hm_profile_enable", "hm_profile_reset", "hm_profile_get",
     "hm_test_trunc_batched", "hm_test_eval_batched",
     "hm_flush_capture", "hm_flush_capture_info", "hm_flush_replay", "hm_flush_capture_free",
 ]
@@ -86,6 +87,8 @@ def load(path: str = LIB_PATH):
         "hm_sync": (C.c_int, [vp]),
         "hm_build": (C.c_int, [vp, P_f64, P_f64, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,
                                C.POINTER(vp), P_i64]),
+        "hm_build_nrm": (C.c_int, [vp, P_f64, P_f64, P_f64, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,
+                                   C.POINTER(vp), P_i64]),
         "hm_import": (C.c_int, [vp, C.POINTER(HostDesc), C.POINTER(vp)]),
         "hm_export": (C.c_int, [vp, vp, C.POINTER(HostDesc)]),
         "hm_export_sizes": (C.c_int, [vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -93,10 +96,13 @@ def load(path: str = LIB_PATH):
         "hm_clone": (C.c_int, [vp, vp, C.POINTER(vp)]),
         "hm_free": (C.c_int, [vp, vp]),
         "hm_addmul": (C.c_int, [vp, C.c_double, vp, vp, vp, C.c_double]),
+        "hm_addmul_std": (C.c_int, [vp, C.c_double, vp, vp, vp, C.c_double]),
         "hm_lr": (C.c_int, [vp, vp, C.c_double]),
         "hm_chol": (C.c_int, [vp, vp, C.c_double, C.c_double]),
         "hm_matvec_thin": (C.c_int, [vp, vp, C.c_int, C.c_double, vp, C.c_int64, C.c_double, vp,
                                      C.c_int64, C.c_int]),
+        "hm_solve_thin": (C.c_int, [vp, vp, C.c_int, vp, C.c_int64, C.c_int]),
+        "hm_precond_error": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_uint64, P_f64]),
         "hm_stats": (C.c_int, [vp, vp, C.POINTER(Stats)]),
         "hm_profile_enable": (C.c_int, [vp, C.c_int]),
         "hm_profile_reset": (C.c_int, [vp]),

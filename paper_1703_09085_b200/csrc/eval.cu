@@ -493,13 +493,19 @@ __global__ void __launch_bounds__(kNT) k_trsm2(const TrsmJob* __restrict__ jobs,
       // leaf clusters larger than 64 rows (leaf size > 64): plain substitution
       // in global memory, one thread per column
       double* v = J.V + S.r0;
+      const int mm = S.m;
+      // reversed (upper) steps: row i of the forward sweep is row mm-1-i of T / the panel
+      auto tr_at = [&](int i, int p) {
+        const int a = S.rev ? mm - 1 - i : i, b = S.rev ? mm - 1 - p : p;
+        return S.trans ? S.P[b + (int64_t)a * S.ld] : S.P[a + (int64_t)b * S.ld];
+      };
       for (int col = tid; col < J.ncols; col += kNT) {
         double* x = v + (int64_t)col * J.ldv;
-        for (int i = 0; i < S.m; i++) {
-          double acc = x[i];
-          for (int p = 0; p < i; p++)
-            acc = fma(-(S.trans ? S.P[p + (int64_t)i * S.ld] : S.P[i + (int64_t)p * S.ld]), x[p], acc);
-          x[i] = S.unit ? acc : acc / S.P[i + (int64_t)i * S.ld];
+        for (int i = 0; i < mm; i++) {
+          const int xi = S.rev ? mm - 1 - i : i;
+          double acc = x[xi];
+          for (int p = 0; p < i; p++) acc = fma(-tr_at(i, p), x[S.rev ? mm - 1 - p : p], acc);
+          x[xi] = S.unit ? acc : acc / tr_at(i, i);
         }
       }
       __syncthreads();
@@ -511,7 +517,8 @@ __global__ void __launch_bounds__(kNT) k_trsm2(const TrsmJob* __restrict__ jobs,
       double* v = J.V + S.r0;
       for (int e = tid; e < m * m; e += kNT) {
         const int i = e % m, j = e / m;
-        tri[i + j * kLdS] = S.trans ? S.P[j + (int64_t)i * S.ld] : S.P[i + (int64_t)j * S.ld];
+        const int a = S.rev ? m - 1 - i : i, b = S.rev ? m - 1 - j : j;
+        tri[i + j * kLdS] = S.trans ? S.P[b + (int64_t)a * S.ld] : S.P[a + (int64_t)b * S.ld];
       }
       __syncthreads();
       for (int i = tid; i < m; i += kNT) dinv[i] = S.unit ? 1.0 : 1.0 / tri[i + i * kLdS];
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(kNT) k_trsm2(const TrsmJob* __restrict__ jobs,
         const int cc = min(kTrsmCols, J.ncols - c0);
         for (int e = tid; e < m * cc; e += kNT) {
           const int i = e % m, c = e / m;
-          xs[c * ldx + i] = v[i + (int64_t)(c0 + c) * J.ldv];
+          xs[c * ldx + i] = v[(S.rev ? m - 1 - i : i) + (int64_t)(c0 + c) * J.ldv];
         }
         __syncthreads();
         // x_p final = x_p * dinv_p; rows i > p: x_i -= T(i, p) x_p dinv_p
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(kNT) k_trsm2(const TrsmJob* __restrict__ jobs,
         }
         for (int e = tid; e < m * cc; e += kNT) {
           const int i = e % m, c = e / m;
-          v[i + (int64_t)(c0 + c) * J.ldv] = xs[c * ldx + i] * dinv[i];
+          v[(S.rev ? m - 1 - i : i) + (int64_t)(c0 + c) * J.ldv] = xs[c * ldx + i] * dinv[i];
         }
         __syncthreads();
       }

@@ -1436,6 +1436,9 @@ struct Factorizer {
   }
 };
 
+#include "hm_std.inc"
+#include "hm_solve.inc"
+
 }  // namespace
 
 // Kernel-level parity export of the batched H x thin-dense product (Fig. 1
@@ -1556,6 +1559,99 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
   s.flops_dense = F.P.fl_dense;
   s.bytes_dense = F.P.by_dense;
   F.P.persist.release();
+  HM_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void solve_thin(Ctx* c, Mat* F, int part, double* x, int64_t ldx, int ncols) {
+  if (!F || !x || ncols < 0 || ldx < F->tree->n) throw Error(HM_EINVAL, "hm_solve_thin: bad arguments");
+  if (part < 0 || part > 5) throw Error(HM_EINVAL, "hm_solve_thin: unknown operator");
+  Solver S(c, F, part);
+  S.run(x, (int)ldx, ncols);
+}
+
+// ||I - F^{-1} G0||_2 by power iteration on E^T E (oracle
+// factor.precond_error): F = L R (kind 0) or L L^T (kind 1) in place.
+double precond_error(Ctx* c, Mat* G0, Mat* F, int kind, int iters, uint64_t seed) {
+  if (!G0 || !F || iters <= 0) throw Error(HM_EINVAL, "hm_precond_error: bad arguments");
+  if (!G0->tree->same_structure(*F->tree)) throw Error(HM_ESTRUCT, "hm_precond_error: G and F trees differ");
+  const int64_t n = F->tree->n;
+  cudaStream_t st = c->stream;
+  Arena ar(c);
+  double* v = ar.alloc(n);
+  double* y = ar.alloc(n);
+  double* w = ar.alloc(n);
+  double* d_nrm = ar.alloc(8);
+  const NormJob* dj_v = ar.upload(std::vector<NormJob>{NormJob{v, (int)n, 1, (int)n, nullptr}});
+  const NormJob* dj_w = ar.upload(std::vector<NormJob>{NormJob{w, (int)n, 1, (int)n, nullptr}});
+  auto norm = [&](const NormJob* j) {
+    launch_norm(j, 1, d_nrm, st);
+    double h = 0;
+    HM_CUDA(cudaMemcpyAsync(&h, d_nrm, sizeof(double), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaStreamSynchronize(st));
+    return std::sqrt(h);
+  };
+  std::unique_ptr<Solver> s1(new Solver(c, F, kind == 0 ? 0 : 4)), s2(new Solver(c, F, kind == 0 ? 1 : 5));
+  std::unique_ptr<Solver> t1, t2;
+  if (kind == 0) {   // F^{-T} = L^{-T} R^{-T}
+    t1.reset(new Solver(c, F, 3));
+    t2.reset(new Solver(c, F, 2));
+  }
+  launch_randn(v, n, seed, st);
+  double nv = norm(dj_v);
+  launch_axpby(0.0, v, n, 1.0 / nv, v, n, n, 1, st);
+  double est = 0;
+  for (int it = 0; it < iters; it++) {
+    matvec(c, G0, HM_OP_G, 1.0, v, n, 0.0, y, n, 1);            // y = G v
+    s1->rec(F->tree->bl_row[0], y, (int)n, 1);                    // y = F^{-1} G v
+    s2->rec(F->tree->bl_row[0], y, (int)n, 1);
+    launch_axpby(1.0, v, n, 0.0, w, n, n, 1, st);                  // w = v - y = E v
+    launch_axpby(-1.0, y, n, 1.0, w, n, n, 1, st);
+    est = norm(dj_w);
+    if (est == 0.0) break;
+    launch_axpby(1.0, w, n, 0.0, y, n, n, 1, st);                  // y = F^{-T} w
+    if (kind == 0) {
+      t1->rec(F->tree->bl_row[0], y, (int)n, 1);
+      t2->rec(F->tree->bl_row[0], y, (int)n, 1);
+    } else {
+      s1->rec(F->tree->bl_row[0], y, (int)n, 1);
+      s2->rec(F->tree->bl_row[0], y, (int)n, 1);
+    }
+    matvec(c, G0, HM_OP_GT, 1.0, y, n, 0.0, v, n, 1);             // v = G^T F^{-T} w
+    launch_axpby(1.0, w, n, -1.0, v, n, n, 1, st);                 // v = w - v = E^T E v_old
+    nv = norm(dj_v);
+    if (nv == 0.0) break;
+    launch_axpby(0.0, v, n, 1.0 / nv, v, n, n, 1, st);
+  }
+  HM_CUDA(cudaStreamSynchronize(st));
+  return est;
+}
+
+void addmul_std(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps) {
+  if (!X || !Y || !Z) throw Error(HM_EINVAL, "hm_addmul_std: null matrix");
+  if (Z == X || Z == Y) throw Error(HM_ESTRUCT, "hm_addmul_std: Z aliases X or Y (use hm_clone)");
+  if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_addmul_std: eps must be >= 0");
+  const Tree& T = *Z->tree;
+  if (!(X->tree->same_structure(T) && Y->tree->same_structure(T)))
+    throw Error(HM_ESTRUCT, "hm_addmul_std: X, Y and Z must share one block tree");
+  c->sp_prepare();
+  StdExec S(c, X, Y, Z, alpha, eps);
+  S.run(Z);
+  hm_stats_t& s = c->last;
+  s = hm_stats_t{};
+  s.addproduct_calls = S.n_addproduct;
+  s.evaluated_terms = (int64_t)S.terms.size();
+  s.truncations = S.P.n_trunc;
+  s.trunc_cols = S.P.n_cols;
+  s.merges = S.n_m;
+  s.dense_adds = S.P.n_dense;
+  s.levels = S.rounds;
+  s.flops_trunc = S.P.fl_trunc;
+  s.bytes_trunc = S.P.by_trunc;
+  s.flops_eval = S.P.fl_eval;
+  s.bytes_eval = S.P.by_eval;
+  s.flops_dense = S.P.fl_dense;
+  s.bytes_dense = S.P.by_dense;
+  S.P.persist.release();
   HM_CUDA(cudaStreamSynchronize(c->stream));
 }
 

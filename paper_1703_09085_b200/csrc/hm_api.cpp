@@ -407,18 +407,48 @@ hm_status hm_addmul(hm_ctx ctx, double alpha, hm_mat X, hm_mat Y, hm_mat Z, doub
 
 hm_status hm_build(hm_ctx ctx, const double* pts_host, const double* area_host, int64_t n, int kernel,
                    int leaf_size, double eta, double eps, hm_mat* out, int64_t* perm_host) {
+  return hm_build_nrm(ctx, pts_host, area_host, nullptr, n, kernel, leaf_size, eta, eps, out, perm_host);
+}
+
+hm_status hm_build_nrm(hm_ctx ctx, const double* pts_host, const double* area_host, const double* nrm_host,
+                       int64_t n, int kernel, int leaf_size, double eta, double eps, hm_mat* out,
+                       int64_t* perm_host) {
   if (!ctx || !pts_host || !area_host || !out) return HM_EINVAL;
   return guard(ctx, [&] {
     set_device(ctx->c);
-    if (kernel != HM_KERNEL_SLP && kernel != HM_KERNEL_SLP_SYM)
+    if (kernel != HM_KERNEL_SLP && kernel != HM_KERNEL_SLP_SYM && kernel != HM_KERNEL_DLP)
       throw Error(HM_EINVAL, "hm_build: unknown kernel");
     if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_build: eps must be >= 0");
-    Mat* M = build_matrix(&ctx->c, pts_host, area_host, n, kernel, leaf_size, eta, eps, perm_host);
+    Mat* M = build_matrix(&ctx->c, pts_host, area_host, nrm_host, n, kernel, leaf_size, eta, eps, perm_host);
     auto* H = new hm_mat_s;
     H->m = std::move(*M);
     delete M;
     ctx->c.live.insert(H);
     *out = H;
+  });
+}
+
+hm_status hm_addmul_std(hm_ctx ctx, double alpha, hm_mat X, hm_mat Y, hm_mat Z, double eps) {
+  if (!ctx || !X || !Y || !Z) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    addmul_std(&ctx->c, alpha, &X->m, &Y->m, &Z->m, eps);
+  });
+}
+
+hm_status hm_solve_thin(hm_ctx ctx, hm_mat F, int op, double* x_dev, int64_t ldx, int ncols) {
+  if (!ctx || !F) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    solve_thin(&ctx->c, &F->m, op, x_dev, ldx, ncols);
+  });
+}
+
+hm_status hm_precond_error(hm_ctx ctx, hm_mat G, hm_mat F, int kind, int iters, uint64_t seed, double* out) {
+  if (!ctx || !G || !F || !out || (kind != 0 && kind != 1)) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    *out = precond_error(&ctx->c, &G->m, &F->m, kind, iters, seed);
   });
 }
 

@@ -42,8 +42,9 @@ void push_gemm(std::vector<GemmJob>& v, int64_t& tiles, const double* A, int lda
 
 }  // namespace
 
-Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int kernel, int leaf_size,
-                  double eta, double eps, int64_t* perm_out) {
+Mat* build_matrix(Ctx* c, const double* pts, const double* area, const double* nrm, int64_t n, int kernel,
+                  int leaf_size, double eta, double eps, int64_t* perm_out) {
+  if (kernel == HM_KERNEL_DLP && !nrm) throw Error(HM_EINVAL, "hm_build: the double-layer kernel needs normals");
   std::shared_ptr<Tree> T = build_trees(pts, n, leaf_size, eta);
   if (perm_out) std::copy(T->perm.begin(), T->perm.end(), perm_out);
   cudaStream_t st = c->stream;
@@ -53,6 +54,11 @@ Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int 
   int64_t* dperm = static_cast<int64_t*>(geo.alloc_bytes(sizeof(int64_t) * n));
   HM_CUDA(cudaMemcpyAsync(dx, pts, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
   HM_CUDA(cudaMemcpyAsync(dw, area, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  double* dn = nullptr;
+  if (nrm) {
+    dn = geo.alloc(3 * (size_t)n);
+    HM_CUDA(cudaMemcpyAsync(dn, nrm, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+  }
   HM_CUDA(cudaMemcpyAsync(dperm, T->perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
 
   auto* M = new Mat;
@@ -86,7 +92,7 @@ Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int 
         off += (size_t)k.m * k.n;
       }
       ProfScope ps(c, PC_GEN, 0, 8.0 * nd);
-      launch_gen(ar.upload(gj), (int)gj.size(), tiles, dx, dw, dperm, kernel, st);
+      launch_gen(ar.upload(gj), (int)gj.size(), tiles, dx, dw, dn, dperm, kernel, st);
       HM_CHECK_LAUNCH();
       HM_CUDA(cudaStreamSynchronize(st));
     }
@@ -131,7 +137,7 @@ Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int 
           off += (size_t)chunk[i].m * chunk[i].n;
         }
         ProfScope ps(c, PC_GEN, 0, 8.0 * gtot);
-        launch_gen(ar.upload(gj), (int)gj.size(), tiles, dx, dw, dperm, kernel, st);
+        launch_gen(ar.upload(gj), (int)gj.size(), tiles, dx, dw, dn, dperm, kernel, st);
         HM_CHECK_LAUNCH();
       }
       // small blocks: TRUNC of the exact block;  large: randomized + certificate

@@ -221,12 +221,15 @@ double trunc_flops(double m, double n, double l, double k);
 double trunc_bytes(double m, double n, double l, double k);
 
 void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps);
+void addmul_std(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps);
+void solve_thin(Ctx* c, Mat* F, int part, double* x, int64_t ldx, int ncols);
+double precond_error(Ctx* c, Mat* G0, Mat* F, int kind, int iters, uint64_t seed);
 void flush_replay(Ctx* c, int level, double eps, int reps, double* ms_out, int64_t* rank_sum);
 void eval_batched_test(Ctx* c, Mat* H, int njobs, const int* blk, const int* trans, const double* coef,
                        const double* const* V, const int* ldv, double* const* out, const int* ldo, const int* w,
                        double split_thr);
 void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_pivot);
-Mat* build_matrix(Ctx* c, const double* pts, const double* area, int64_t n, int kernel,
+Mat* build_matrix(Ctx* c, const double* pts, const double* area, const double* nrm, int64_t n, int kernel,
                   int leaf_size, double eta, double eps, int64_t* perm_out);
 void matvec(Ctx* c, Mat* G, int op, double alpha, const double* x, int64_t ldx, double beta,
             double* y, int64_t ldy, int ncols);

@@ -461,9 +461,24 @@ __device__ __forceinline__ double g_slp(const double* x, const double* w, int64_
   return __ddiv_rn(w[j], __dmul_rn(4.0 * M_PI, __dsqrt_rn(r2)));
 }
 
+// K_ij = w_j ((x_j - x_i) . n_j) / (4 pi |x_i - x_j|^3), K_ii = 1/2: the
+// double layer + 1/2 I (sign reading R20), same
+// operation order as oracle/kernel.py dlp_entries.
+__device__ __forceinline__ double g_dlp(const double* x, const double* w, const double* nr, int64_t i, int64_t j) {
+  if (i == j) return 0.5;
+  const double dx = __dsub_rn(x[3 * j], x[3 * i]);
+  const double dy = __dsub_rn(x[3 * j + 1], x[3 * i + 1]);
+  const double dz = __dsub_rn(x[3 * j + 2], x[3 * i + 2]);
+  const double dot = __dadd_rn(__dadd_rn(__dmul_rn(dx, nr[3 * j]), __dmul_rn(dy, nr[3 * j + 1])), __dmul_rn(dz, nr[3 * j + 2]));
+  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const double r = __dsqrt_rn(r2);
+  return __ddiv_rn(__dmul_rn(w[j], dot), __dmul_rn(__dmul_rn(4.0 * M_PI, r2), r));
+}
+
 __global__ void __launch_bounds__(256) k_gen(const GenJob* __restrict__ jobs, int njobs,
                                              const double* __restrict__ x,
                                              const double* __restrict__ w,
+                                             const double* __restrict__ nr,
                                              const int64_t* __restrict__ perm, int kernel) {
   const int64_t tile = blockIdx.x;
   const GenJob& J = jobs[find_job(jobs, njobs, tile)];
@@ -474,17 +489,22 @@ __global__ void __launch_bounds__(256) k_gen(const GenJob* __restrict__ jobs, in
     const int i = ti * 32 + (e & 31), j = tj * 32 + (e >> 5);
     if (i >= J.m || j >= J.n) continue;
     const int64_t oi = perm[J.r0 + i], oj = perm[J.c0 + j];
-    double v = g_slp(x, w, oi, oj);
-    if (kernel == 1) v = __dmul_rn(0.5, __dadd_rn(v, g_slp(x, w, oj, oi)));
+    double v;
+    if (kernel == 2) {
+      v = g_dlp(x, w, nr, oi, oj);
+    } else {
+      v = g_slp(x, w, oi, oj);
+      if (kernel == 1) v = __dmul_rn(0.5, __dadd_rn(v, g_slp(x, w, oj, oi)));
+    }
     J.dst[i + (int64_t)j * J.ld] = v;
   }
 }
 
 void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x, const double* w,
-                const int64_t* perm, int kernel, cudaStream_t st) {
+                const double* nrm, const int64_t* perm, int kernel, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
   count_launch();
-  k_gen<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, x, w, perm, kernel);
+  k_gen<<<(unsigned)ntiles, 256, 0, st>>>(d_jobs, njobs, x, w, nrm, perm, kernel);
 }
 
 // ------------------------------------------------------------------ norms
@@ -524,6 +544,21 @@ __global__ void k_randn(double* dst, int64_t count, uint64_t seed) {
     const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
     dst[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
   }
+}
+
+__global__ void k_axpby(double a, const double* __restrict__ x, int64_t ldx, double b, double* y, int64_t ldy,
+                        int64_t n, int ncols) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * ncols; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    y[i + j * ldy] = a * x[i + j * ldx] + b * y[i + j * ldy];
+  }
+}
+
+void launch_axpby(double a, const double* x, int64_t ldx, double b, double* y, int64_t ldy, int64_t n, int ncols,
+                  cudaStream_t st) {
+  if (n <= 0 || ncols <= 0) return;
+  count_launch();
+  k_axpby<<<592, 256, 0, st>>>(a, x, ldx, b, y, ldy, n, ncols);
 }
 
 void launch_randn(double* dst, int64_t count, uint64_t seed, cudaStream_t st) {

@@ -142,7 +142,12 @@ struct TrsmStep {
   const double* P;
   int ld, trans, unit;
   int lb, le;
+  int rev;             // kind 0: T is UPPER triangular (backward substitution, run as a forward
+                       // substitution in reversed row order)
 };
+// y = a x + b y (n x ncols panels)
+void launch_axpby(double a, const double* x, int64_t ldx, double b, double* y, int64_t ldy, int64_t n, int ncols,
+                  cudaStream_t st);
 struct TrsmJob {
   double* V;
   int ldv, ncols;
@@ -187,7 +192,7 @@ void launch_trsm2(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, con
 void launch_leaf_factor(const LeafFactorJob* d_jobs, int njobs, int chol, int* fail, double* minpiv,
                         int maxm, cudaStream_t st);
 void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x,
-                const double* w, const int64_t* perm, int kernel, cudaStream_t st);
+                const double* w, const double* nrm, const int64_t* perm, int kernel, cudaStream_t st);
 void launch_norm(const NormJob* d_jobs, int njobs, double* out, cudaStream_t st);
 void launch_randn(double* dst, int64_t count, uint64_t seed, cudaStream_t st);
 void launch_matvec_leaves(const LeafDesc* leaves, int nleaves, int trans, double alpha,

@@ -100,3 +100,79 @@ def test_chol_pivot_failure(hm, ctx):
     with pytest.raises(hm.HMError) as ei:
         hm.chol(Gg, 1e-4, shift=-10.0)   # makes the matrix indefinite
     assert "EPIVOT" in str(ei.value) and "cluster" in str(ei.value)
+
+
+@pytest.mark.parametrize("kind", ["lr", "chol"])
+def test_solve_thin(hm, ctx, kind):
+    """hm_solve_thin (block substitution with the device factors) vs
+    oracle.factor.solve_factor applied to the SAME factors (exported): the
+    same exact operator inverse, rounding-level agreement; n = 5120 so the
+    multi-launch path (clusters > 1024 rows) and the single-CTA path both run."""
+    import torch
+    from oracle.factor import solve_factor
+    L, leaf, eps = 4, 32, 1e-4
+    x, w = sphere_points(L)
+    G = build(Problem(x, w, leaf, 2.0, kernel=K.KERNEL_SLP if kind == "lr" else K.KERNEL_SLP_SYM), eps)
+    Gg = ctx.import_desc(export(G))
+    (hm.lr if kind == "lr" else hm.chol)(Gg, eps)
+    P = Problem(x, w, leaf, 2.0)
+    Fg = import_payload(P.bt, Gg.export())
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((P.ct.n, 5))
+    for op in (["L", "R", "LT", "RT"] if kind == "lr" else ["Lc", "LcT"]):
+        xg = torch.from_numpy(X.T.copy()).cuda().T
+        hm.solve(Gg, xg, op)
+        ref = solve_factor(Fg, op, X.copy())
+        got = xg.cpu().numpy()
+        assert np.linalg.norm(got - ref) <= 1e-11 * np.linalg.norm(ref), op
+
+
+@pytest.mark.parametrize("kind", ["lr", "chol"])
+def test_precond_error(hm, ctx, kind):
+    """Device power iteration (hm_precond_error) vs the exact
+    ||I - F^{-1} G||_2 of the device's own factors (dense numpy at n = 1280)."""
+    from oracle.factor import apply_factor
+    L, leaf, eps = 3, 32, 1e-4
+    x, w = sphere_points(L)
+    kern = K.KERNEL_SLP if kind == "lr" else K.KERNEL_SLP_SYM
+    G = build(Problem(x, w, leaf, 2.0, kernel=kern), eps)
+    G0 = ctx.import_desc(export(G))
+    Fd = G0.clone()
+    (hm.lr if kind == "lr" else hm.chol)(Fd, eps)
+    est = hm.precond_error(G0, Fd, kind, iters=150)
+    P = Problem(x, w, leaf, 2.0)
+    Fo = import_payload(P.bt, Fd.export())
+    n = P.ct.n
+    M = apply_factor(Fo, "L", apply_factor(Fo, "R", np.eye(n))) if kind == "lr" else \
+        apply_factor(Fo, "Lc", apply_factor(Fo, "LcT", np.eye(n)))
+    E = np.eye(n) - np.linalg.solve(M, G.to_dense())
+    exact = np.linalg.norm(E, 2)
+    assert abs(est - exact) <= 1e-3 * exact, (est, exact)
+    print(f"{kind}: preconditioner error {est:.3e} (exact {exact:.3e})")
+
+
+def test_dlp_build_and_lr(hm, ctx):
+    """Double-layer matrix K + I/2: the device build equals
+    the oracle build (bit-identical trees, identical ranks, <= 1e-9 per
+    block), and its H-LR matches the oracle's (the paper's "L R = K" run,
+    Fig. 11 right)."""
+    from hm_inputs import sphere_normals
+    L, leaf, eps = 3, 32, 1e-4
+    x, w = sphere_points(L)
+    nr = sphere_normals(L)
+    P = Problem(x, w, leaf, 2.0, kernel=K.KERNEL_DLP, nrm=nr)
+    Go = build(P, eps)
+    Gg = ctx.build(x, w, leaf, 2.0, eps, kernel=2, normals=nr)
+    do = export(Go)
+    rep = compare(Gg.export(), do)
+    assert not rep["rank_mismatch"], rep
+    assert rep["worst"] <= TOL, rep
+    octx = TruncCtx(eps)
+    Fo, _ = o_lr(Go.clone(), eps, ctx=octx)
+    Gi = ctx.import_desc(do)
+    hm.lr(Gi, eps)
+    assert ctx.last_stats()["truncations"] == octx.count
+    dfo = export(Fo)
+    rep = compare(Gi.export(), dfo, near_block_set(dfo, octx))
+    assert not rep["unexplained_mismatch"], rep
+    assert rep["worst"] <= TOL, rep

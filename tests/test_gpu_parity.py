@@ -295,3 +295,56 @@ def test_flush_capture_replay(hm, ctx):
     # level batches hold every truncation except the rkmerge ones (T4)
     assert 0 < ntr <= ctx.last_stats()["truncations"]
     hm.flush_capture_free(ctx)
+
+
+@pytest.mark.parametrize("L,leaf,eps,alpha", [
+    (1, 4, 0.0, 1.0),       # n=80: exact arithmetic, every S0 branch incl. temporaries
+    (2, 8, 1e-4, -0.5),     # n=320: nested temporaries + rkmerge
+    (3, 32, 1e-4, 1.0),     # config 1
+])
+def test_addmul_std_parity(hm, ctx, L, leaf, eps, alpha):
+    """Device standard product S0 (hm_addmul_std) vs oracle.product.addmul_s0
+    (P:L806-883): same truncation count, identical ranks, <= 1e-9 per block;
+    at eps = 0 the exact product."""
+    from oracle.product import addmul_s0
+    P, G = _cfg(L, leaf, eps)
+    octx = TruncCtx(eps)
+    Zo, octx, st = addmul_s0(alpha, G.clone(), G.clone(), G.clone(), eps, ctx=octx)
+    do = export(Zo)
+    Gg = ctx.import_desc(export(G))
+    X, Y, Z = Gg.clone(), Gg.clone(), Gg.clone()
+    hm.addmul_std(alpha, X, Y, Z, eps)
+    s = ctx.last_stats()
+    assert s["addproduct_calls"] == st.addproduct
+    assert s["truncations"] == octx.count
+    dg = Z.export()
+    rep = compare(dg, do, near_block_set(do, octx))
+    assert not rep["unexplained_mismatch"], rep
+    assert rep["worst"] <= TOL, rep
+    if eps == 0.0:
+        Gd = G.to_dense()
+        ref = Gd + alpha * Gd @ Gd
+        from oracle.hmatrix import import_payload
+        Zg = import_payload(P.bt, dg).to_dense()
+        assert np.linalg.norm(Zg - ref) <= 1e-12 * np.linalg.norm(ref)
+    print(f"S0 n={P.ct.n}: {s['truncations']} truncations in {s['levels']} rounds")
+
+
+def test_addmul_std_vs_accumulated(hm, ctx):
+    """The paper's claim in numbers (Fig. 9): on the same input
+    the standard product truncates far more often than the accumulated one,
+    and both stay within the eps bound of each other (north-star check 3)."""
+    P, G = _cfg(3, 32, 1e-4)
+    Gg = ctx.import_desc(export(G))
+    Z2 = Gg.clone()
+    hm.addmul(1.0, Gg.clone(), Gg.clone(), Z2, 1e-4)
+    t2 = ctx.last_stats()["truncations"]
+    Z0 = Gg.clone()
+    hm.addmul_std(1.0, Gg.clone(), Gg.clone(), Z0, 1e-4)
+    t0 = ctx.last_stats()["truncations"]
+    assert t0 > 3 * t2, (t0, t2)
+    from oracle.hmatrix import import_payload
+    A = import_payload(P.bt, Z2.export()).to_dense()
+    B = import_payload(P.bt, Z0.export()).to_dense()
+    depth = P.bt.depth()
+    assert np.linalg.norm(A - B) <= 2 * (depth + 2) * 1e-4 * np.linalg.norm(A)

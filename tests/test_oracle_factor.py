@@ -110,3 +110,76 @@ def test_probe_residual_cfg1(kind):
     res = probe_residual(G0, F, v, kind)
     assert res <= 50 * eps, res
     assert fo.min_pivot > 0
+
+
+@pytest.mark.parametrize("kind", ["lr", "chol"])
+def test_solve_factor_and_precond_error(kind):
+    """solve_factor (block substitution through the cluster tree) equals
+    numpy.linalg.solve with the dense operator apply_factor(F, part, I) for
+    every part; the power-iteration preconditioner error
+    converges to numpy.linalg.norm(I - (F)^{-1} G, 2)."""
+    from oracle.factor import apply_factor, precond_error, solve_factor
+    from oracle import kernel as Kk
+    x, w = sphere_points(2)
+    P = Problem(x, w, 8, 2.0, kernel=Kk.KERNEL_SLP if kind == "lr" else Kk.KERNEL_SLP_SYM)
+    G = build(P, 1e-3)
+    F, _ = (lr if kind == "lr" else chol)(G.clone(), 1e-3)
+    n = P.ct.n
+    rng = np.random.default_rng(7)
+    V = rng.standard_normal((n, 3))
+    parts = ["L", "R", "LT", "RT"] if kind == "lr" else ["Lc", "LcT"]
+    for part in parts:
+        M = apply_factor(F, part, np.eye(n))
+        ref = np.linalg.solve(M, V)
+        got = solve_factor(F, part, V.copy())
+        assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref), part
+    Gd = G.to_dense()
+    if kind == "lr":
+        Fd = apply_factor(F, "L", apply_factor(F, "R", np.eye(n)))
+    else:
+        Fd = apply_factor(F, "Lc", apply_factor(F, "LcT", np.eye(n)))
+    E = np.eye(n) - np.linalg.solve(Fd, Gd)
+    exact = np.linalg.norm(E, 2)
+    est = precond_error(G, F, kind, iters=200)
+    assert abs(est - exact) <= 1e-3 * exact, (est, exact)
+    assert 1e-6 < exact < 1.0
+
+
+def test_dlp_kernel_pins():
+    """Double-layer matrix K + I/2 (reading R20): entries by
+    hand, unit diagonal 1/2, and the Gauss integral of the closed polyhedral
+    sphere: the row sums of K (without the I/2) tend to +1/2 at the O(h) rate
+    of the one-point collocation (error halves per refinement)."""
+    from oracle import kernel as Kk
+    from hm_inputs import sphere_normals
+    x = np.array([[0.0, 0.0, 0.0], [0.0, 0.0, 2.0]])
+    w = np.array([0.3, 0.7])
+    nr = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, -1.0]])
+    Kd = Kk.dense_matrix(x, w, kernel=Kk.KERNEL_DLP, nrm=nr)
+    # K_01 = w_1 ((x_1 - x_0) . n_1) / (4 pi 2^3) = 0.7 * (-2) / (32 pi)
+    assert Kd[0, 1] == pytest.approx(0.7 * -2.0 / (32 * np.pi), rel=1e-15)
+    assert Kd[1, 0] == pytest.approx(0.3 * -2.0 / (32 * np.pi), rel=1e-15)
+    assert Kd[0, 0] == Kd[1, 1] == 0.5
+    devs = []
+    for L in (2, 3, 4):
+        xs, ws = sphere_points(L)
+        Kd = Kk.dense_matrix(xs, ws, kernel=Kk.KERNEL_DLP, nrm=sphere_normals(L))
+        devs.append(np.abs(Kd.sum(1) - 0.5 - 0.5).max())
+    assert devs[2] < 0.01 and devs[1] < 0.6 * devs[0] and devs[2] < 0.6 * devs[1], devs
+
+
+def test_lr_of_dlp_probe_residual():
+    """H-LR with accumulated updates of the double-layer matrix K (the paper's
+    second test matrix, Fig. 11 right): probe residual of
+    L R ~ K within 50 eps (reading #21), preconditioner error finite."""
+    from oracle import kernel as Kk
+    from oracle.factor import precond_error
+    from hm_inputs import sphere_normals
+    x, w = sphere_points(3)
+    P = Problem(x, w, 32, 2.0, kernel=Kk.KERNEL_DLP, nrm=sphere_normals(3))
+    G = build(P, 1e-4)
+    F, fo = lr(G.clone(), 1e-4)
+    v = probe_vectors(P.ct.n)[P.perm]
+    assert probe_residual(G, F, v, "lr") <= 50 * 1e-4
+    err = precond_error(G, F, "lr", iters=20)
+    assert 0 < err < 0.1, err
