@@ -74,6 +74,13 @@ NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA/DMMA: SMs x FMA/clk
 CPU_SAMPLE_LEVEL = 5   # oracle sample: icosphere L5 (n = 20480) with config 4's leaf / eta / eps
 
 
+T0 = time.time()
+
+
+def log(msg):
+    print(f"[bench {time.time() - T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -301,6 +308,7 @@ def standalone_flush(hm, ctx, torch, dev, X, Y, G, eps, top=3):
     hm.addmul(1.0, X, Y, Z, eps)
     Z.free()
     info = hm.flush_capture_info(ctx)
+    log(f"flush capture: {len(info)} level batches")
     fl = [sum(trunc_flops(int(a), int(b), int(c), int(d)) for a, b, c, d in zip(L["m"], L["n"], L["l"], L["k"]))
           for L in info]
     order = sorted(range(len(info)), key=lambda i: -fl[i])[:top]
@@ -324,6 +332,7 @@ def standalone_flush(hm, ctx, torch, dev, X, Y, G, eps, top=3):
         tot_fl += fl[i]
         tot_ms += ms
     hm.flush_capture_free(ctx)
+    log("flush replay done")
     out = {"captured": {"levels": levels, "gflops": tot_fl / (tot_ms * 1e-3) / 1e9 if tot_ms else None,
                         "all_level_gflop": sum(fl) / 1e9,
                         "note": "TRUNC batches of the top levels by convention flops, replayed from captured stacks"}}
@@ -381,6 +390,7 @@ def run_ours(args, cfg):
     t0 = time.time()
     G = ctx.build(x, w, cfg["leaf"], cfg["eta"], cfg["eps"])
     build_s = time.time() - t0
+    log(f"built n={len(w)} in {build_s:.1f}s")
     gstats = G.stats()
     X, Y = G.clone(), G.clone()
     nsteps = args.warmup + args.steps
@@ -410,6 +420,7 @@ def run_ours(args, cfg):
         ev1.record(stream)
         torch.cuda.synchronize(dev)
     ms = ev0.elapsed_time(ev1)
+    log(f"timed {args.steps} steps: {ms / args.steps:.1f} ms/step")
     launches = ctx.last_stats()["kernel_launches"] - l0
     prof = ctx.profile_get()
     ctx.profile(False)
@@ -446,6 +457,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize(dev)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     e2e_value = ws * flops / (e2e_ms * 1e-3) / 1e9
+    log(f"e2e {e2e_ms:.1f} ms/step")
 
     # ---- roofline of the top kernel functions
     peaks = load_peaks()
@@ -475,6 +487,7 @@ def run_ours(args, cfg):
 
     # ---- standalone batched flush (captured + synthetic)
     flush = None
+    log("roofline done")
     if rank == 0 and not args.no_flush:
         try:
             flush = standalone_flush(hm, ctx, torch, dev, X, Y, G, cfg["eps"])
@@ -484,6 +497,7 @@ def run_ours(args, cfg):
     # ---- H-LR / H-Cholesky setup seconds (BASELINE configs[1], [2], [4] and the
     # metric's n = 81920 H-LR, "config 4'"), device time with CUDA events
     factor = {}
+    log("standalone flush done")
     if rank == 0 and not args.no_factor:
         X.free(), Y.free(), G.free()
         for key, L, leaf, eps, kern, op, reps in FACTOR_RUNS:
@@ -508,6 +522,7 @@ def run_ours(args, cfg):
                 Gf.free()
             G0.free()
             fgf = (fst["flops_trunc"] + fst["flops_eval"] + fst["flops_dense"]) / 1e9
+            log(f"{key}: build {tb:.1f}s, setup {min(times):.2f}s")
             factor[key] = {"setup_s": min(times), "runs": len(times), "n": len(wf), "leaf": leaf, "eps": eps,
                            "truncations": fst["truncations"], "trunc_cols": fst["trunc_cols"],
                            "convention_gflop": fgf, "gflops": fgf / min(times), "min_pivot": fst["min_pivot"],
@@ -517,6 +532,7 @@ def run_ours(args, cfg):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cores = host_cores()
         rate, dt, sample, gf, _ = oracle_sample(cfg, cores)
+        log(f"cpu baseline: {sample}")
         cpu = {"value": rate, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
 
     if rank == 0:

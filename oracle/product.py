@@ -205,12 +205,17 @@ class S2:
         if counter is not None:
             ctx.counter = counter
 
-    def addproduct(self, acc: Acc2, alpha, bx, by):
-        """Fig. 5, S2: evaluated terms are appended exactly."""
+    def addproduct(self, acc: Acc2, alpha, bx, by, X=None, Y=None):
+        """Fig. 5, S2: evaluated terms are appended exactly.
+        X, Y: the H-matrices the blocks bx, by belong to (default: the
+        product's X and Y; the inversion of Fig. 8 mixes G and the auxiliary
+        H); a pending product remembers them."""
+        X = self.X if X is None else X
+        Y = self.Y if Y is None else Y
         self.st.addproduct += 1
-        ev = evaluate(alpha, bx, by, self.X, self.Y, self.st, self.counter)
+        ev = evaluate(alpha, bx, by, X, Y, self.st, self.counter)
         if ev is None:
-            acc.pending.append((alpha, bx, by))
+            acc.pending.append((alpha, bx, by, X, Y))
         else:
             acc.terms.append(ev)
 
@@ -241,9 +246,9 @@ class S2:
                     base = (A0[ti.start - t.start:ti.start - t.start + ti.size],
                             B0[rj.start - r.start:rj.start - r.start + rj.size])
                 son = Acc2(ti, rj, base)
-                for alpha, bx, by in acc.pending:
+                for alpha, bx, by, X, Y in acc.pending:
                     for l in range(len(bx.s.sons)):
-                        self.addproduct(son, alpha, bx.son(i, l), by.son(l, j))
+                        self.addproduct(son, alpha, bx.son(i, l), by.son(l, j), X, Y)
                 row.append(son)
             grid.append(row)
         return grid

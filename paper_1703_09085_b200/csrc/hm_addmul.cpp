@@ -38,15 +38,21 @@ struct FP {            // device factor pair; rows relative to clusters starting
   int k;
 };
 
+// Operands carry the index of the H-matrix they belong to (Planner::mats):
+// the product has X, Y, Z; the factorizations one matrix G; the inversion of
+// Fig. 8 mixes G and the auxiliary H.  alpha is per product.
 struct Term {
   int bx, by, br, w;
   bool xd = false, yd = false;   // X|ts / Y|sr is a dense leaf (identity branches 0 / 2 available)
+  int xm = 0, ym = 0;
+  double alpha = 1.0;
 };
-struct Pend { int bx, by; };
+struct Pend { int bx, by; int xm, ym; double alpha; };
 
 struct Node {
   int t, r;
   int zt, zb;
+  int zm = 0;                 // index (Planner::mats) of the matrix holding block zb
   int base = -1;
   std::vector<Term> terms;
   std::vector<Pend> pend;
@@ -61,15 +67,18 @@ struct Planner {
   Arena persist;        // FP outputs (freed at the end of hm_addmul)
   const Tree& T;
   Mat *X, *Y, *Z;
+  std::vector<Mat*> mats;     // distinct matrices; X, Y, Z are mats[xm0], mats[ym0], mats[zm0]
+  int xm0 = 0, ym0 = 0, zm0 = 0;
   double alpha, eps;
   std::vector<FP> fps;
   std::vector<std::vector<Node>> levels;
-  std::vector<int> zresult;   // real adm leaf id -> FP id
-  std::vector<LeafDesc> lx, ly;
-  std::vector<double> lx_mat, lx_mn, ly_mat, ly_mn;   // DFS prefix sums (convention counts)
+  std::vector<std::vector<int>> zresult;   // [matrix][real adm leaf id] -> FP id
+  std::vector<std::pair<int, int>> touched;   // (matrix, block) whose zresult was set
+  std::vector<std::vector<LeafDesc>> ltab;      // per matrix: leaves in DFS order
+  std::vector<std::vector<double>> lmat, lmn;   // DFS prefix sums (convention counts)
+  std::vector<LeafDesc*> dltab;                 // device copies of ltab
   double t_wait = 0;
   int64_t n_sync = 0;
-  LeafDesc *dlx = nullptr, *dly = nullptr;
   // stats
   int64_t n_addproduct = 0, n_eval = 0, n_trunc = 0, n_cols = 0, n_merge = 0, n_dense = 0;
   double fl_trunc = 0, by_trunc = 0, fl_eval = 0, by_eval = 0, fl_dense = 0, by_dense = 0;
@@ -82,18 +91,39 @@ struct Planner {
   Arena* fp_arena = nullptr;   // where new_fp allocates (default: persist)
 
   Planner(Ctx* c_, const Tree& T_, Mat* X_, Mat* Y_, Mat* Z_, double a, double e)
-      : c(c_), persist(c_, true), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {}
+      : c(c_), persist(c_, true), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {
+    xm0 = add_mat(X_);
+    ym0 = add_mat(Y_);
+    zm0 = add_mat(Z_);
+  }
+  int add_mat(Mat* m) {
+    for (size_t i = 0; i < mats.size(); i++)
+      if (mats[i] == m) return (int)i;
+    mats.push_back(m);
+    return (int)mats.size() - 1;
+  }
+  int& zres(int m, int b) { return zresult[m][b]; }
+  void set_zres(int m, int b, int fp) {
+    zresult[m][b] = fp;
+    touched.push_back({m, b});
+  }
 
   int csize(int cl) const { return T.cl_size[cl]; }
   int cstart(int cl) const { return T.cl_start[cl]; }
   int yb(int by) const { return ytrans ? tmap[by] : by; }
 
   // Fig. 5 classification in printed branch order.
-  bool classify(int bx, int by, Term& out) const {
+  bool classify(int bx, int by, Term& out) const { return classify(bx, by, xm0, ym0, out); }
+  bool classify(int bx, int by, int xm, int ym, Term& out) const {
     const int kx = T.bl_kind[bx], ky = T.bl_kind[by];
     const int t = T.bl_row[bx], s = T.bl_col[bx], r = T.bl_col[by];
+    const Mat* Xm = mats[xm];
+    const Mat* Ym = mats[ym];
     out.bx = bx;
     out.by = by;
+    out.xm = xm;
+    out.ym = ym;
+    out.alpha = alpha;
     out.xd = kx == HM_BLOCK_DENSE;
     out.yd = ky == HM_BLOCK_DENSE;
     if (kx == HM_BLOCK_DENSE) {
@@ -103,9 +133,9 @@ struct Planner {
       if (csize(r) <= csize(s)) { out.br = 2; out.w = csize(r); }
       else { out.br = 3; out.w = csize(s); }
     } else if (kx == HM_BLOCK_ADM) {
-      out.br = 4; out.w = X->rank[bx];
+      out.br = 4; out.w = Xm->rank[bx];
     } else if (ky == HM_BLOCK_ADM) {
-      out.br = 5; out.w = Y->rank[yb(by)];
+      out.br = 5; out.w = Ym->rank[yb(by)];
     } else {
       return false;
     }
@@ -118,29 +148,37 @@ struct Planner {
       };
       if (kx == HM_BLOCK_DENSE) cand(csize(t) <= csize(s) ? 0 : 1, std::min(csize(t), csize(s)));
       if (ky == HM_BLOCK_DENSE) cand(csize(r) <= csize(s) ? 2 : 3, std::min(csize(r), csize(s)));
-      if (kx == HM_BLOCK_ADM) cand(4, X->rank[bx]);
-      if (ky == HM_BLOCK_ADM) cand(5, Y->rank[yb(by)]);
+      if (kx == HM_BLOCK_ADM) cand(4, Xm->rank[bx]);
+      if (ky == HM_BLOCK_ADM) cand(5, Ym->rank[yb(by)]);
     }
     return true;
   }
   bool narrow = true;
 
-  void addproduct(Node& nd, int bx, int by) {
+  void addproduct(Node& nd, int bx, int by) { addproduct(nd, bx, by, xm0, ym0, alpha); }
+  void addproduct(Node& nd, int bx, int by, int xm, int ym, double a) {
     n_addproduct++;
     Term tm;
-    if (classify(bx, by, tm)) { nd.terms.push_back(tm); n_eval++; }
-    else nd.pend.push_back(Pend{bx, by});
+    if (classify(bx, by, xm, ym, tm)) {
+      tm.alpha = a;
+      nd.terms.push_back(tm);
+      n_eval++;
+    } else {
+      nd.pend.push_back(Pend{bx, by, xm, ym, a});
+    }
   }
 
-  FP zview(int zb) const {
+  FP zview(int zb) const { return zview(zm0, zb); }
+  FP zview(int zm, int zb) const {
+    const Mat* Zm = mats[zm];
     FP f;
-    f.A = Z->pA[zb];
-    f.B = Z->pB[zb];
+    f.A = Zm->pA[zb];
+    f.B = Zm->pB[zb];
     f.lda = csize(T.bl_row[zb]);
     f.ldb = csize(T.bl_col[zb]);
     f.t0 = cstart(T.bl_row[zb]);
     f.r0 = cstart(T.bl_col[zb]);
-    f.k = Z->rank[zb];
+    f.k = Zm->rank[zb];
     return f;
   }
 
@@ -179,16 +217,17 @@ struct Planner {
 
   // H-side product over the DFS leaves of block blk of X (yside = false) or Y
   // (yside = true); trans: out += coef H|_blk^T V instead of H|_blk V.
-  struct EvalMeta { double cost; int blk, yside; };
+  struct EvalMeta { double cost; int blk, mat; };
   std::vector<EvalMeta> emeta;   // host-side companions of the level's EvalJobs
   double split_thr = -1;         // > 0: fixed split threshold (hm_test_eval_batched)
   std::vector<int2> erng;        // leaf-range table of split jobs (uploaded with the jobs)
 
-  void add_eval(std::vector<EvalJob>& ej, bool yside, int blk, int trans, double coef, double* out,
+  // H-side product over the DFS leaves of block blk of matrix mats[mi]
+  void add_eval(std::vector<EvalJob>& ej, int mi, int blk, int trans, double coef, double* out,
                 int ldo, int w, const double* V, int ldv, int vtrans, int videntity) {
     if (w <= 0) return;
     EvalJob e{};
-    e.leaves = yside ? dly : dlx;
+    e.leaves = dltab[mi];
     e.leaf_begin = T.bl_lbeg[blk];
     e.leaf_end = T.bl_lend[blk];
     e.trans = trans;
@@ -204,8 +243,8 @@ struct Planner {
     e.videntity = videntity;
     // convention work from DFS prefix sums over the leaf table (O(1) per term):
     // dense leaf 2 m'n' w flops, low-rank leaf 2 k'(m'+n') w; bytes = payload + panels
-    const std::vector<double>& pm = yside ? ly_mat : lx_mat;
-    const std::vector<double>& pn = yside ? ly_mn : lx_mn;
+    const std::vector<double>& pm = lmat[mi];
+    const std::vector<double>& pn = lmn[mi];
     const double smat = pm[e.leaf_end] - pm[e.leaf_begin];
     const double smn = pn[e.leaf_end] - pn[e.leaf_begin];
     double fl = videntity ? 0.0 : 2.0 * w * smat;   // expansion: a copy, not arithmetic
@@ -215,7 +254,7 @@ struct Planner {
     e.nrng = 0;
     e.rng = nullptr;
     ej.push_back(e);
-    emeta.push_back(EvalMeta{by + fl, blk, yside ? 1 : 0});
+    emeta.push_back(EvalMeta{by + fl, blk, mi});
   }
 
   // Load balance of one eval batch: a job whose cost exceeds thr is cut into
@@ -240,8 +279,8 @@ struct Planner {
       const EvalJob& e = ej[ji];
       const EvalMeta& em = emeta[ji];
       if (em.cost <= thr || e.next) { out.push_back(e); mout.push_back(em); continue; }
-      const std::vector<double>& pm = em.yside ? ly_mat : lx_mat;
-      const std::vector<double>& pn = em.yside ? ly_mn : lx_mn;
+      const std::vector<double>& pm = lmat[em.mat];
+      const std::vector<double>& pn = lmn[em.mat];
       auto bcost = [&](int b) {
         const double smat = pm[T.bl_lend[b]] - pm[T.bl_lbeg[b]], smn = pn[T.bl_lend[b]] - pn[T.bl_lbeg[b]];
         return 8.0 * (smat + smn * e.w) + (e.videntity ? 0.0 : 2.0 * e.w * smat);
@@ -290,7 +329,7 @@ struct Planner {
         }
         s.nrng = (int)(erng.size() - r0);
         s.rng = reinterpret_cast<const int2*>(static_cast<intptr_t>(r0));
-        if (s.nrng > 0) { out.push_back(s); mout.push_back(EvalMeta{g.cost, em.blk, em.yside}); }
+        if (s.nrng > 0) { out.push_back(s); mout.push_back(EvalMeta{g.cost, em.blk, em.mat}); }
       }
     }
     ej.swap(out);
@@ -341,32 +380,36 @@ struct Planner {
     // addeval (no transpose) over the stored block (r,s).
     const int ybk = yb(by);
     const int ytr = ytrans ? 0 : 1;
+    const Mat* Xm = mats[tm.xm];
+    const Mat* Ym = mats[tm.ym];
+    const int xi = tm.xm, yi = tm.ym;
+    const double al = tm.alpha;
     switch (tm.br) {
       case 0:  // A = alpha I_t ; B = Y|sr^T N_X^T
-        add_copy(cj, ctiles, a, m, nullptr, 0, nt, nt, 0, 1, alpha);
-        add_eval(ej, true, ybk, ytr, 1.0, b, n, w, X->pA[bx], nt, 1, 0);
+        add_copy(cj, ctiles, a, m, nullptr, 0, nt, nt, 0, 1, al);
+        add_eval(ej, yi, ybk, ytr, 1.0, b, n, w, Xm->pA[bx], nt, 1, 0);
         break;
       case 1:  // A = alpha N_X ; B = Y|sr^T I
-        add_copy(cj, ctiles, a, m, X->pA[bx], nt, nt, ns, 0, 0, alpha);
-        add_eval(ej, true, ybk, ytr, 1.0, b, n, w, nullptr, 0, 0, 1);
+        add_copy(cj, ctiles, a, m, Xm->pA[bx], nt, nt, ns, 0, 0, al);
+        add_eval(ej, yi, ybk, ytr, 1.0, b, n, w, nullptr, 0, 0, 1);
         break;
       case 2:  // B = I_r ; A = alpha X|ts N_Y   (view: N_Y = N_(r,s)^T)
         add_copy(cj, ctiles, b, n, nullptr, 0, nr, nr, 0, 1, 1.0);
-        if (ytrans) add_eval(ej, false, bx, 0, alpha, a, m, w, Y->pA[ybk], nr, 1, 0);
-        else add_eval(ej, false, bx, 0, alpha, a, m, w, Y->pA[by], ns, 0, 0);
+        if (ytrans) add_eval(ej, xi, bx, 0, al, a, m, w, Ym->pA[ybk], nr, 1, 0);
+        else add_eval(ej, xi, bx, 0, al, a, m, w, Ym->pA[by], ns, 0, 0);
         break;
       case 3:  // B = N_Y^T ; A = alpha X|ts I  (view: N_Y^T = N_(r,s))
-        if (ytrans) add_copy(cj, ctiles, b, n, Y->pA[ybk], nr, nr, ns, 0, 0, 1.0);
-        else add_copy(cj, ctiles, b, n, Y->pA[by], ns, nr, ns, 1, 0, 1.0);
-        add_eval(ej, false, bx, 0, alpha, a, m, w, nullptr, 0, 0, 1);
+        if (ytrans) add_copy(cj, ctiles, b, n, Ym->pA[ybk], nr, nr, ns, 0, 0, 1.0);
+        else add_copy(cj, ctiles, b, n, Ym->pA[by], ns, nr, ns, 1, 0, 1.0);
+        add_eval(ej, xi, bx, 0, al, a, m, w, nullptr, 0, 0, 1);
         break;
       case 4:  // A = alpha A_X ; B = Y|sr^T B_X
-        add_copy(cj, ctiles, a, m, X->pA[bx], nt, nt, w, 0, 0, alpha);
-        add_eval(ej, true, ybk, ytr, 1.0, b, n, w, X->pB[bx], ns, 0, 0);
+        add_copy(cj, ctiles, a, m, Xm->pA[bx], nt, nt, w, 0, 0, al);
+        add_eval(ej, yi, ybk, ytr, 1.0, b, n, w, Xm->pB[bx], ns, 0, 0);
         break;
       case 5:  // B = B_Y ; A = alpha X|ts A_Y   (view: A_Y = B_(r,s), B_Y = A_(r,s))
-        add_copy(cj, ctiles, b, n, ytrans ? Y->pA[ybk] : Y->pB[by], nr, nr, w, 0, 0, 1.0);
-        add_eval(ej, false, bx, 0, alpha, a, m, w, ytrans ? Y->pB[ybk] : Y->pA[by], ns, 0, 0);
+        add_copy(cj, ctiles, b, n, ytrans ? Ym->pA[ybk] : Ym->pB[by], nr, nr, w, 0, 0, 1.0);
+        add_eval(ej, xi, bx, 0, al, a, m, w, ytrans ? Ym->pB[ybk] : Ym->pA[by], ns, 0, 0);
         break;
     }
   }
@@ -413,9 +456,9 @@ struct Planner {
 
   // chained continuation jobs of the current eval batch (identity groups)
   std::vector<EvalJob> etail;
-  void add_eval_chained(std::vector<EvalJob>& ej, int& head, int& last, bool yside, int blk, int trans,
+  void add_eval_chained(std::vector<EvalJob>& ej, int& head, int& last, int mi, int blk, int trans,
                         double coef, double* out, int ldo, int w, const double* V, int ldv, int vtrans) {
-    add_eval(ej, yside, blk, trans, coef, out, ldo, w, V, ldv, vtrans, 0);
+    add_eval(ej, mi, blk, trans, coef, out, ldo, w, V, ldv, vtrans, 0);
     if (head < 0) {
       head = (int)ej.size() - 1;
       last = -1;
@@ -441,7 +484,8 @@ struct Planner {
     double* b = SB + (size_t)col * n;
     const int nt = csize(nd.t), nr = csize(nd.r);
     int head = -1, last = -1;
-    if (which == 1) add_copy(cj, ctiles, a, m, nullptr, 0, nt, nt, 0, 1, alpha);
+    // alpha is folded into the summed side (terms of one group may differ in alpha)
+    if (which == 1) add_copy(cj, ctiles, a, m, nullptr, 0, nt, nt, 0, 1, 1.0);
     else add_copy(cj, ctiles, b, n, nullptr, 0, nr, nr, 0, 1, 1.0);
     for (size_t i = 0; i < nd.terms.size(); i++) {
       if (g.role[i] != which) continue;
@@ -449,11 +493,11 @@ struct Planner {
       const int bx = tm.bx, by = tm.by, ybk = yb(by);
       const int ns = csize(T.bl_col[bx]);
       if (which == 1) {
-        add_eval_chained(ej, head, last, true, ybk, ytrans ? 0 : 1, 1.0, b, n, nt, X->pA[bx], nt, 1);
+        add_eval_chained(ej, head, last, tm.ym, ybk, ytrans ? 0 : 1, tm.alpha, b, n, nt, mats[tm.xm]->pA[bx], nt, 1);
       } else if (ytrans) {
-        add_eval_chained(ej, head, last, false, bx, 0, alpha, a, m, nr, Y->pA[ybk], nr, 1);
+        add_eval_chained(ej, head, last, tm.xm, bx, 0, tm.alpha, a, m, nr, mats[tm.ym]->pA[ybk], nr, 1);
       } else {
-        add_eval_chained(ej, head, last, false, bx, 0, alpha, a, m, nr, Y->pA[by], ns, 0);
+        add_eval_chained(ej, head, last, tm.xm, bx, 0, tm.alpha, a, m, nr, mats[tm.ym]->pA[by], ns, 0);
       }
     }
   }
@@ -531,7 +575,7 @@ struct Planner {
         else nd.red = nd.base;
       } else if (nd.zt == ZA || nd.zt == ZV) {
         kind = 2;
-        l = zview(nd.zb).k + kb + wt;
+        l = zview(nd.zm, nd.zb).k + kb + wt;
       } else if (nd.zt == ZD) {
         if (kb + wt > 0) { kind = 3; l = kb + wt; }
       } else {
@@ -597,7 +641,7 @@ struct Planner {
       Node& nd = nodes[s.node];
       int col = 0;
       if (s.kind == 2) {
-        FP zf = zview(nd.zb);
+        FP zf = zview(nd.zm, nd.zb);
         copy_view(zf, nd.t, nd.r, s.A, s.m, s.B, s.n, col, cj, ctiles);
         col += zf.k;
       }
@@ -639,7 +683,7 @@ struct Planner {
         GemmJob g{};
         g.A = s.A; g.lda = s.m; g.transA = 0;
         g.B = s.B; g.ldb = s.n; g.transB = 1;
-        g.C = Z->pA[nd.zb]; g.ldc = s.m;
+        g.C = mats[nd.zm]->pA[nd.zb]; g.ldc = s.m;
         g.m = s.m; g.n = s.n; g.k = s.l;
         g.alpha = 1.0; g.beta = 1.0;
         g.tile0 = gtiles;
@@ -688,7 +732,7 @@ struct Planner {
     t_d += now_s() - t3;
     for (auto& s : stacks) {
       Node& nd = nodes[s.node];
-      if (s.kind == 2 && nd.zt == ZA) zresult[nd.zb] = nd.result;
+      if (s.kind == 2 && nd.zt == ZA) set_zres(nd.zm, nd.zb, nd.result);
     }
     lt.d_ranks = d_ranks;
     lt.tr = std::move(tr);
@@ -719,6 +763,7 @@ struct Planner {
         Node ch;
         ch.t = T.cl_son0[t] + i;
         ch.r = T.cl_son0[r] + j;
+        ch.zm = nd.zm;
         if (lower_only && cstart(ch.t) < cstart(ch.r)) {
           ch.t = -1;
           out.push_back(std::move(ch));
@@ -736,7 +781,7 @@ struct Planner {
         for (auto& p : nd.pend) {
           const int s = T.bl_col[p.bx];
           for (int l = 0; l < T.cl_nsons[s]; l++)
-            addproduct(ch, T.son(p.bx, i, l), T.son(p.by, l, j));
+            addproduct(ch, T.son(p.bx, i, l), T.son(p.by, l, j), p.xm, p.ym, p.alpha);
         }
         out.push_back(std::move(ch));
       }
@@ -852,7 +897,7 @@ struct Planner {
           else {
             Node& nd = levels[lev][mn[mi]];
             nd.result = pre[w].out;
-            if (nd.zt == ZA) zresult[nd.zb] = nd.result;
+            if (nd.zt == ZA) set_zres(nd.zm, nd.zb, nd.result);
           }
         }
         scratch.release();
@@ -867,8 +912,8 @@ struct Planner {
     const int nb = T.nblocks();
     for (int b = 0; b < nb; b++) {
       if (T.bl_kind[b] != HM_BLOCK_ADM) continue;
-      if (zresult[b] < 0) throw Error(HM_ESTRUCT, "internal: admissible Z leaf without update");
-      const FP& f = fps[zresult[b]];
+      if (zres(zm0, b) < 0) throw Error(HM_ESTRUCT, "internal: admissible Z leaf without update");
+      const FP& f = fps[zres(zm0, b)];
       total += (size_t)(f.lda + f.ldb) * f.k;
     }
     double* pool = static_cast<double*>(c->dmalloc((total + 1) * sizeof(double)));
@@ -879,7 +924,7 @@ struct Planner {
     std::vector<int> nk(nb, 0);
     for (int b = 0; b < nb; b++) {
       if (T.bl_kind[b] != HM_BLOCK_ADM) continue;
-      const FP& f = fps[zresult[b]];
+      const FP& f = fps[zres(zm0, b)];
       nA[b] = pool + off;
       off += (size_t)f.lda * f.k;
       nB[b] = pool + off;
@@ -930,24 +975,29 @@ struct Planner {
   }
 
   void setup_tables(bool upload) {
-    zresult.assign(T.nblocks(), -1);
-    lx = leaf_table(*X);
-    ly = leaf_table(*Y);
-    for (int side = 0; side < 2; side++) {
-      const std::vector<LeafDesc>& lt = side ? ly : lx;
-      std::vector<double>& pm = side ? ly_mat : lx_mat;
-      std::vector<double>& pn = side ? ly_mn : lx_mn;
-      pm.assign(lt.size() + 1, 0.0);
-      pn.assign(lt.size() + 1, 0.0);
-      for (size_t i = 0; i < lt.size(); i++) {
-        const LeafDesc& L = lt[i];
-        pm[i + 1] = pm[i] + (L.kind == HM_BLOCK_DENSE ? (double)L.m * L.n : (double)L.k * (L.m + L.n));
-        pn[i + 1] = pn[i] + (double)(L.m + L.n);
-      }
+    const size_t nm = mats.size();
+    zresult.assign(nm, std::vector<int>(T.nblocks(), -1));
+    ltab.assign(nm, {});
+    lmat.assign(nm, {});
+    lmn.assign(nm, {});
+    dltab.assign(nm, nullptr);
+    for (size_t mi = 0; mi < nm; mi++) {
+      ltab[mi] = leaf_table(*mats[mi]);
+      refresh_sums(mi);
+      if (upload) dltab[mi] = persist.upload(ltab[mi]);
     }
-    if (upload) {
-      dlx = persist.upload(lx);
-      dly = persist.upload(ly);
+  }
+  // convention-count prefix sums of matrix mi's leaf table (after rank changes)
+  void refresh_sums(size_t mi) {
+    const std::vector<LeafDesc>& lt = ltab[mi];
+    std::vector<double>& pm = lmat[mi];
+    std::vector<double>& pn = lmn[mi];
+    pm.assign(lt.size() + 1, 0.0);
+    pn.assign(lt.size() + 1, 0.0);
+    for (size_t i = 0; i < lt.size(); i++) {
+      const LeafDesc& L = lt[i];
+      pm[i + 1] = pm[i] + (L.kind == HM_BLOCK_DENSE ? (double)L.m * L.n : (double)L.k * (L.m + L.n));
+      pn[i + 1] = pn[i] + (double)(L.m + L.n);
     }
   }
 
@@ -957,6 +1007,7 @@ struct Planner {
     root.t = T.bl_row[0];
     root.r = T.bl_col[0];
     root.zb = 0;
+    root.zm = zm0;
     root.zt = T.bl_kind[0] == HM_BLOCK_SUB ? ZS : (T.bl_kind[0] == HM_BLOCK_ADM ? ZA : ZD);
     addproduct(root, 0, 0);
     std::vector<Node> roots;
@@ -1017,11 +1068,11 @@ struct Factorizer {
       if (T.cl_nsons[t] != 0 && T.cl_nsons[t] != 2)
         throw Error(HM_EUNSUPPORTED, "H-LR/H-Cholesky need a binary cluster tree (P:L1361-1363)");
     P.setup_tables(false);
-    lt = P.lx;
+    lt = P.ltab[0];
     leafpos.assign(nb, -1);
     for (size_t i = 0; i < T.leaf_order.size(); i++) leafpos[T.leaf_order[i]] = (int)i;
     dlt = P.persist.upload(lt);
-    P.dlx = P.dly = dlt;
+    P.dltab[0] = dlt;
     own.assign(nb, {nullptr, 0});
     d_fail = static_cast<int*>(P.persist.alloc_bytes(sizeof(int)));
     HM_CUDA(cudaMemsetAsync(d_fail, 0, sizeof(int), c->stream));
@@ -1074,13 +1125,13 @@ struct Factorizer {
     P.fp_arena = &local;
     std::vector<int> zbs;
     for (auto& nd : roots) {
-      P.zresult[nd.zb] = -1;
+      P.zres(0, nd.zb) = -1;
       zbs.push_back(nd.zb);
     }
     P.run_from(std::move(roots));
     for (int zb : zbs) {
       if (T.bl_kind[zb] != HM_BLOCK_ADM) continue;
-      const int f = P.zresult[zb];
+      const int f = P.zres(0, zb);
       if (f < 0) throw Error(HM_ESTRUCT, "internal: flush produced no result");
       const FP& fp = P.fps[f];
       const int m = fp.lda, n = fp.ldb, k = fp.k;
@@ -1454,7 +1505,7 @@ void eval_batched_test(Ctx* c, Mat* H, int njobs, const int* blk, const int* tra
   std::vector<EvalJob> ej;
   for (int i = 0; i < njobs; i++) {
     if (blk[i] < 0 || blk[i] >= T.nblocks()) throw Error(HM_EINVAL, "hm_test_eval_batched: bad block id");
-    P.add_eval(ej, false, blk[i], trans[i] ? 1 : 0, coef[i], out[i], ldo[i], w[i], V[i], ldv[i], 0, 0);
+    P.add_eval(ej, 0, blk[i], trans[i] ? 1 : 0, coef[i], out[i], ldo[i], w[i], V[i], ldv[i], 0, 0);
   }
   P.launch_evals(ej, scratch, P.fl_eval, P.by_eval);
   HM_CUDA(cudaStreamSynchronize(c->stream));
