@@ -231,6 +231,19 @@ hm_status hm_lr(hm_ctx ctx, hm_mat G, double eps);
 hm_status hm_chol(hm_ctx ctx, hm_mat G, double eps, double shift);
 
 /*
+ * hm_inv: G <- approximate G^{-1} in place, H-matrix inversion with
+ * accumulated updates (§6, Fig. 8): block LR steps
+ * on the binary cluster tree, every update through addproduct / split /
+ * flush, an auxiliary H-matrix for H12 / H21 (allocated and
+ * released inside the call), dense leaf inverses by Gauss-Jordan without
+ * pivoting (the paper assumes invertible principal submatrices,
+ * P:L1357-1360).  Reading R21: Fig. 8's last addproduct goes to
+ * the (t1,t1) accumulator it is flushed from.  HM_EPIVOT on a singular leaf
+ * pivot; hm_stats: truncations etc. of the call, min_pivot.  Synchronizes.
+ */
+hm_status hm_inv(hm_ctx ctx, hm_mat G, double eps);
+
+/*
  * hm_solve_thin: X <- op(F)^{-1} X in place, F = an hm_lr / hm_chol result,
  * X: n x ncols device panel in tree order (ld ldx >= n).  op:
  *   HM_SOLVE_L (unit lower L), HM_SOLVE_R (upper R), HM_SOLVE_LT (L^T),
@@ -246,7 +259,8 @@ hm_status hm_solve_thin(hm_ctx ctx, hm_mat F, int op, double* x_dev, int64_t ldx
  * hm_precond_error: the paper's preconditioner error ||I - F^{-1} G||_2
  * ("estimate the spectral norm ... using a power iteration"),
  * F = L R (kind 0, after hm_lr) or L L^T (kind 1, after hm_chol), G the
- * unfactored matrix (e.g. an hm_clone taken before factorizing): `iters`
+ * unfactored matrix (e.g. an hm_clone taken before factorizing), or kind 2:
+ * F = the approximate inverse from hm_inv (E = I - F G); `iters`
  * power steps on E^T E from a seeded Gaussian start (device generator,
  * `seed`); *out = ||E v|| of the last step (a lower bound converging to
  * ||E||_2).  All vector work on the device; synchronizes.

@@ -228,6 +228,11 @@ def addmul_std(alpha, X: HMatrix, Y: HMatrix, Z: HMatrix, eps):
     Z.ctx.check(lib().hm_addmul_std(Z.ctx.h, float(alpha), X.h, Y.h, Z.h, float(eps)))
 
 
+def inv(G: HMatrix, eps):
+    """In-place H-inversion with accumulated updates (hm_inv, Fig. 8)."""
+    G.ctx.check(lib().hm_inv(G.ctx.h, G.h, float(eps)))
+
+
 def lr(G: HMatrix, eps):
     """In-place H-LR with accumulated updates (hm_lr): strict lower part = L
     (unit diagonal), upper part = R."""
@@ -274,7 +279,7 @@ def solve(F: HMatrix, x, op):
 def precond_error(G: HMatrix, F: HMatrix, kind="lr", iters=30, seed=1703):
     """||I - F^{-1} G||_2 by power iteration (hm_precond_error)."""
     out = C.c_double()
-    G.ctx.check(lib().hm_precond_error(G.ctx.h, G.h, F.h, 0 if kind == "lr" else 1, int(iters),
+    G.ctx.check(lib().hm_precond_error(G.ctx.h, G.h, F.h, {"lr": 0, "chol": 1, "inv": 2}[kind], int(iters),
                                        C.c_uint64(int(seed)), C.byref(out)))
     return out.value
 
@@ -423,5 +428,5 @@ def flush_capture_free(ctx: Context):
     ctx.check(lib().hm_flush_capture_free(ctx.h))
 
 
-__all__ = ["Context", "HMatrix", "HMError", "addmul", "addmul_std", "solve", "precond_error", "chol", "lr", "matvec", "lib", "test_trunc_batched",
+__all__ = ["Context", "HMatrix", "HMError", "addmul", "addmul_std", "inv", "solve", "precond_error", "chol", "lr", "matvec", "lib", "test_trunc_batched",
            "test_eval_batched", "flush_capture", "flush_capture_info", "flush_replay", "flush_capture_free"]

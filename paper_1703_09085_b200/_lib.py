@@ -65,7 +65,7 @@ class Prof(C.Structure):
 EXPORTS = [
     "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_build", "hm_build_nrm",
     "hm_import", "hm_export", "hm_export_sizes", "hm_export_into", "hm_clone", "hm_free", "hm_addmul", "hm_addmul_std",
-    "hm_lr", "hm_chol",
+    "hm_lr", "hm_chol", "hm_inv",
     "hm_matvec_thin", "hm_solve_thin", "hm_precond_error", "hm_stats", "hm_profile_enable", "hm_profile_reset", "hm_profile_get",
     "hm_test_trunc_batched", "hm_test_eval_batched",
     "hm_flush_capture", "hm_flush_capture_info", "hm_flush_replay", "hm_flush_capture_free",
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
         "hm_addmul": (C.c_int, [vp, C.c_double, vp, vp, vp, C.c_double]),
         "hm_addmul_std": (C.c_int, [vp, C.c_double, vp, vp, vp, C.c_double]),
         "hm_lr": (C.c_int, [vp, vp, C.c_double]),
+        "hm_inv": (C.c_int, [vp, vp, C.c_double]),
         "hm_chol": (C.c_int, [vp, vp, C.c_double, C.c_double]),
         "hm_matvec_thin": (C.c_int, [vp, vp, C.c_int, C.c_double, vp, C.c_int64, C.c_double, vp,
                                      C.c_int64, C.c_int]),

@@ -568,7 +568,10 @@ struct Planner {
       const int kb = nd.base >= 0 ? fps[nd.base].k : 0;
       groups[i] = plan_groups(nd);
       const int wt = groups[i].width;
-      if (!nd.pend.empty() || nd.force_split) {
+      if (!nd.pend.empty() || nd.force_split || nd.zt == ZS) {
+        // (iv) split with pending products; (iii) P = 0 into a subdivided
+        // block: reduce (T1), then the sons (every leaf below) receive the
+        // restricted base -- Fig. 7, the rkupdate of Fig. 3
         if (nd.zt == ZD && !nd.force_split)
           throw Error(HM_ESTRUCT, "flush: pending products into an inadmissible leaf");
         if (!nd.terms.empty()) { kind = 1; l = kb + wt; }
@@ -578,8 +581,6 @@ struct Planner {
         l = zview(nd.zm, nd.zb).k + kb + wt;
       } else if (nd.zt == ZD) {
         if (kb + wt > 0) { kind = 3; l = kb + wt; }
-      } else {
-        throw Error(HM_EUNSUPPORTED, "flush branch (iii) into a subdivided block with P = 0");
       }
       if (kind) stacks.push_back(Stack{i, kind, m, n, l, nullptr, nullptr, -1});
     }
@@ -744,7 +745,7 @@ struct Planner {
   std::vector<Node> split_level(std::vector<Node>& nodes) {
     std::vector<Node> next;
     for (auto& nd : nodes) {
-      if (nd.pend.empty()) continue;
+      if (nd.pend.empty() && nd.zt != ZS) continue;
       nd.child0 = (int)next.size();
       expand(nd, false, next);
     }
@@ -1489,6 +1490,7 @@ struct Factorizer {
 
 #include "hm_std.inc"
 #include "hm_solve.inc"
+#include "hm_inv.inc"
 
 }  // namespace
 
@@ -1623,7 +1625,7 @@ void solve_thin(Ctx* c, Mat* F, int part, double* x, int64_t ldx, int ncols) {
 // ||I - F^{-1} G0||_2 by power iteration on E^T E (oracle
 // factor.precond_error): F = L R (kind 0) or L L^T (kind 1) in place.
 double precond_error(Ctx* c, Mat* G0, Mat* F, int kind, int iters, uint64_t seed) {
-  if (!G0 || !F || iters <= 0) throw Error(HM_EINVAL, "hm_precond_error: bad arguments");
+  if (!G0 || !F || iters <= 0 || kind < 0 || kind > 2) throw Error(HM_EINVAL, "hm_precond_error: bad arguments");
   if (!G0->tree->same_structure(*F->tree)) throw Error(HM_ESTRUCT, "hm_precond_error: G and F trees differ");
   const int64_t n = F->tree->n;
   cudaStream_t st = c->stream;
@@ -1641,20 +1643,30 @@ double precond_error(Ctx* c, Mat* G0, Mat* F, int kind, int iters, uint64_t seed
     HM_CUDA(cudaStreamSynchronize(st));
     return std::sqrt(h);
   };
-  std::unique_ptr<Solver> s1(new Solver(c, F, kind == 0 ? 0 : 4)), s2(new Solver(c, F, kind == 0 ? 1 : 5));
-  std::unique_ptr<Solver> t1, t2;
+  // kind 0 / 1: F^{-1} by the factor solves; kind 2: F = the inverse itself (hm_inv)
+  std::unique_ptr<Solver> s1, s2, t1, t2;
+  if (kind != 2) {
+    s1.reset(new Solver(c, F, kind == 0 ? 0 : 4));
+    s2.reset(new Solver(c, F, kind == 0 ? 1 : 5));
+  }
   if (kind == 0) {   // F^{-T} = L^{-T} R^{-T}
     t1.reset(new Solver(c, F, 3));
     t2.reset(new Solver(c, F, 2));
   }
+  double* tmp = kind == 2 ? ar.alloc(n) : nullptr;
   launch_randn(v, n, seed, st);
   double nv = norm(dj_v);
   launch_axpby(0.0, v, n, 1.0 / nv, v, n, n, 1, st);
   double est = 0;
   for (int it = 0; it < iters; it++) {
-    matvec(c, G0, HM_OP_G, 1.0, v, n, 0.0, y, n, 1);            // y = G v
-    s1->rec(F->tree->bl_row[0], y, (int)n, 1);                    // y = F^{-1} G v
-    s2->rec(F->tree->bl_row[0], y, (int)n, 1);
+    if (kind == 2) {
+      matvec(c, G0, HM_OP_G, 1.0, v, n, 0.0, tmp, n, 1);         // y = Ginv (G v)
+      matvec(c, F, HM_OP_G, 1.0, tmp, n, 0.0, y, n, 1);
+    } else {
+      matvec(c, G0, HM_OP_G, 1.0, v, n, 0.0, y, n, 1);            // y = G v
+      s1->rec(F->tree->bl_row[0], y, (int)n, 1);                    // y = F^{-1} G v
+      s2->rec(F->tree->bl_row[0], y, (int)n, 1);
+    }
     launch_axpby(1.0, v, n, 0.0, w, n, n, 1, st);                  // w = v - y = E v
     launch_axpby(-1.0, y, n, 1.0, w, n, n, 1, st);
     est = norm(dj_w);
@@ -1663,9 +1675,11 @@ double precond_error(Ctx* c, Mat* G0, Mat* F, int kind, int iters, uint64_t seed
     if (kind == 0) {
       t1->rec(F->tree->bl_row[0], y, (int)n, 1);
       t2->rec(F->tree->bl_row[0], y, (int)n, 1);
-    } else {
+    } else if (kind == 1) {
       s1->rec(F->tree->bl_row[0], y, (int)n, 1);
       s2->rec(F->tree->bl_row[0], y, (int)n, 1);
+    } else {
+      matvec(c, F, HM_OP_GT, 1.0, w, n, 0.0, y, n, 1);            // y = Ginv^T w
     }
     matvec(c, G0, HM_OP_GT, 1.0, y, n, 0.0, v, n, 1);             // v = G^T F^{-T} w
     launch_axpby(1.0, w, n, -1.0, v, n, n, 1, st);                 // v = w - v = E^T E v_old
@@ -1675,6 +1689,58 @@ double precond_error(Ctx* c, Mat* G0, Mat* F, int kind, int iters, uint64_t seed
   }
   HM_CUDA(cudaStreamSynchronize(st));
   return est;
+}
+
+// H-inversion with accumulated updates (Fig. 8): G <- approximate G^{-1}
+void invert_matrix(Ctx* c, Mat* G, double eps, double* min_pivot) {
+  if (!G) throw Error(HM_EINVAL, "hm_inv: null matrix");
+  if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_inv: eps must be >= 0");
+  const Tree& T = *G->tree;
+  if (T.bl_kind[0] == HM_BLOCK_ADM) throw Error(HM_ESTRUCT, "hm_inv: the root block must not be admissible");
+  for (int t = 0; t < T.nclusters(); t++)
+    if (T.cl_nsons[t] == 0 && T.cl_size[t] > kMaxLeafFactor)
+      throw Error(HM_EUNSUPPORTED, "hm_inv: leaf cluster larger than " + std::to_string(kMaxLeafFactor) + " rows");
+  const int nb = T.nblocks();
+  Mat H;   // auxiliary H-matrix: same tree, zero
+  H.tree = G->tree;
+  H.rank.assign(nb, 0);
+  H.pA.assign(nb, nullptr);
+  H.pB.assign(nb, nullptr);
+  size_t nd = 0;
+  for (int b = 0; b < nb; b++)
+    if (T.bl_kind[b] == HM_BLOCK_DENSE) nd += (size_t)T.cl_size[T.bl_row[b]] * T.cl_size[T.bl_col[b]];
+  double* dp = static_cast<double*>(c->dmalloc((nd + 1) * sizeof(double)));
+  H.dpool = {dp, (nd + 1) * sizeof(double)};
+  HM_CUDA(cudaMemsetAsync(dp, 0, (nd + 1) * sizeof(double), c->stream));
+  size_t off = 0;
+  for (int b = 0; b < nb; b++)
+    if (T.bl_kind[b] == HM_BLOCK_DENSE) {
+      H.pA[b] = dp + off;
+      off += (size_t)T.cl_size[T.bl_row[b]] * T.cl_size[T.bl_col[b]];
+    }
+  c->sp_prepare();
+  {
+    Inverter I(c, G, &H, eps);
+    I.invert(T.bl_row[0], I.acc_for(0, 0));
+    I.finish(min_pivot);
+    hm_stats_t& s = c->last;
+    s.addproduct_calls = I.P.n_addproduct;
+    s.evaluated_terms = I.P.n_eval;
+    s.truncations = I.P.n_trunc;
+    s.trunc_cols = I.P.n_cols;
+    s.merges = I.P.n_merge;
+    s.dense_adds = I.P.n_dense;
+    s.levels = I.n_flush;
+    s.flops_trunc = I.P.fl_trunc;
+    s.bytes_trunc = I.P.by_trunc;
+    s.flops_eval = I.P.fl_eval;
+    s.bytes_eval = I.P.by_eval;
+    s.flops_dense = I.P.fl_dense;
+    s.bytes_dense = I.P.by_dense;
+    I.P.persist.release();
+  }
+  H.free_all(c);
+  HM_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 void addmul_std(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps) {

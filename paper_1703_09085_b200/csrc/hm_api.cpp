@@ -445,10 +445,21 @@ hm_status hm_solve_thin(hm_ctx ctx, hm_mat F, int op, double* x_dev, int64_t ldx
 }
 
 hm_status hm_precond_error(hm_ctx ctx, hm_mat G, hm_mat F, int kind, int iters, uint64_t seed, double* out) {
-  if (!ctx || !G || !F || !out || (kind != 0 && kind != 1)) return HM_EINVAL;
+  if (!ctx || !G || !F || !out || kind < 0 || kind > 2) return HM_EINVAL;
   return guard(ctx, [&] {
     set_device(ctx->c);
     *out = precond_error(&ctx->c, &G->m, &F->m, kind, iters, seed);
+  });
+}
+
+hm_status hm_inv(hm_ctx ctx, hm_mat G, double eps) {
+  if (!ctx || !G) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    double mp = 0;
+    ctx->c.last = hm_stats_t{};
+    invert_matrix(&ctx->c, &G->m, eps, &mp);
+    ctx->c.last.min_pivot = mp;
   });
 }
 

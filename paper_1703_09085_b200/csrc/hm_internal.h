@@ -224,6 +224,7 @@ void addmul(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps);
 void addmul_std(Ctx* c, double alpha, Mat* X, Mat* Y, Mat* Z, double eps);
 void solve_thin(Ctx* c, Mat* F, int part, double* x, int64_t ldx, int ncols);
 double precond_error(Ctx* c, Mat* G0, Mat* F, int kind, int iters, uint64_t seed);
+void invert_matrix(Ctx* c, Mat* G, double eps, double* min_pivot);
 void flush_replay(Ctx* c, int level, double eps, int reps, double* ms_out, int64_t* rank_sum);
 void eval_batched_test(Ctx* c, Mat* H, int njobs, const int* blk, const int* trans, const double* coef,
                        const double* const* V, const int* ldv, double* const* out, const int* ldo, const int* w,

@@ -441,6 +441,67 @@ __global__ void __launch_bounds__(256) k_leaf_factor(const LeafFactorJob* __rest
   if (tid == 0 && minpiv) minpiv[blockIdx.x] = mp;
 }
 
+// In-place inverse of one diagonal leaf per CTA by Gauss-Jordan elimination
+// without pivoting ("standard linear algebra"; the
+// paper assumes every principal submatrix invertible).  Pivot
+// breakdown sets *fail = cluster id + 1; minpiv[job] = min |pivot|.
+__global__ void __launch_bounds__(256) k_leaf_inverse(const LeafFactorJob* __restrict__ jobs, int* fail,
+                                                      double* minpiv) {
+  extern __shared__ double a[];
+  double* f = a + (size_t)jobs[blockIdx.x].m * jobs[blockIdx.x].m;
+  __shared__ double s_piv;
+  const LeafFactorJob J = jobs[blockIdx.x];
+  const int m = J.m, tid = threadIdx.x;
+  for (int e = tid; e < m * m; e += blockDim.x) a[e] = J.N[(e % m) + (int64_t)(e / m) * J.ld];
+  __syncthreads();
+  double mp = 1e300;
+  for (int k = 0; k < m; k++) {
+    if (tid == 0) s_piv = a[k + k * m];
+    for (int i = tid; i < m; i += blockDim.x) f[i] = a[i + k * m];   // column k before the step
+    __syncthreads();
+    const double p = s_piv;
+    if (!isfinite(p) || fabs(p) <= 1e-300) {
+      if (tid == 0) atomicCAS(fail, 0, J.cluster + 1);
+      return;
+    }
+    mp = fmin(mp, fabs(p));
+    const double pinv = 1.0 / p;
+    // row k: A[k][j] /= p (j != k), A[k][k] = 1/p
+    for (int j = tid; j < m; j += blockDim.x) a[k + j * m] = (j == k ? 1.0 : a[k + j * m]) * pinv;
+    __syncthreads();
+    // rows i != k: A[i][j] -= f_i A[k][j] (j != k), A[i][k] = -f_i / p
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = e % m, j = e / m;
+      if (i == k) continue;
+      a[e] = (j == k ? 0.0 : a[e]) - f[i] * a[k + j * m];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < m * m; e += blockDim.x) J.N[(e % m) + (int64_t)(e / m) * J.ld] = a[e];
+  if (tid == 0 && minpiv) minpiv[blockIdx.x] = mp;
+}
+
+void launch_leaf_inverse(const LeafFactorJob* d_jobs, int njobs, int* fail, double* minpiv, int maxm,
+                         cudaStream_t st) {
+  if (njobs <= 0) return;
+  ensure_smem_attr((const void*)k_leaf_inverse, 210 * 1024);
+  count_launch();
+  k_leaf_inverse<<<njobs, 256, (size_t)maxm * (maxm + 1) * 8, st>>>(d_jobs, fail, minpiv);
+}
+
+// dst_i[0:count_i] = 0 for a list of device ranges (zeroing H-matrix blocks)
+__global__ void k_zero_ranges(double* const* __restrict__ ptr, const int64_t* __restrict__ cnt) {
+  double* p = ptr[blockIdx.x];
+  const int64_t n = cnt[blockIdx.x];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0.0;
+}
+
+void launch_zero_ranges(double* const* d_ptr, const int64_t* d_cnt, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  k_zero_ranges<<<n, 256, 0, st>>>(d_ptr, d_cnt);
+}
+
 void launch_leaf_factor(const LeafFactorJob* d_jobs, int njobs, int chol, int* fail, double* minpiv,
                         int maxm, cudaStream_t st) {
   if (njobs <= 0) return;

@@ -191,6 +191,9 @@ void launch_trsm2(const TrsmJob* d_jobs, int njobs, const TrsmStep* d_steps, con
                   cudaStream_t st);   // eval.cu (shared-memory substitution + eval tiles)
 void launch_leaf_factor(const LeafFactorJob* d_jobs, int njobs, int chol, int* fail, double* minpiv,
                         int maxm, cudaStream_t st);
+void launch_leaf_inverse(const LeafFactorJob* d_jobs, int njobs, int* fail, double* minpiv, int maxm,
+                         cudaStream_t st);
+void launch_zero_ranges(double* const* d_ptr, const int64_t* d_cnt, int n, cudaStream_t st);
 void launch_gen(const GenJob* d_jobs, int njobs, int64_t ntiles, const double* x,
                 const double* w, const double* nrm, const int64_t* perm, int kernel, cudaStream_t st);
 void launch_norm(const NormJob* d_jobs, int njobs, double* out, cudaStream_t st);

@@ -176,3 +176,41 @@ def test_dlp_build_and_lr(hm, ctx):
     rep = compare(Gi.export(), dfo, near_block_set(dfo, octx))
     assert not rep["unexplained_mismatch"], rep
     assert rep["worst"] <= TOL, rep
+
+
+@pytest.mark.parametrize("L,leaf,eps", [(1, 4, 0.0), (2, 8, 0.0), (2, 8, 1e-4), (3, 32, 1e-4)])
+def test_inv_parity(hm, ctx, L, leaf, eps):
+    """Device H-inversion with accumulators (hm_inv, Fig. 8) vs
+    oracle.inverse.invert on the same imported H-matrix: same truncation
+    count, identical ranks, <= 1e-9 per block; at eps = 0 the exact inverse."""
+    from oracle.inverse import invert as o_invert
+    x, w = sphere_points(L)
+    P = Problem(x, w, leaf, 2.0)
+    G = build(P, eps)
+    octx = TruncCtx(eps)
+    Io, _ = o_invert(G.clone(), eps, octx)
+    Gg = ctx.import_desc(export(G))
+    hm.inv(Gg, eps)
+    assert ctx.last_stats()["truncations"] == octx.count
+    dg, do = Gg.export(), export(Io)
+    rep = compare(dg, do, near_block_set(do, octx))
+    assert not rep["unexplained_mismatch"], rep
+    assert rep["worst"] <= TOL, rep
+    if eps == 0.0:
+        D = import_payload(P.bt, dg).to_dense()
+        assert np.linalg.norm(G.to_dense() @ D - np.eye(P.ct.n)) <= 1e-10 * np.sqrt(P.ct.n)
+
+
+def test_inv_precond_error(hm, ctx):
+    """||I - G~^{-1} G||_2 of the device inverse by the device power iteration
+    (hm_precond_error kind 2) vs the dense exact value."""
+    x, w = sphere_points(3)
+    P = Problem(x, w, 32, 2.0)
+    G = build(P, 1e-4)
+    G0 = ctx.import_desc(export(G))
+    Gi = G0.clone()
+    hm.inv(Gi, 1e-4)
+    est = hm.precond_error(G0, Gi, "inv", iters=100)
+    D = import_payload(P.bt, Gi.export()).to_dense()
+    exact = np.linalg.norm(np.eye(P.ct.n) - D @ G.to_dense(), 2)
+    assert abs(est - exact) <= 1e-3 * exact, (est, exact)
