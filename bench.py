@@ -28,9 +28,16 @@ never on the product path.
 """
 from __future__ import annotations
 
+import os
+
+# the CPU oracle legs fork one single-threaded worker per core: pin BLAS to one
+# thread BEFORE numpy is imported anywhere (otherwise every worker runs a
+# core-count OpenBLAS pool and the host is oversubscribed)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
 import argparse
 import json
-import os
 import socket
 import statistics
 import subprocess

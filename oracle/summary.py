@@ -112,15 +112,19 @@ def compare_summaries(got, ref, tol, allowed=frozenset(), eps_bound=None):
     """North-star parity on summaries: identical ranks except on `allowed`
     blocks (near-threshold truncations), and per-block difference estimate
     ||S_got - S_ref||_F / 4 <= tol * max(||Z_ref,b||_F, 1e-12 ||Z_ref||_F)
-    (allowed blocks: <= eps_bound * the same denominator).  Returns a report."""
+    (allowed blocks whose rank flipped: <= eps_bound * the same denominator).
+    Returns a report."""
     assert np.array_equal(got["leaf_ids"], ref["leaf_ids"]), "different leaf sets"
     znorm = float(np.sqrt(np.sum(ref["fro"] ** 2)))
     den = np.maximum(ref["fro"], 1e-12 * znorm)
     diff = np.sqrt(np.sum((got["sk"] - ref["sk"]) ** 2, axis=(1, 2))) / ref["sk"].shape[1]
     rel = diff / den
     ids = ref["leaf_ids"]
-    mism = [int(ids[i]) for i in np.nonzero(got["ranks"] != ref["ranks"])[0]]
-    in_allowed = np.array([int(b) in allowed for b in ids], bool)
+    flipped = got["ranks"] != ref["ranks"]
+    mism = [int(ids[i]) for i in np.nonzero(flipped)[0]]
+    # only a near-flagged block whose rank actually flipped gets the eps bound;
+    # every other block (incl. near-flagged ones with equal rank) is strict
+    in_allowed = np.array([int(b) in allowed for b in ids], bool) & flipped
     strict = ~in_allowed
     worst = float(rel[strict].max()) if strict.any() else 0.0
     worst_b = int(ids[strict][np.argmax(rel[strict])]) if strict.any() else None

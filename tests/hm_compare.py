@@ -64,18 +64,21 @@ def near_block_set(d, octx):
     return near_blocks(d, near_tags(octx))
 
 
-def compare(dg, do, near_blocks=(), tol=1e-9):
+def compare(dg, do, near_blocks=(), tol=1e-9, eps=0.0):
     """Per-block parity (north star): identical ranks except on near-flagged
     blocks (rank_mismatch must be a subset of near_blocks: see
-    `unexplained_mismatch`) and relative Frobenius difference <= tol on every
-    other block.  Returns a report dict."""
+    `unexplained_mismatch`); relative Frobenius difference <= tol on EVERY
+    block whose rank agrees (the difference is measured rank-independently),
+    and <= max(tol, 20 eps) on a near-flagged block whose rank flipped (one
+    singular value at the threshold kept on one side, dropped on the other).
+    Returns a report dict."""
     pg, po = leaf_payloads(dg), leaf_payloads(do)
     assert pg.keys() == po.keys()
     total = 0.0
     for b, v in po.items():
         total += np.linalg.norm(v[1]) ** 2 if v[0] == "dense" else lowrank_norm(v[1], v[2]) ** 2
     znorm = np.sqrt(total)
-    rank_mis, worst, worst_b = [], 0.0, None
+    rank_mis, worst, worst_b, worst_flip = [], 0.0, None, 0.0
     for b, vo in po.items():
         vg = pg[b]
         if vo[0] == "dense":
@@ -86,10 +89,14 @@ def compare(dg, do, near_blocks=(), tol=1e-9):
                 rank_mis.append(b)
             den = max(lowrank_norm(vo[1], vo[2]), 1e-12 * znorm)
             rel = lowrank_diff(vg[1], vg[2], vo[1], vo[2]) / den
-        if b in near_blocks:
+        if vo[0] != "dense" and vg[1].shape[1] != vo[1].shape[1] and b in near_blocks:
+            worst_flip = max(worst_flip, rel)
             continue
         if rel > worst:
             worst, worst_b = rel, b
     near_blocks = set(near_blocks)
-    return dict(rank_mismatch=rank_mis, unexplained_mismatch=[b for b in rank_mis if b not in near_blocks],
-                worst=worst, worst_block=worst_b, znorm=znorm)
+    unexplained = [b for b in rank_mis if b not in near_blocks]
+    if worst_flip > max(tol, 20.0 * eps):
+        unexplained.append(("rank flip beyond the eps bound", worst_flip))
+    return dict(rank_mismatch=rank_mis, unexplained_mismatch=unexplained,
+                worst=worst, worst_block=worst_b, worst_flip=worst_flip, znorm=znorm)
