@@ -180,20 +180,30 @@ class HMatrix:
         self.ctx.check(lib().hm_stats(self.ctx.h, self.h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in _lib.Stats._fields_}
 
-    def export(self, pinned=False):
-        """Host description (dict of numpy arrays).  The payloads are written by
-        the library straight into freshly allocated arrays (hm_export_into);
-        pinned=True allocates them in page-locked memory (full-bandwidth D2H)."""
-        import torch
+    def export_sizes(self):
         nf, nd = C.c_int64(), C.c_int64()
         self.ctx.check(lib().hm_export_sizes(self.ctx.h, self.h, C.byref(nf), C.byref(nd)))
+        return nf.value, nd.value
 
-        def buf(cnt):
+    def export(self, pinned=False, bufs=None):
+        """Host description (dict of numpy arrays).  The payloads are written by
+        the library straight into host arrays (hm_export_into): freshly
+        allocated ones (pinned=True: page-locked, full-bandwidth D2H), or the
+        caller's preallocated (e.g. pinned) float64 buffers bufs = (factors,
+        dense) if they are large enough."""
+        import torch
+        nf, nd = self.export_sizes()
+
+        def buf(cnt, pre):
+            if pre is not None and pre.size >= cnt:
+                return pre[:cnt]
             if pinned:
                 return torch.empty(max(cnt, 1), dtype=torch.float64, pin_memory=True).numpy()[:cnt]
             return np.empty(cnt, np.float64)
 
-        fbuf, dbuf = buf(nf.value), buf(nd.value)
+        fbuf = buf(nf, bufs[0] if bufs else None)
+        dbuf = buf(nd, bufs[1] if bufs else None)
+        nf, nd = C.c_int64(nf), C.c_int64(nd)
         hd = _lib.HostDesc()
         self.ctx.check(lib().hm_export_into(self.ctx.h, self.h, C.byref(hd),
                                             C.c_void_p(fbuf.ctypes.data) if nf.value else None,

@@ -92,7 +92,7 @@ def test_split_conserves_content(tiny320):
 
     def content(a):
         C = a.content_lowrank()
-        for alpha, bx, by in a.pending:
+        for alpha, bx, by, _X, _Y in a.pending:
             X = Gd[bx.t.start:bx.t.start + bx.t.size, bx.s.start:bx.s.start + bx.s.size]
             Y = Gd[by.t.start:by.t.start + by.t.size, by.s.start:by.s.start + by.s.size]
             C = C + alpha * X @ Y
