@@ -60,6 +60,7 @@ struct Node {
   int result = -1;
   int child0 = -1;
   bool force_split = false;   // H-LR/H-Cholesky: split (reduce + expand) even with P = 0
+  bool no_expand = false;     // reduce only (T1); the caller expands the sons itself
 };
 
 struct Planner {
@@ -745,7 +746,7 @@ struct Planner {
   std::vector<Node> split_level(std::vector<Node>& nodes) {
     std::vector<Node> next;
     for (auto& nd : nodes) {
-      if (nd.pend.empty() && nd.zt != ZS) continue;
+      if ((nd.pend.empty() && nd.zt != ZS) || nd.no_expand) continue;
       nd.child0 = (int)next.size();
       expand(nd, false, next);
     }
@@ -795,7 +796,7 @@ struct Planner {
       std::vector<int> mn;
       for (int i = 0; i < (int)levels[lev].size(); i++) {
         const Node& nd = levels[lev][i];
-        if (!nd.pend.empty() && (nd.zt == ZA || nd.zt == ZV)) mn.push_back(i);
+        if (!nd.pend.empty() && !nd.no_expand && (nd.zt == ZA || nd.zt == ZV)) mn.push_back(i);
       }
       if (mn.empty()) continue;
       std::vector<Node>& kids = levels[lev + 1];
@@ -1112,7 +1113,24 @@ struct Factorizer {
   // ii, v) -- all of them in ONE level-synchronous batch.
   void flush(const Node& nd) { flush_many(std::vector<Node>{nd}); }
 
-  void flush_many(std::vector<Node> roots) {
+  // reduce_with: accumulators of subdivided solve targets whose T1 reduce is
+  // independent of these flushes -- it joins the first level batch (one
+  // dependent step instead of two); their .red is set on return
+  void flush_many(std::vector<Node> roots, const std::vector<Node*>& reduce_with = {}) {
+    std::vector<Node*> red_nodes;
+    const size_t nflush = roots.size();
+    for (Node* nd : reduce_with) {
+      if (nd->terms.empty()) {
+        nd->red = nd->base;
+        continue;
+      }
+      Node b = *nd;
+      b.force_split = true;
+      b.no_expand = true;
+      roots.push_back(std::move(b));
+      red_nodes.push_back(nd);
+      n_reduce_calls++;
+    }
     if (roots.empty()) return;
     if (c->plog) {
       int pend = 0;
@@ -1125,11 +1143,12 @@ struct Factorizer {
     Arena local(c, true);
     P.fp_arena = &local;
     std::vector<int> zbs;
-    for (auto& nd : roots) {
-      P.zres(0, nd.zb) = -1;
-      zbs.push_back(nd.zb);
+    for (size_t i = 0; i < nflush; i++) {
+      P.zres(0, roots[i].zb) = -1;
+      zbs.push_back(roots[i].zb);
     }
     P.run_from(std::move(roots));
+    for (size_t i = 0; i < red_nodes.size(); i++) red_nodes[i]->red = P.levels[0][nflush + i].red;
     for (int zb : zbs) {
       if (T.bl_kind[zb] != HM_BLOCK_ADM) continue;
       const int f = P.zres(0, zb);
@@ -1318,13 +1337,12 @@ struct Factorizer {
       if (T.bl_kind[it.b] == HM_BLOCK_SUB) subR.push_back(&it);
       else { leaf_accs.push_back(it.acc); leaf_targets.push_back({it.b, rmode}); }
     }
-    flush_many(std::move(leaf_accs));
-    trsm_set(t, leaf_targets);
-    if (subL.empty() && subR.empty()) return;
     std::vector<Node*> red;
     for (auto* it : subL) red.push_back(&it->acc);
     for (auto* it : subR) red.push_back(&it->acc);
-    reduce_many(red);
+    flush_many(std::move(leaf_accs), red);   // leaf flushes + the subdivided targets' T1 in one batch
+    trsm_set(t, leaf_targets);
+    if (subL.empty() && subR.empty()) return;
     const int t1 = son0(t), t2 = t1 + 1;
     std::vector<Item> L1, L2, R1, R2;
     for (auto* it : subL) {            // b = (t, r): sons (t_i, r_j), row-major

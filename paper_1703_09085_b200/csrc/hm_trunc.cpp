@@ -115,7 +115,8 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     // both factors tall and the one-sided M (min(m,n) x l) too large for shared
     // memory: QR both (two independent CTAs) so M = R_A R_B^T is only l x l --
     // avoids a third, sequential QR of M on the critical path
-    if (r.l < r.m && r.l < r.n && (int64_t)std::min(r.m, r.n) * r.l > 12 * 1024) qa[i] = qb[i] = 1;
+    static const int64_t both_thr = [] { const char* e = std::getenv("HM_QR_BOTH_THR"); return e ? std::atoll(e) : (int64_t)12 * 1024; }();
+    if (r.l < r.m && r.l < r.n && (int64_t)std::min(r.m, r.n) * r.l > both_thr) qa[i] = qb[i] = 1;
     p[i] = qa[i] ? r.l : r.m;
     q[i] = qb[i] ? r.l : r.n;
     if (qa[i]) tau_total += r.l;
@@ -337,7 +338,8 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     const TruncReq& r = reqs[i];
     const int L = std::max(p[i], q[i]), cc = std::min(p[i], q[i]);
     const int64_t full = svd_smem_need(L, cc);
-    if (full > caps[2] && L > cc && L <= 24 * 1024) {
+    static const bool use_preqr = [] { const char* e = std::getenv("HM_PREQR"); return !(e && e[0] == '0'); }();
+    if (use_preqr && full > caps[2] && L > cc && L <= 24 * 1024) {
       preqr[i] = 1;
       tauM[i] = ar.alloc(cc + 1);
       const int b = L <= 384 ? 0 : (L <= 768 ? 1 : (L <= 1536 ? 2 : 3));
