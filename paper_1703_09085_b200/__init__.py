@@ -41,9 +41,15 @@ def _ptr(a, ct):
 
 
 class Context:
-    """hm_ctx bound to a device and a CUDA stream."""
+    """hm_ctx bound to a device and a CUDA stream.
 
-    def __init__(self, device: int = 0, stream=None):
+    torch_allocator=True routes every device allocation of the library through
+    torch's caching allocator (hm_allocator hook: torch.cuda.caching_allocator_alloc
+    / _delete on the context's stream), so the library's memory is visible to
+    and shared with torch; default: the context's private stream-ordered pool
+    (no Python in the allocation path)."""
+
+    def __init__(self, device: int = 0, stream=None, torch_allocator=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1703_09085_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
@@ -51,8 +57,21 @@ class Context:
         with torch.cuda.device(device):
             s = stream if stream is not None else torch.cuda.current_stream(device)
         self.stream = s
+        self._alloc = None
+        if torch_allocator:
+            def _a(nbytes, stream_ptr, user):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), device, s)
+                except Exception:
+                    return None
+
+            def _f(ptr, nbytes, stream_ptr, user):
+                torch.cuda.caching_allocator_delete(int(ptr))
+
+            self._alloc = _lib.Allocator(_lib.ALLOC_FN(_a), _lib.FREE_FN(_f), None)   # kept alive with the context
         h = C.c_void_p()
-        st = lib().hm_ctx_create(device, C.c_void_p(s.cuda_stream), None, C.byref(h))
+        st = lib().hm_ctx_create(device, C.c_void_p(s.cuda_stream),
+                                 C.byref(self._alloc) if self._alloc is not None else None, C.byref(h))
         if st != 0:
             raise HMError(st, "hm_ctx_create failed")
         self.h = h

@@ -348,3 +348,28 @@ def test_addmul_std_vs_accumulated(hm, ctx):
     B = import_payload(P.bt, Z0.export()).to_dense()
     depth = P.bt.depth()
     assert np.linalg.norm(A - B) <= 2 * (depth + 2) * 1e-4 * np.linalg.norm(A)
+
+
+def test_torch_allocator_hook(hm):
+    """hm_allocator hook (include/hm.h) with torch's caching allocator: the
+    library's pools come from torch (torch.cuda.memory_allocated grows while
+    matrices live, returns after the context is destroyed) and the product is
+    unchanged (same result as with the private pool)."""
+    import torch
+    P, G = _cfg(2, 8, 1e-4)
+    d = export(G)
+    c1 = hm.Context(0)
+    X, Y, Z = c1.import_desc(d), c1.import_desc(d), c1.import_desc(d)
+    hm.addmul(1.0, X, Y, Z, 1e-4)
+    ref = Z.export()
+    c1.close()
+    base = torch.cuda.memory_allocated()
+    c2 = hm.Context(0, torch_allocator=True)
+    X, Y, Z = c2.import_desc(d), c2.import_desc(d), c2.import_desc(d)
+    assert torch.cuda.memory_allocated() > base
+    hm.addmul(1.0, X, Y, Z, 1e-4)
+    rep = compare(Z.export(), ref)
+    assert not rep["rank_mismatch"] and rep["worst"] <= 1e-12, rep
+    c2.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() == base
