@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <new>
 
 #include "hm_internal.h"
@@ -169,7 +170,15 @@ hm_status hm_ctx_create(int device, void* cuda_stream, const hm_allocator* alloc
     // GB per level would dominate the run time.  The device's default pool (the
     // one torch and other cudaMallocAsync users see) is left untouched; the
     // private pool's memory is returned by hm_ctx_destroy.
-    if (!c->c.has_alloc) {
+    // HM_POOL=default: the device's default pool (profiling tools that do not
+    // follow private pools); the release threshold is raised as before
+    const char* pe = std::getenv("HM_POOL");
+    if (!c->c.has_alloc && pe && std::string(pe) == "default") {
+      cudaMemPool_t dp;
+      HM_CUDA(cudaDeviceGetDefaultMemPool(&dp, device));
+      uint64_t thr = UINT64_MAX;
+      HM_CUDA(cudaMemPoolSetAttribute(dp, cudaMemPoolAttrReleaseThreshold, &thr));
+    } else if (!c->c.has_alloc) {
       cudaMemPoolProps props{};
       props.allocType = cudaMemAllocationTypePinned;
       props.location.type = cudaMemLocationTypeDevice;

@@ -891,7 +891,15 @@ void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int 
   // the 26 K bucket (208 KB) fits one CTA per SM whatever the batch: 512
   // threads (ncu: 256-thread CTAs left it at 12 % achieved occupancy)
   static const int t26 = [] { const char* e = std::getenv("HM_TS26_THREADS"); return e ? std::atoi(e) : 512; }();
-  int threads = njobs < 296 ? 512 : (cap > 10 * 1024 ? t26 : 256);
+  // latency mode (few stacks): threads per bucket (4K / 10K / 26K), HM_TS_LAT="a,b,c"
+  static int tlat[3] = {512, 512, 512};
+  static const bool tl_init = [] {
+    if (const char* e = std::getenv("HM_TS_LAT")) std::sscanf(e, "%d,%d,%d", &tlat[0], &tlat[1], &tlat[2]);
+    return true;
+  }();
+  (void)tl_init;
+  const int bk = cap <= 4 * 1024 ? 0 : (cap <= 10 * 1024 ? 1 : 2);
+  int threads = njobs < 296 ? tlat[bk] : (cap > 10 * 1024 ? t26 : 256);
   if (tsmall > 0 && njobs >= 296 && cap <= 4 * 1024) threads = tsmall;
   k_trunc_small<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, drop_rel_host());
 }

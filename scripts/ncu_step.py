@@ -15,7 +15,11 @@ import torch
 import paper_1703_09085_b200 as hm
 from hm_inputs import sphere_points
 mode, path = sys.argv[1], sys.argv[2]
-L, leaf, eps = 6, 64, 1e-6
+import os
+# NCU_L: icosphere level (6 = config 4; ncu's per-launch overhead grows with the
+# allocated device memory: the committed captures use L = 5, n = 20480, the
+# same leaf / eta / eps and the same kernels at the deep levels)
+L, leaf, eps = int(os.environ.get("NCU_L", "6")), 64, 1e-6
 ctx = hm.Context(0)
 if mode == "save":
     x, w = sphere_points(L)
