@@ -90,9 +90,11 @@ struct Planner {
   bool ytrans = false;
   std::vector<int> tmap;
   Arena* fp_arena = nullptr;   // where new_fp allocates (default: persist)
+  Arena heap;                  // non-LIFO FP outputs that must outlive a flush's local (stack) arena
+  bool fp_heap = false;        // new_fp allocates from heap (T1 results of no_expand nodes)
 
   Planner(Ctx* c_, const Tree& T_, Mat* X_, Mat* Y_, Mat* Z_, double a, double e)
-      : c(c_), persist(c_, true), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {
+      : c(c_), persist(c_, true), heap(c_, false), T(T_), X(X_), Y(Y_), Z(Z_), alpha(a), eps(e) {
     xm0 = add_mat(X_);
     ym0 = add_mat(Y_);
     zm0 = add_mat(Z_);
@@ -185,7 +187,7 @@ struct Planner {
 
   int new_fp(int m, int n, int kcap, int t0, int r0) {
     FP f;
-    Arena& ar = fp_arena ? *fp_arena : persist;
+    Arena& ar = fp_heap ? heap : (fp_arena ? *fp_arena : persist);
     f.A = ar.alloc((size_t)m * std::max(kcap, 1));
     f.B = ar.alloc((size_t)n * std::max(kcap, 1));
     f.lda = m;
@@ -697,7 +699,11 @@ struct Planner {
         continue;
       }
       const int kcap = trunc_kcap(s.m, s.n, s.l);
+      // a reduce-only node's T1 result is read after the enclosing flush has
+      // rewound its LIFO arena (Factorizer::flush_many): it lives on the heap
+      fp_heap = s.kind == 1 && nd.no_expand;
       const int out = new_fp(s.m, s.n, kcap, cstart(nd.t), cstart(nd.r));
+      fp_heap = false;
       s.out = out;
       TruncReq q{s.m, s.n, s.l, s.A, s.B, fps[out].A, fps[out].B, d_ranks + tr.size(), nullptr};
       tr.push_back(q);

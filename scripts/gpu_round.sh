@@ -9,7 +9,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/${TAG}_smi.txt 2>&1
 if [ -z "$SKIP_TESTS" ]; then
-  timeout 1800 python -m pytest tests -m gpu -x -q > $OUT/${TAG}_pytest_gpu.log 2>&1
+  timeout 1800 python -m pytest tests -m gpu -q > $OUT/${TAG}_pytest_gpu.log 2>&1
   echo "pytest exit $?" >> $OUT/${TAG}_pytest_gpu.log
   tail -3 $OUT/${TAG}_pytest_gpu.log
 fi
