@@ -1254,19 +1254,6 @@ struct Factorizer {
     HM_CHECK_LAUNCH();
   }
 
-  // panel solve on the rows of a dense leaf's transpose: N <- N op^{-1}
-  void trsm_right_dense(int mode, int s, int b) {
-    const int m = T.cl_size[T.bl_row[b]], n = T.cl_size[T.bl_col[b]];
-    Arena ar(c);
-    double* tmp = ar.alloc((size_t)m * n);
-    std::vector<CopyJob> cj{CopyJob{tmp, G->pA[b], n, m, n, m, 1, 0, 0, 1.0, 0}};
-    launch_copy(ar.upload(cj), 1, (int64_t)((n + 31) / 32) * ((m + 31) / 32), c->stream);
-    trsm(mode, s, tmp, n, m);
-    std::vector<CopyJob> cb{CopyJob{G->pA[b], tmp, m, n, m, n, 1, 0, 0, 1.0, 0}};
-    launch_copy(ar.upload(cb), 1, (int64_t)((m + 31) / 32) * ((n + 31) / 32), c->stream);
-    HM_CHECK_LAUNCH();
-  }
-
   void leaf_factor(int t) {
     n_leaf++;
     const int d = blk(t, t);
@@ -1377,7 +1364,87 @@ struct Factorizer {
     solve_set(t2, L2, R2);
   }
 
-  // ---- LR (O8)
+  // ---- merged recursion: factor G|tt from its accumulator AND
+  // solve every pending target of row cluster t (L: SOLVE_L blocks (t, r)) or
+  // column cluster t (R: SOLVE_R / SOLVE_LT blocks (t', t)) handed down by ALL
+  // ancestors.  O8/O9 run solve_set(t1, ...) once per ancestor level after
+  // lr(t) has returned; the sub-solves with a son t1 only need L|t1t1 / R|t1t1,
+  // so here they join the recursion into t1 as soon as lr(t1) is done: one
+  // dependent batch per cluster instead of one per (cluster, ancestor level).
+  // Every accumulator still receives exactly the addproducts of the serial
+  // recursion before it is reduced, split or flushed (same truncation inputs
+  // as oracle/factor.py), only independent steps share a batch.
+  void factor_merged(int t, Node acc, std::vector<Item> L, std::vector<Item> R) {
+    const int rmode = chol ? 2 : 1;
+    if (T.cl_nsons[t] == 0) {
+      // targets of a leaf cluster are leaves themselves: the diagonal flush and
+      // theirs are independent -> one batch; then the leaf factors, then the solves
+      std::vector<Node> accs{acc};
+      std::vector<std::pair<int, int>> targets;
+      for (auto& it : L) { accs.push_back(it.acc); targets.push_back({it.b, 0}); }
+      for (auto& it : R) { accs.push_back(it.acc); targets.push_back({it.b, rmode}); }
+      flush_many(std::move(accs));
+      leaf_factor(t);
+      trsm_set(t, targets);
+      return;
+    }
+    std::vector<Node> leaf_accs;
+    std::vector<std::pair<int, int>> leaf_targets;
+    std::vector<Item*> subL, subR;
+    for (auto& it : L) {
+      if (T.bl_kind[it.b] == HM_BLOCK_SUB) subL.push_back(&it);
+      else { leaf_accs.push_back(it.acc); leaf_targets.push_back({it.b, 0}); }
+    }
+    for (auto& it : R) {
+      if (T.bl_kind[it.b] == HM_BLOCK_SUB) subR.push_back(&it);
+      else { leaf_accs.push_back(it.acc); leaf_targets.push_back({it.b, rmode}); }
+    }
+    // T1 of the diagonal accumulator and of the subdivided targets: one batch
+    std::vector<Node*> red{&acc};
+    for (auto* it : subL) red.push_back(&it->acc);
+    for (auto* it : subR) red.push_back(&it->acc);
+    reduce_many(red);
+    std::vector<Node> ch;
+    P.expand(acc, chol, ch);   // (t1,t1), (t1,t2) [chol: placeholder], (t2,t1), (t2,t2)
+    const int t1 = son0(t), t2 = t1 + 1;
+    std::vector<Item> L1, L2, R1, R2;
+    for (auto* it : subL) {            // b = (t, r): sons (t_i, r_j), row-major
+      std::vector<Node> cs;
+      P.expand(it->acc, false, cs);
+      const int nr = T.cl_nsons[T.bl_col[it->b]];
+      for (int j = 0; j < nr; j++) {
+        L1.push_back(Item{T.son(it->b, 0, j), cs[j]});
+        L2.push_back(Item{T.son(it->b, 1, j), cs[nr + j]});
+      }
+    }
+    for (auto* it : subR) {            // b = (t', t): sons (t'_i, t_j)
+      std::vector<Node> cs;
+      P.expand(it->acc, false, cs);
+      const int nt = T.cl_nsons[T.bl_row[it->b]];
+      for (int i = 0; i < nt; i++) {
+        R1.push_back(Item{T.son(it->b, i, 0), cs[2 * i]});
+        R2.push_back(Item{T.son(it->b, i, 1), cs[2 * i + 1]});
+      }
+    }
+    const size_t nl = L1.size(), nr_ = R1.size();
+    std::vector<Item> L1x = L1, R1x = R1;
+    if (!chol) L1x.push_back(Item{blk(t1, t2), ch[1]});
+    R1x.push_back(Item{blk(t2, t1), ch[2]});
+    factor_merged(t1, ch[0], std::move(L1x), std::move(R1x));
+    for (size_t j = 0; j < nl; j++)          // acc_(t2,r') += -L_(t2,t1) R_(t1,r')
+      P.addproduct(L2[j].acc, blk(t2, t1), L1[j].b);
+    for (size_t i = 0; i < nr_; i++)         // acc_(t',t2) += -L_(t',t1) R_(t1,t2)  [chol: L_(t2,t1)^T]
+      P.addproduct(R2[i].acc, R1[i].b, blk(t1, t2));
+    P.addproduct(ch[3], blk(t2, t1), blk(t1, t2));
+    factor_merged(t2, ch[3], std::move(L2), std::move(R2));
+    // leaf targets of cluster t itself: their solves run through all of L|tt / R|tt
+    if (!leaf_accs.empty()) {
+      flush_many(std::move(leaf_accs));
+      trsm_set(t, leaf_targets);
+    }
+  }
+
+  // ---- LR (O8), serial recursion (HM_FACTOR_SERIAL=1: A/B reference for factor_merged)
   void lr(int t, Node acc) {
     if (T.cl_nsons[t] == 0) {
       flush(acc);
@@ -1390,46 +1457,6 @@ struct Factorizer {
     solve_set(t1, {Item{blk(t1, t2), ch[1]}}, {Item{blk(t2, t1), ch[2]}});
     P.addproduct(ch[3], blk(t2, t1), blk(t1, t2));
     lr(t2, ch[3]);
-  }
-
-  void solve_l(int t, int b, Node acc) {
-    const int kind = T.bl_kind[b];
-    if (kind == HM_BLOCK_ADM) {
-      flush(acc);
-      trsm(0, t, G->pA[b], T.cl_size[T.bl_row[b]], G->rank[b]);
-    } else if (kind == HM_BLOCK_DENSE) {
-      flush(acc);
-      trsm(0, t, G->pA[b], T.cl_size[T.bl_row[b]], T.cl_size[T.bl_col[b]]);
-    } else {
-      std::vector<Node> ch = split(acc, false);
-      const int t1 = son0(t), t2 = t1 + 1;
-      for (int j = 0; j < T.cl_nsons[T.bl_col[b]]; j++) {
-        const int b1 = T.son(b, 0, j), b2 = T.son(b, 1, j);
-        solve_l(t1, b1, ch[j]);
-        P.addproduct(ch[2 + j], blk(t2, t1), b1);
-        solve_l(t2, b2, ch[2 + j]);
-      }
-    }
-  }
-
-  void solve_r(int s, int b, Node acc) {
-    const int kind = T.bl_kind[b];
-    if (kind == HM_BLOCK_ADM) {
-      flush(acc);
-      trsm(1, s, G->pB[b], T.cl_size[T.bl_col[b]], G->rank[b]);
-    } else if (kind == HM_BLOCK_DENSE) {
-      flush(acc);
-      trsm_right_dense(1, s, b);
-    } else {
-      std::vector<Node> ch = split(acc, false);
-      const int s1 = son0(s), s2 = s1 + 1;
-      for (int i = 0; i < T.cl_nsons[T.bl_row[b]]; i++) {
-        const int b1 = T.son(b, i, 0), b2 = T.son(b, i, 1);
-        solve_r(s1, b1, ch[2 * i]);
-        P.addproduct(ch[2 * i + 1], b1, blk(s1, s2));
-        solve_r(s2, b2, ch[2 * i + 1]);
-      }
-    }
   }
 
   // ---- Cholesky (O9)
@@ -1445,26 +1472,6 @@ struct Factorizer {
     solve_set(t1, {}, {Item{blk(t2, t1), ch[2]}});
     P.addproduct(ch[3], blk(t2, t1), blk(t1, t2));   // Y = L^T view: (t1,t2) of L^T = (t2,t1) of L
     cholesky(t2, ch[3]);
-  }
-
-  void solve_lt(int s, int b, Node acc) {
-    const int kind = T.bl_kind[b];
-    if (kind == HM_BLOCK_ADM) {
-      flush(acc);
-      trsm(2, s, G->pB[b], T.cl_size[T.bl_col[b]], G->rank[b]);
-    } else if (kind == HM_BLOCK_DENSE) {
-      flush(acc);
-      trsm_right_dense(2, s, b);
-    } else {
-      std::vector<Node> ch = split(acc, false);
-      const int s1 = son0(s), s2 = s1 + 1;
-      for (int i = 0; i < T.cl_nsons[T.bl_row[b]]; i++) {
-        const int b1 = T.son(b, i, 0), b2 = T.son(b, i, 1);
-        solve_lt(s1, b1, ch[2 * i]);
-        P.addproduct(ch[2 * i + 1], b1, blk(s1, s2));
-        solve_lt(s2, b2, ch[2 * i + 1]);
-      }
-    }
   }
 
   // compact G's admissible factors into one pool; check pivots
@@ -1612,7 +1619,9 @@ void factorize(Ctx* c, Mat* G, double eps, bool chol, double shift, double* min_
   Factorizer F(c, G, eps, chol);
   Node root = F.acc_for(0);
   const int t = T.bl_row[0];
-  if (chol) F.cholesky(t, root);
+  static const bool serial = std::getenv("HM_FACTOR_SERIAL") != nullptr;
+  if (!serial) F.factor_merged(t, root, {}, {});
+  else if (chol) F.cholesky(t, root);
   else F.lr(t, root);
   F.finish(min_pivot);
   if (std::getenv("HM_DEBUG_TIMING"))

@@ -47,6 +47,11 @@ Ctx::~Ctx() {
   if (ws) dfree(ws, ws_cap * sizeof(double));
   if (sp) dfree(sp, sp_cap);
   cudaStreamSynchronize(stream);
+  for (int i = 0; i < kAux; i++) {
+    if (aux[i]) { cudaStreamSynchronize(aux[i]); cudaStreamDestroy(aux[i]); }
+    if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
   if (pin) cudaFreeHost(pin);
   if (pool) cudaMemPoolDestroy(pool);
   if (plog) std::fclose(plog);
@@ -100,21 +105,44 @@ cudaEvent_t Ctx::get_event() {
   return e;
 }
 
-void Ctx::prof_begin(int cls, cudaEvent_t* a) {
+bool Ctx::multi_stream() {
+  static const bool on = [] { const char* e = std::getenv("HM_STREAMS"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
+cudaStream_t Ctx::fork(int i) {
+  if (!multi_stream()) return stream;
+  if (!aux[i]) {
+    HM_CUDA(cudaStreamCreateWithFlags(&aux[i], cudaStreamNonBlocking));
+    HM_CUDA(cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming));
+  }
+  if (!ev_fork) HM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  HM_CUDA(cudaEventRecord(ev_fork, stream));
+  HM_CUDA(cudaStreamWaitEvent(aux[i], ev_fork, 0));
+  return aux[i];
+}
+
+void Ctx::join(int i) {
+  if (!multi_stream() || !aux[i]) return;
+  HM_CUDA(cudaEventRecord(ev_join[i], aux[i]));
+  HM_CUDA(cudaStreamWaitEvent(stream, ev_join[i], 0));
+}
+
+void Ctx::prof_begin(int cls, cudaEvent_t* a, cudaStream_t st) {
   (void)cls;
   if (!prof) return;
   *a = get_event();
-  HM_CUDA(cudaEventRecord(*a, stream));
+  HM_CUDA(cudaEventRecord(*a, st ? st : stream));
   if (plog && !pbase) {
     HM_CUDA(cudaEventCreate(&pbase));
     HM_CUDA(cudaEventRecord(pbase, stream));
   }
 }
 
-void Ctx::prof_end(int cls, cudaEvent_t a, double fl, double by) {
+void Ctx::prof_end(int cls, cudaEvent_t a, double fl, double by, cudaStream_t st) {
   if (!prof || !a) return;
   cudaEvent_t b = get_event();
-  cudaEventRecord(b, stream);
+  cudaEventRecord(b, st ? st : stream);
   pend.push_back(Pending{cls, a, b, fl, by, std::move(note)});
   note.clear();
   if (pend.size() > 4096) prof_collect();

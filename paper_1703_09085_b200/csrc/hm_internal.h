@@ -107,8 +107,18 @@ struct Ctx {
   void* dmalloc(size_t bytes);
   void dfree(void* p, size_t bytes);
   cudaEvent_t get_event();
-  void prof_begin(int cls, cudaEvent_t* a);
-  void prof_end(int cls, cudaEvent_t a, double flops, double bytes);
+  void prof_begin(int cls, cudaEvent_t* a, cudaStream_t st = nullptr);
+  void prof_end(int cls, cudaEvent_t a, double flops, double bytes, cudaStream_t st = nullptr);
+  // auxiliary streams: independent kernel groups of one TRUNC batch (the fused
+  // small stacks, the QR / SVD shared-memory buckets) run side by side.
+  // fork(i): aux[i] waits for everything enqueued on `stream` so far;
+  // join(i): `stream` waits for aux[i].  HM_STREAMS=0: everything on `stream`.
+  static constexpr int kAux = 5;
+  cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool multi_stream();
+  cudaStream_t fork(int i);
+  void join(int i);
   void prof_collect();   // synchronizes pending events
 };
 
@@ -157,10 +167,12 @@ struct ProfScope {
   int cls;
   double fl, by;
   cudaEvent_t a = nullptr;
-  ProfScope(Ctx* c_, int cls_, double fl_ = 0, double by_ = 0) : c(c_), cls(cls_), fl(fl_), by(by_) {
-    c->prof_begin(cls, &a);
+  cudaStream_t st;
+  ProfScope(Ctx* c_, int cls_, double fl_ = 0, double by_ = 0, cudaStream_t st_ = nullptr)
+      : c(c_), cls(cls_), fl(fl_), by(by_), st(st_) {
+    c->prof_begin(cls, &a, st);
   }
-  ~ProfScope() { c->prof_end(cls, a, fl, by); }
+  ~ProfScope() { c->prof_end(cls, a, fl, by, st); }
 };
 
 // Cluster tree + block tree, breadth-first numbered.

@@ -83,13 +83,27 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
     c->prof_note("fused jobs " + std::to_string(nf) + " maxmn " + std::to_string(mx) + " maxl " + std::to_string(ml) +
                  " staged " + std::to_string(rest.size()));
   }
+  // the fused small stacks and the staged pipeline of the larger ones are
+  // independent: the fused kernels run on an auxiliary stream next to it
+  bool forked = false;
   {
-    ProfScope ps(c, PC_FUSED, fl, by);
-    for (int b = 0; b < 3; b++)
-      if (!fb[b].empty()) launch_trunc_small(ar.upload(fb[b]), (int)fb[b].size(), eps, fcap[b], c->stream);
-    HM_CHECK_LAUNCH();
+    const TruncSmallJob* dj[3];
+    bool any = false;
+    for (int b = 0; b < 3; b++) {
+      dj[b] = fb[b].empty() ? nullptr : ar.upload(fb[b]);
+      any = any || dj[b];
+    }
+    if (any) {
+      forked = !rest.empty() && c->multi_stream();
+      cudaStream_t sf = forked ? c->fork(0) : c->stream;
+      ProfScope ps(c, PC_FUSED, fl, by, sf);
+      for (int b = 0; b < 3; b++)
+        if (dj[b]) launch_trunc_small(dj[b], (int)fb[b].size(), eps, fcap[b], sf);
+      HM_CHECK_LAUNCH();
+    }
   }
   trunc_general(c, ar, rest, eps);
+  if (forked) c->join(0);
 }
 
 static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double eps) {
@@ -181,6 +195,21 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     return qr_has_T(rows, l) ? L.T + (size_t)ch * ((l + 15) / 16) * 256 : nullptr;
   };
   // --- QR jobs, bucketed by shared-memory need
+  static const int qr_stepped = [] { const char* e = std::getenv("HM_QR_STEPPED"); return e ? std::atoi(e) : 1; }();
+  static const int qr_stepped_min = [] { const char* e = std::getenv("HM_QR_STEPPED_MIN"); return e ? std::atoi(e) : 32; }();
+  auto stepped_ok = [&](int njobs) { return qr_stepped && njobs >= qr_stepped_min; };
+  // bucket b <= 2 (m <= 1536, every job has a T buffer): stepped QR for batches,
+  // the one-CTA-per-job kernel for the few-job (latency-bound) case
+  auto launch_bucket = [&](const std::vector<QrJob>& v, const QrJob* dv, int b, int cap, cudaStream_t s) {
+    if (b <= 2 && stepped_ok((int)v.size())) {
+      std::vector<int> nc(v.size());
+      int mm = 0;
+      for (size_t i = 0; i < v.size(); i++) { nc[i] = v[i].n; mm = std::max(mm, v[i].m); }
+      launch_qr_stepped(dv, nc.data(), (int)v.size(), mm, s);
+    } else {
+      launch_qr_blocked(dv, (int)v.size(), cap, s);
+    }
+  };
   auto launch_qr_set = [&](const std::vector<QrJob>& jobs) {
     std::vector<QrJob> qs, qbk[4], qr_huge;
     for (const QrJob& j : jobs) {
@@ -190,19 +219,39 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       const int b = j.m <= 384 ? 0 : (j.m <= 768 ? 1 : (j.m <= 1536 ? 2 : 3));
       qbk[b].push_back(j);
     }
-    if (!qs.empty()) {
-      ProfScope pb(c, PC_QR_SMALL, 0, (double)qs.size());
-      launch_qr(ar.upload(qs), (int)qs.size(), 4 * 1024, st);
+    // stepped QR (qr.cu): jobs sorted by column count, so that every panel step
+    // launches only the prefix of jobs that still has columns left
+    for (int b = 0; b < 3; b++)
+      if (stepped_ok((int)qbk[b].size()))
+        std::stable_sort(qbk[b].begin(), qbk[b].end(), [](const QrJob& x, const QrJob& y) { return x.n > y.n; });
+    // uploads first (they are ordered on the main stream), then every bucket
+    // on its own auxiliary stream: the buckets are independent problems
+    const QrJob* dqs = qs.empty() ? nullptr : ar.upload(qs);
+    const QrJob* dqh = qr_huge.empty() ? nullptr : ar.upload(qr_huge);
+    const QrJob* dqb[4];
+    int used = (dqs ? 1 : 0) + (dqh ? 1 : 0);
+    for (int b = 0; b < 4; b++) {
+      dqb[b] = qbk[b].empty() ? nullptr : ar.upload(qbk[b]);
+      used += dqb[b] ? 1 : 0;
     }
+    const bool par = used > 1 && c->multi_stream();
     // blocked (compact-WY) QR, bucketed by panel height so that small panels
     // get several CTAs per SM: cap = 16 * rows doubles of shared memory
     const int qcap[4] = {6 * 1024, 12 * 1024, 24 * 1024, 24 * 1024};
-    for (int b = 0; b < 4; b++)
-      if (!qbk[b].empty()) {
-        ProfScope pb(c, PC_QR_B0 + b, 0, (double)qbk[b].size());
-        launch_qr_blocked(ar.upload(qbk[b]), (int)qbk[b].size(), qcap[b], st);
+    for (int b = 3; b >= 0; b--)
+      if (dqb[b]) {
+        cudaStream_t sb = par ? c->fork(1 + b) : st;
+        ProfScope pb(c, PC_QR_B0 + b, 0, (double)qbk[b].size(), sb);
+        launch_bucket(qbk[b], dqb[b], b, qcap[b], sb);
       }
-    if (!qr_huge.empty()) launch_qr(ar.upload(qr_huge), (int)qr_huge.size(), 0, st);
+    if (dqs) {
+      ProfScope pb(c, PC_QR_SMALL, 0, (double)qs.size());
+      launch_qr(dqs, (int)qs.size(), 4 * 1024, st);
+    }
+    if (dqh) launch_qr(dqh, (int)qr_huge.size(), 0, st);
+    if (par)
+      for (int b = 0; b < 4; b++)
+        if (dqb[b]) c->join(1 + b);
   };
   std::vector<QrJob> qjobs;
   std::vector<double*> tauA(nj, nullptr), tauB(nj, nullptr), Mp(nj, nullptr), TA(nj, nullptr), TB(nj, nullptr);
@@ -350,7 +399,11 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   {
     ProfScope ps(c, PC_PREQR, 0, 0);
     for (int b = 0; b < 4; b++)
-      if (!pq[b].empty()) launch_qr_blocked(ar.upload(pq[b]), (int)pq[b].size(), pqcap[b], st);
+      if (!pq[b].empty()) {
+        if (b <= 2 && stepped_ok((int)pq[b].size()))
+          std::stable_sort(pq[b].begin(), pq[b].end(), [](const QrJob& x, const QrJob& y) { return x.n > y.n; });
+        launch_bucket(pq[b], ar.upload(pq[b]), b, pqcap[b], st);
+      }
     HM_CHECK_LAUNCH();
   }
   for (int i = 0; i < nj; i++) {
@@ -386,11 +439,22 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   c->prof_note(shapes);
   {
     ProfScope ps(c, PC_SVD, fl_svd, 0);
+    const SvdJob* dsj[4];
+    int used = 0;
     for (int b = 0; b < 4; b++) {
-      if (sj[b].empty()) continue;
-      ProfScope pb(c, PC_SVD_B0 + b, fl_b[b], (double)sj[b].size());
-      launch_svd(ar.upload(sj[b]), (int)sj[b].size(), eps, caps[b], st);
+      dsj[b] = sj[b].empty() ? nullptr : ar.upload(sj[b]);
+      used += dsj[b] ? 1 : 0;
     }
+    const bool par = used > 1 && c->multi_stream();
+    for (int b = 3; b >= 0; b--) {   // the largest problems first
+      if (!dsj[b]) continue;
+      cudaStream_t sb = par ? c->fork(1 + b) : st;
+      ProfScope pb(c, PC_SVD_B0 + b, fl_b[b], (double)sj[b].size(), sb);
+      launch_svd(dsj[b], (int)sj[b].size(), eps, caps[b], sb);
+    }
+    if (par)
+      for (int b = 0; b < 4; b++)
+        if (dsj[b]) c->join(1 + b);
     HM_CHECK_LAUNCH();
   }
   if (dump) {

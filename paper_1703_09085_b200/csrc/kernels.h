@@ -181,7 +181,11 @@ struct NormJob {
 void launch_gemm(const GemmJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_gemm_mapped(const GemmJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
 void launch_qr(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
-void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);   // rows <= 24576
+void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st);
+// Stepped variant (panel kernel + multi-CTA DMMA trailing update per 16
+// columns); jobs sorted by n descending, ncols = host copy of their n; every
+// job has a T buffer and m <= 1536 (max_m = the largest m).
+void launch_qr_stepped(const QrJob* d_jobs, const int* ncols, int njobs, int max_m, cudaStream_t st);   // rows <= 24576
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);

@@ -403,6 +403,319 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_qr_blocked(const QrJob
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// Stepped blocked QR: the same factorisation as k_qr_blocked
+// (16-column panels, compact-WY T per panel, LAPACK layout), but the batch
+// advances panel by panel with TWO kernels per step:
+//   k_qrs_panel : one CTA per job factors the 16-column panel in shared memory
+//                 (the Householder loop of k_qr_blocked) and writes R, the
+//                 reflectors and the panel's T factor;
+//   k_qrs_update: one CTA per (job, 32 trailing columns): W = V^T A_slab,
+//                 Z = -T^T W, A_slab += V Z on the FP64 tensor pipe (DMMA),
+//                 V read straight from the factored panel in global memory / L2.
+// The trailing update -- 2 m l^2 of the 2 m l^2 QR flops -- is spread over the
+// whole GPU instead of running inside the job's one CTA, and no CTA holds
+// more than one panel in shared memory.
+template <int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_qrs_panel(const QrJob* __restrict__ jobs, int k0) {
+  extern __shared__ double Vs[];            // panel (rows x 16), column-major, ld = rows
+  __shared__ double T[kNbMax * kNbMax];
+  __shared__ double G[kNbMax * kNbMax];
+  __shared__ double red2[2 * 16 * kNbMax];
+  __shared__ double piv[2 * kNbMax];
+  __shared__ double stau[kNbMax];
+  const QrJob J = jobs[blockIdx.x];
+  const int m = J.m, n = J.n, lda = J.lda;
+  if (k0 >= n) return;
+  double* A = J.A;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = kThreads, NW = NT >> 5;
+  const int kb = min(kNbMax, n - k0);
+  const int rows = m - k0;
+  const int ldp = rows;
+  {
+    const double* Ap = A + k0 + (int64_t)k0 * lda;
+    for (int j = 0; j < kb; j++)
+      for (int i = tid; i < rows; i += NT) Vs[i + (int64_t)j * ldp] = Ap[i + (int64_t)j * lda];
+  }
+  __syncthreads();
+  for (int j = 0; j < kb; j++) {
+    const int nc = kb - j;
+    const double* x = Vs + (int64_t)j * ldp;
+    double part[kNbMax];
+#pragma unroll
+    for (int q = 0; q < kNbMax; q++) part[q] = 0.0;
+    const int i0 = tid > j ? tid : tid + ((j - tid) / NT + 1) * NT;
+    for (int i = i0; i < rows; i += NT) {
+      const double xi = x[i];
+#pragma unroll
+      for (int q = 0; q < kNbMax; q++)
+        if (q < nc) part[q] = fma(xi, Vs[i + (int64_t)(j + q) * ldp], part[q]);
+    }
+    double* rb = red2 + (j & 1) * (16 * kNbMax);
+    double* pv = piv + (j & 1) * kNbMax;
+    {
+      double h8[8], h4[4], h2[2];
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const double send = b4 ? part[q] : part[q + 8];
+        h8[q] = (b4 ? part[q + 8] : part[q]) + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const double send = b3 ? h8[q] : h8[q + 4];
+        h4[q] = (b3 ? h8[q + 4] : h8[q]) + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const double send = b2 ? h4[q] : h4[q + 2];
+        h2[q] = (b2 ? h4[q + 2] : h4[q]) + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      const double send = b1 ? h2[0] : h2[1];
+      double h1 = (b1 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
+      h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+      const int slot = (b4 ? 8 : 0) + (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+      if ((lane & 1) == 0 && slot < nc) rb[warp * kNbMax + slot] = h1;
+    }
+    if (tid == j % NT) {
+#pragma unroll
+      for (int q = 0; q < kNbMax; q++)
+        if (q < nc) pv[q] = Vs[j + (int64_t)(j + q) * ldp];
+    }
+    __syncthreads();
+    double tq = 0.0;
+    if (lane < nc) {
+      double r16[16];
+#pragma unroll
+      for (int w = 0; w < 16; w++) r16[w] = w < NW ? rb[w * kNbMax + lane] : 0.0;
+#pragma unroll
+      for (int w = 0; w < 16; w++) tq += r16[w];
+    }
+    const double xn2 = __shfl_sync(0xffffffffu, tq, 0);
+    const double alpha = pv[0];
+    double t = 0.0, sc = 0.0, beta = alpha;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      t = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    double dq = 0.0;
+    if (lane >= 1 && lane < nc) dq = (pv[lane] + sc * tq) * t;
+    double d[kNbMax];
+#pragma unroll
+    for (int q = 1; q < kNbMax; q++) d[q] = __shfl_sync(0xffffffffu, dq, q);
+    if (tid == 0) { J.tau[k0 + j] = t; stau[j] = t; }
+    if (tid == j % NT) {
+      Vs[j + (int64_t)j * ldp] = beta;
+#pragma unroll
+      for (int q = 1; q < kNbMax; q++)
+        if (q < nc) Vs[j + (int64_t)(j + q) * ldp] = pv[q] - d[q];
+    }
+    if (t != 0.0)
+      for (int i = i0; i < rows; i += NT) {
+        const double vi = Vs[i + (int64_t)j * ldp] * sc;
+        Vs[i + (int64_t)j * ldp] = vi;
+#pragma unroll
+        for (int q = 1; q < kNbMax; q++)
+          if (q < nc) Vs[i + (int64_t)(j + q) * ldp] -= d[q] * vi;
+      }
+  }
+  __syncthreads();
+  {
+    double* Ap = A + k0 + (int64_t)k0 * lda;
+    for (int j = 0; j < kb; j++)
+      for (int i = tid; i < rows; i += NT) Ap[i + (int64_t)j * lda] = Vs[i + (int64_t)j * ldp];
+  }
+  __syncthreads();
+  for (int e = tid; e < kb * kb; e += NT) {
+    const int i = e % kb, j = e / kb;
+    if (i < j) Vs[i + (int64_t)j * ldp] = 0.0;
+    else if (i == j) Vs[i + (int64_t)j * ldp] = 1.0;
+  }
+  __syncthreads();
+  // T (dlarft, forward columnwise) as in k_qr_blocked
+  for (int pr = warp; pr < kb * kb; pr += NW) {
+    const int a = pr % kb, b = pr / kb;
+    if (a >= b) continue;
+    const double* va = Vs + (int64_t)a * ldp;
+    const double* vb = Vs + (int64_t)b * ldp;
+    double d = 0.0;
+    for (int i = b + lane; i < rows; i += 32) d = fma(va[i], vb[i], d);
+    d = wsum(d);
+    if (lane == 0) G[a + b * kNbMax] = d;
+  }
+  __syncthreads();
+  if (warp == 0 && lane < kb) {
+    const int r = lane;
+    for (int i = r; i < kb; i++) {
+      if (i == r) { T[r + r * kNbMax] = stau[r]; continue; }
+      double s = 0.0;
+      for (int q = r; q < i; q++) s = fma(T[r + q * kNbMax], G[q + i * kNbMax], s);
+      T[r + i * kNbMax] = -stau[i] * s;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kNbMax * kNbMax; e += NT) {
+    const int r = e & 15, q = e >> 4;
+    J.T[(int64_t)(k0 / kNbMax) * kNbMax * kNbMax + e] = (r <= q && q < kb) ? T[e] : 0.0;
+  }
+}
+
+// Trailing update of step k0 for 32 trailing columns of one job (blockIdx.y =
+// job, blockIdx.x = column slab).  256 threads = 8 warps; rows are dealt to
+// the warps 4 (phase 1) / 8 (phase 2) at a time.
+__global__ void __launch_bounds__(256, 3) k_qrs_update(const QrJob* __restrict__ jobs, int k0) {
+  __shared__ double Wp[8 * 512];   // per-warp partial W (16 x 32), then W itself in Wp[0..512)
+  __shared__ double Zn[512];       // -T^T W (16 x 32)
+  __shared__ double Ts[256];
+  const QrJob J = jobs[blockIdx.y];
+  const int n = J.n;
+  if (k0 >= n) return;
+  const int kb = min(kNbMax, n - k0);
+  const int ncol = n - k0 - kb;
+  const int cb = blockIdx.x * 32;
+  if (cb >= ncol) return;
+  const int wcb = min(32, ncol - cb);
+  const int lda = J.lda, rows = J.m - k0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  const double* Vg = J.A + k0 + (int64_t)k0 * lda;            // panel: v(i, q), implicit unit diagonal
+  double* At = J.A + k0 + (int64_t)(k0 + kb + cb) * lda;      // slab (rows x wcb)
+  Ts[tid] = J.T[(int64_t)(k0 / kNbMax) * 256 + tid];
+  // ---- phase 1: partial W = V^T A over this warp's rows
+  double d[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) d[a][b][0] = d[a][b][1] = 0.0;
+  const double* vq0 = Vg + (int64_t)min(lr, kb - 1) * lda;
+  const double* vq1 = Vg + (int64_t)min(8 + lr, kb - 1) * lda;
+  const bool q0ok = lr < kb, q1ok = 8 + lr < kb;
+  const double* ac[4];
+  bool cok[4];
+#pragma unroll
+  for (int ct = 0; ct < 4; ct++) {
+    const int jc = ct * 8 + lr;
+    cok[ct] = jc < wcb;
+    ac[ct] = At + (int64_t)(cok[ct] ? jc : 0) * lda;
+  }
+  // the first 16 rows carry the unit triangle of V: masked loads
+  for (int i0 = 4 * warp; i0 < rows; i0 += 32) {
+    const int i = i0 + lk;
+    const bool iok = i < rows;
+    double a0 = 0.0, a1 = 0.0;
+    if (i0 >= kNbMax) {
+      if (iok) { a0 = q0ok ? vq0[i] : 0.0; a1 = q1ok ? vq1[i] : 0.0; }
+    } else if (iok) {
+      const int qa = lr, qb = 8 + lr;
+      a0 = !q0ok ? 0.0 : (i > qa ? vq0[i] : (i == qa ? 1.0 : 0.0));
+      a1 = !q1ok ? 0.0 : (i > qb ? vq1[i] : (i == qb ? 1.0 : 0.0));
+    }
+    double b[4];
+#pragma unroll
+    for (int ct = 0; ct < 4; ct++) b[ct] = (iok && cok[ct]) ? ac[ct][i] : 0.0;
+#pragma unroll
+    for (int ct = 0; ct < 4; ct++) {
+      dmma_qr(d[0][ct], a0, b[ct]);
+      dmma_qr(d[1][ct], a1, b[ct]);
+    }
+  }
+  {
+    double* w = Wp + warp * 512;
+#pragma unroll
+    for (int qt = 0; qt < 2; qt++)
+#pragma unroll
+      for (int ct = 0; ct < 4; ct++) {
+        const int q = qt * 8 + lr;
+        w[q + (ct * 8 + 2 * lk) * 16] = d[qt][ct][0];
+        w[q + (ct * 8 + 2 * lk + 1) * 16] = d[qt][ct][1];
+      }
+  }
+  __syncthreads();
+  for (int e = tid; e < 512; e += 256) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) sacc += Wp[w * 512 + e];
+    Zn[e] = sacc;   // W, staged in Zn
+  }
+  __syncthreads();
+  for (int e = tid; e < 512; e += 256) {   // Z(q, j) = -sum_{r <= q} T(r, q) W(r, j)
+    const int q = e & 15, j = e >> 4;
+    double sacc = 0.0;
+    if (q < kb)
+      for (int r = 0; r <= q; r++) sacc = fma(Ts[r + q * kNbMax], Zn[r + j * 16], sacc);
+    Wp[e] = -sacc;
+  }
+  __syncthreads();
+  // ---- phase 2: A_slab += V Z, 8-row tiles round-robin over the warps
+  {
+    double bz[4][4];
+#pragma unroll
+    for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+      for (int ks = 0; ks < 4; ks++) bz[ct][ks] = Wp[(ks * 4 + lk) + (ct * 8 + lr) * 16];
+    const int nrt = (rows + 7) >> 3;
+    for (int rt = warp; rt < nrt; rt += 8) {
+      const int i = rt * 8 + lr;
+      const bool iok = i < rows;
+      double a[4];
+#pragma unroll
+      for (int ks = 0; ks < 4; ks++) {
+        const int q = ks * 4 + lk;
+        double v = 0.0;
+        if (q < kb && iok) v = (rt >= 2 || i > q) ? Vg[i + (int64_t)q * lda] : (i == q ? 1.0 : 0.0);
+        a[ks] = v;
+      }
+      double c2[4][2];
+#pragma unroll
+      for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int j = ct * 8 + 2 * lk + h;
+          c2[ct][h] = (iok && j < wcb) ? At[i + (int64_t)j * lda] : 0.0;
+        }
+#pragma unroll
+      for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+        for (int ks = 0; ks < 4; ks++) dmma_qr(c2[ct], a[ks], bz[ct][ks]);
+#pragma unroll
+      for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int j = ct * 8 + 2 * lk + h;
+          if (iok && j < wcb) At[i + (int64_t)j * lda] = c2[ct][h];
+        }
+    }
+  }
+}
+
+// jobs sorted by n (columns) descending; ncols[i] = n of job i (host copy).
+// All jobs need m * 16 <= 24 K doubles and a T buffer.
+void launch_qr_stepped(const QrJob* d_jobs, const int* ncols, int njobs, int max_m, cudaStream_t st) {
+  if (njobs <= 0) return;
+  const size_t smem = (size_t)max_m * kNbMax * sizeof(double);
+  const bool big = max_m > 768;
+  if (big) ensure_smem_attr((const void*)k_qrs_panel<512, 1>, 24 * 1024 * 8);
+  else ensure_smem_attr((const void*)k_qrs_panel<256, 2>, 12 * 1024 * 8);
+  int active = njobs;
+  for (int k0 = 0; k0 < ncols[0]; k0 += kNbMax) {
+    while (active > 0 && ncols[active - 1] <= k0) active--;
+    if (active == 0) break;
+    count_launch();
+    if (big) k_qrs_panel<512, 1><<<active, 512, smem, st>>>(d_jobs, k0);
+    else k_qrs_panel<256, 2><<<active, 256, smem, st>>>(d_jobs, k0);
+    const int ncol = ncols[0] - k0 - kNbMax;
+    if (ncol > 0) {
+      int act2 = active;
+      while (act2 > 0 && ncols[act2 - 1] <= k0 + kNbMax) act2--;
+      if (act2 > 0) {
+        count_launch();
+        k_qrs_update<<<dim3((ncol + 31) / 32, act2), 256, 0, st>>>(d_jobs, k0);
+      }
+    }
+  }
+}
+
 template <int kThreads, int kMinBlocks>
 static void launch_qr_variant(const QrJob* d_jobs, int njobs, int cap, int rb, cudaStream_t st) {
   static const int dm = [] { const char* e = std::getenv("HM_QR_DMMA"); return e ? std::atoi(e) : 1; }();

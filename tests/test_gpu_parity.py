@@ -109,6 +109,37 @@ def test_trunc_kernel_tall(hm, ctx):
         _assert_one_orthonormal(U, V, k)
 
 
+def test_trunc_kernel_stepped_qr(hm, ctx):
+    """Batches large enough (>= 32 QR jobs per shared-memory bucket) to take
+    the stepped QR (k_qrs_panel + k_qrs_update, qr.cu): ragged column counts
+    (not multiples of 16), every bucket (<= 384 / 768 / 1536 rows), jobs that
+    run out of columns at different panel steps -- closed form + oracle TRUNC."""
+    eps = 1e-6
+    rng = np.random.default_rng(77)
+    shapes = []
+    for i in range(40):
+        m = 200 + (i * 7) % 180
+        shapes.append((m, m - 11, 10 + i % 25, i % 4))
+        m = 500 + (i * 13) % 260
+        shapes.append((m, m - 30, 20 + (i * 3) % 70, i % 3))
+        m = 900 + (i * 29) % 600
+        shapes.append((m, 800 + (i * 17) % 500, 30 + (i * 5) % 120, i % 5))
+    stacks, svals = [], []
+    for m, n, q, junk in shapes:
+        s = 10.0 ** (-0.17 * np.arange(q))
+        A, B = _prescribed(rng, m, n, s, junk)
+        stacks.append((A, B))
+        svals.append(s)
+    out, ranks, _ = hm.test_trunc_batched(ctx, stacks, eps)
+    for (A, B), (U, V), k, s in zip(stacks, out, ranks, svals):
+        kk = next(j for j in range(len(s) + 1) if np.sum(s[j:] ** 2) <= eps ** 2 * np.sum(s ** 2))
+        assert k == kk
+        _assert_one_orthonormal(U, V, k)
+        Uo, Vo = trunc(A, B, TruncCtx(eps))
+        assert Uo.shape[1] == k
+        assert lowrank_diff(U, V, Uo, Vo) <= TOL * lowrank_norm(Uo, Vo) + 1e-14
+
+
 def test_trunc_kernel_degenerate(hm, ctx):
     rng = np.random.default_rng(3)
     R = (rng.standard_normal((30, 4)), rng.standard_normal((25, 4)))
