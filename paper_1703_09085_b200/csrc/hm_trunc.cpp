@@ -200,8 +200,29 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   auto stepped_ok = [&](int njobs) { return qr_stepped && njobs >= qr_stepped_min; };
   // bucket b <= 2 (m <= 1536, every job has a T buffer): stepped QR for batches,
   // the one-CTA-per-job kernel for the few-job (latency-bound) case
+  // buckets 0 / 1 (m <= 768): register-panel QR (qr_reg.cu), one launch per row
+  // class (the class fixes threads and rows per thread); HM_QR_REG=0: the
+  // shared-memory-panel kernels
+  static const int qr_reg = [] { const char* e = std::getenv("HM_QR_REG"); return e ? std::atoi(e) : 1; }();
+  auto qr_class = [](int m) { return m <= 128 ? 0 : (m <= 256 ? 1 : (m <= 384 ? 2 : (m <= 512 ? 3 : 4))); };
+  // order of a bucket's jobs before the upload
+  auto prep_bucket = [&](std::vector<QrJob>& v, int b) {
+    if (b <= 1 && qr_reg)
+      std::stable_sort(v.begin(), v.end(), [&](const QrJob& x, const QrJob& y) { return qr_class(x.m) < qr_class(y.m); });
+    else if (b <= 2 && stepped_ok((int)v.size()))
+      std::stable_sort(v.begin(), v.end(), [](const QrJob& x, const QrJob& y) { return x.n > y.n; });
+  };
   auto launch_bucket = [&](const std::vector<QrJob>& v, const QrJob* dv, int b, int cap, cudaStream_t s) {
-    if (b <= 2 && stepped_ok((int)v.size())) {
+    if (b <= 1 && qr_reg) {
+      for (size_t i0 = 0; i0 < v.size();) {
+        const int cl = qr_class(v[i0].m);
+        size_t i1 = i0;
+        int mm = 0;
+        while (i1 < v.size() && qr_class(v[i1].m) == cl) { mm = std::max(mm, v[i1].m); i1++; }
+        launch_qr_reg(dv + i0, (int)(i1 - i0), mm, s);
+        i0 = i1;
+      }
+    } else if (b <= 2 && stepped_ok((int)v.size())) {
       std::vector<int> nc(v.size());
       int mm = 0;
       for (size_t i = 0; i < v.size(); i++) { nc[i] = v[i].n; mm = std::max(mm, v[i].m); }
@@ -221,9 +242,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     }
     // stepped QR (qr.cu): jobs sorted by column count, so that every panel step
     // launches only the prefix of jobs that still has columns left
-    for (int b = 0; b < 3; b++)
-      if (stepped_ok((int)qbk[b].size()))
-        std::stable_sort(qbk[b].begin(), qbk[b].end(), [](const QrJob& x, const QrJob& y) { return x.n > y.n; });
+    for (int b = 0; b < 3; b++) prep_bucket(qbk[b], b);
     // uploads first (they are ordered on the main stream), then every bucket
     // on its own auxiliary stream: the buckets are independent problems
     const QrJob* dqs = qs.empty() ? nullptr : ar.upload(qs);
@@ -400,8 +419,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     ProfScope ps(c, PC_PREQR, 0, 0);
     for (int b = 0; b < 4; b++)
       if (!pq[b].empty()) {
-        if (b <= 2 && stepped_ok((int)pq[b].size()))
-          std::stable_sort(pq[b].begin(), pq[b].end(), [](const QrJob& x, const QrJob& y) { return x.n > y.n; });
+        prep_bucket(pq[b], b);
         launch_bucket(pq[b], ar.upload(pq[b]), b, pqcap[b], st);
       }
     HM_CHECK_LAUNCH();

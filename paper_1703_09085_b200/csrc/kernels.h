@@ -186,6 +186,9 @@ void launch_qr_blocked(const QrJob* d_jobs, int njobs, int cap, cudaStream_t st)
 // columns); jobs sorted by n descending, ncols = host copy of their n; every
 // job has a T buffer and m <= 1536 (max_m = the largest m).
 void launch_qr_stepped(const QrJob* d_jobs, const int* ncols, int njobs, int max_m, cudaStream_t st);   // rows <= 24576
+// Register-panel blocked QR (qr_reg.cu): every job n < m <= 768 (max_m = the
+// largest m); writes the compact-WY T factors when QrJob::T != nullptr.
+void launch_qr_reg(const QrJob* d_jobs, int njobs, int max_m, cudaStream_t st);
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);

@@ -41,19 +41,32 @@ static double drop_rel_host() {
 
 // diagnostics: -DHM_PHASE_TIMING prints per-phase SM cycles of CTA 0
 #ifdef HM_PHASE_TIMING
+// phases of CTA 0 are buffered and printed once at the end of the kernel (a
+// printf per phase would be charged to the next phase)
+__device__ long long g_ph_cyc[32];
+__device__ const char* g_ph_name[32];
+__device__ int g_ph_n;
 #define PHASE(name)                                                                        \
   do {                                                                                     \
     __syncthreads();                                                                       \
     if (blockIdx.x == 0 && threadIdx.x == 0) {                                             \
       const long long t_ = clock64();                                                      \
-      printf("[phase] %-10s %8lld cycles\n", name, t_ - ph_t0);                            \
-      ph_t0 = t_;                                                                          \
+      if (g_ph_n < 32) { g_ph_cyc[g_ph_n] = t_ - ph_t0; g_ph_name[g_ph_n++] = name; }      \
+      ph_t0 = clock64();                                                                   \
     }                                                                                      \
   } while (0)
 #define PHASE_INIT long long ph_t0 = clock64()
+#define PHASE_FLUSH                                                                        \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                             \
+      for (int i_ = 0; i_ < g_ph_n; i_++) printf("[phase] %-10s %8lld cycles\n", g_ph_name[i_], g_ph_cyc[i_]); \
+      g_ph_n = 0;                                                                          \
+    }                                                                                      \
+  } while (0)
 #else
 #define PHASE(name) do {} while (0)
 #define PHASE_INIT do {} while (0)
+#define PHASE_FLUSH do {} while (0)
 #endif
 // fused TRUNC: no stack QR when m, n <= this (0 = always QR the thin side;
 // measured: skipping it does not shorten the H-LR critical path)
@@ -444,9 +457,6 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
                        : (c <= 128 ? jacobi_sweeps<32, 4>(X, ldx, c, rt, tol2, delta2)
                                    : jacobi_sweeps<32, 8>(X, ldx, c, rt, tol2, delta2));
   PHASE("jacobi");
-#ifdef HM_PHASE_TIMING
-  if (blockIdx.x == 0 && tid == 0) printf("[phase] L=%d c=%d rt=%d sweeps=%d G=%d\n", L, c, rt, sweep, G);
-#endif
   if (tid == 0 && J.nsweep) *J.nsweep = sweep + 1000 * rt;
   // ---------------------------------------------------------------- 3. rank
   for (int base = warp * gpwq; base < rt; base += NW * gpwq) {
@@ -600,6 +610,9 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
     }
   }
   PHASE("output");
+#ifdef HM_PHASE_TIMING
+  if (blockIdx.x == 0 && tid == 0) printf("[phase] L=%d c=%d rt=%d sweeps=%d G=%d\n", L, c, rt, sweep, G);
+#endif
 }
 
 __global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, double eps, double drop_rel, int cap) {
@@ -629,6 +642,7 @@ __global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, do
     C[i + (int64_t)j * ldc] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
   }
   svd_core(J, eps, drop_rel, tr, L, c, C, ldc, X, tau, nrm, sig, perm, order);
+  PHASE_FLUSH;
 }
 
 // In-place Householder QR (dgeqr2 layout) of a rows x cols panel in shared
@@ -875,6 +889,7 @@ __global__ void __launch_bounds__(512) k_trunc_small(const TruncSmallJob* __rest
   if (qa) apply_q_smem(sA, lda, tA, m, l, J.Aout, m, k);
   if (qb) apply_q_smem(sB, ldb, tB, n, l, J.Bout, n, k);
   PHASE("apply_q");
+  PHASE_FLUSH;
 }
 
 void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
@@ -913,6 +928,9 @@ void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream
   static const int tg = [] { const char* e = std::getenv("HM_SVDG_THREADS"); return e ? std::atoi(e) : 512; }();
   int threads = (cap == 0 || cap > 8 * 1024 || njobs < 296) ? 512 : 256;
   if (cap == 0) threads = tg;   // global workspace: no shared-memory limit on CTAs per SM
+  // latency mode (few matrices): threads per CTA, HM_SVD_LAT (0 = the default above)
+  static const int tlat = [] { const char* e = std::getenv("HM_SVD_LAT"); return e ? std::atoi(e) : 0; }();
+  if (tlat > 0 && njobs < 296) threads = tlat;
   count_launch();
   k_svd<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, drop_rel_host(), cap);
 }

@@ -140,6 +140,36 @@ def test_trunc_kernel_stepped_qr(hm, ctx):
         assert lowrank_diff(U, V, Uo, Vo) <= TOL * lowrank_norm(Uo, Vo) + 1e-14
 
 
+def test_trunc_kernel_reg_qr(hm, ctx):
+    """Stacks whose QR jobs cover the five row classes of the register-panel
+    QR (qr_reg.cu: <= 128 / 256 / 384 / 512 / 768 rows), ragged column counts
+    (last panel < 16 columns, l = 17 .. 133), few and many jobs, TSQR chunk
+    stacks (2 l .. 5 l rows) and pre-QR of M -- closed form + oracle TRUNC."""
+    eps = 1e-6
+    rng = np.random.default_rng(2718)
+    shapes = []
+    for i in range(12):
+        shapes.append((130 + 19 * i, 125 + 17 * i, 17 + 9 * i, i % 3))        # classes 1-2, both sides QR'd
+        shapes.append((400 + 30 * i, 90 + 5 * i, 33 + 8 * i, i % 2))          # classes 3-4 one-sided
+        shapes.append((1600 + 400 * i, 300 + 20 * i, 20 + 6 * i, 1))          # TSQR: chunk stacks of 2-7 l rows
+    shapes += [(768, 767, 133, 0), (385, 384, 100, 1), (257, 256, 31, 2), (129, 128, 47, 0), (513, 512, 64, 1)]
+    stacks, svals = [], []
+    for m, n, q, junk in shapes:
+        s = 10.0 ** (-0.21 * np.arange(q))
+        A, B = _prescribed(rng, m, n, s, junk)
+        stacks.append((A, B))
+        svals.append(s)
+    for batch in (stacks, stacks[:3]):
+        out, ranks, _ = hm.test_trunc_batched(ctx, batch, eps)
+        for (A, B), (U, V), k, s in zip(batch, out, ranks, svals):
+            kk = next(j for j in range(len(s) + 1) if np.sum(s[j:] ** 2) <= eps ** 2 * np.sum(s ** 2))
+            assert k == kk
+            _assert_one_orthonormal(U, V, k)
+            Uo, Vo = trunc(A, B, TruncCtx(eps))
+            assert Uo.shape[1] == k
+            assert lowrank_diff(U, V, Uo, Vo) <= TOL * lowrank_norm(Uo, Vo) + 1e-14
+
+
 def test_trunc_kernel_degenerate(hm, ctx):
     rng = np.random.default_rng(3)
     R = (rng.standard_normal((30, 4)), rng.standard_normal((25, 4)))
