@@ -523,7 +523,21 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       for (const ApplyQJob& j : v) m = std::max(m, j.c);
       return m;
     };
-    if (!aq1.empty()) launch_applyq(ar.upload(aq1), (int)aq1.size(), cmax(aq1), st);
+    // jobs with compact-WY T factors and <= 1536 rows: panel-wise DMMA kernel
+    // (all columns of X per pass over a panel); the others: one warp per column
+    static const int aq_dmma = [] { const char* e = std::getenv("HM_APPLYQ_DMMA"); return e ? std::atoi(e) : 1; }();
+    auto launch_applyq_split = [&](std::vector<ApplyQJob>& v) {
+      if (v.empty()) return;
+      std::vector<ApplyQJob> fast, slow;
+      int mm = 0;
+      for (const ApplyQJob& j : v) {
+        if (aq_dmma && j.T && j.m <= 1536) { fast.push_back(j); mm = std::max(mm, j.m); }
+        else slow.push_back(j);
+      }
+      if (!fast.empty()) launch_applyq_dmma(ar.upload(fast), (int)fast.size(), cmax(fast), mm, st);
+      if (!slow.empty()) launch_applyq(ar.upload(slow), (int)slow.size(), cmax(slow), st);
+    };
+    launch_applyq_split(aq1);
     if (!ts.empty()) {
       // TSQR: X_top[0:l] = output[0:l] (the SVD's factor), zeros below; then per
       // level (top down) X_j <- blockdiag(Q_j) X_j and scatter its l-row blocks
@@ -556,11 +570,11 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
             add_copy(cj, tiles, D.X + r0, D.ldx, U.X + (size_t)ch * P.l, U.ldx, P.l, P.kcap, 0);
           }
         }
-        launch_applyq(ar.upload(tq), (int)tq.size(), cmax(tq), st);
+        launch_applyq_split(tq);
         launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
       }
     }
-    if (!aq.empty()) launch_applyq(ar.upload(aq), (int)aq.size(), cmax(aq), st);
+    launch_applyq_split(aq);
     HM_CHECK_LAUNCH();
   }
 }

@@ -189,6 +189,8 @@ void launch_qr_stepped(const QrJob* d_jobs, const int* ncols, int njobs, int max
 // Register-panel blocked QR (qr_reg.cu): every job n < m <= 768 (max_m = the
 // largest m); writes the compact-WY T factors when QrJob::T != nullptr.
 void launch_qr_reg(const QrJob* d_jobs, int njobs, int max_m, cudaStream_t st);
+// Panel-wise apply-Q on the tensor pipe (qr_reg.cu): every job T != nullptr, m <= 1536.
+void launch_applyq_dmma(const ApplyQJob* d_jobs, int njobs, int cmax, int max_m, cudaStream_t st);
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);

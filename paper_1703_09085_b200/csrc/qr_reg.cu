@@ -33,6 +33,8 @@ __device__ __forceinline__ void dmma_r(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __host__ __device__ __forceinline__ int ld4mod16(int n) { return n + ((4 - (n & 15)) & 15); }
 }  // namespace
 
@@ -212,19 +214,22 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_qr_reg(const QrJob* __restr
       if (ga < gb) Wz[e] = (Wz[e] + Wz[256 + e]) + (Wz[512 + e] + Wz[768 + e]);
     }
     __syncthreads();
-    if (warp == 0 && lane < kNb) {   // lane r computes row r of T
+    if (warp == 0 && lane < kNb) {   // lane r computes row r of T, kept in registers
       const int r = lane;
+      double trow[kNb];
 #pragma unroll
       for (int i = 0; i < kNb; i++) {
         double v = 0.0;
-        if (i < kb && r <= i) {
-          if (i == r) v = stau[r];
-          else {
-            double s = 0.0;
-            for (int q = r; q < i; q++) s = fma(T[r + q * kNb], Wz[q + i * kNb], s);
-            v = -stau[i] * s;
+        if (i < kb) {   // uniform
+          double s0 = 0.0, s1 = 0.0;   // sum_{q < i} T(r, q) G(q, i)  (T(r, q) = 0 for q < r)
+#pragma unroll
+          for (int q = 0; q < i; q++) {
+            if (q & 1) s1 = fma(trow[q], Wz[q + i * kNb], s1);
+            else s0 = fma(trow[q], Wz[q + i * kNb], s0);
           }
+          v = r == i ? stau[i] : (r < i ? -stau[i] * (s0 + s1) : 0.0);
         }
+        trow[i] = v;
         T[r + i * kNb] = v;
       }
     }
@@ -245,15 +250,30 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_qr_reg(const QrJob* __restr
           const double* vq1 = vq0 + 8 * ldp;
           const double* ac = At + (int64_t)(cok ? c0 + lr : c0) * lda + lk;
           double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0}, e0[2] = {0.0, 0.0}, e1[2] = {0.0, 0.0};
+          // the warp's 8 columns are prefetched into L1 one 128-row chunk ahead
+          // (9 lines per column and chunk: 72 prefetches per warp)
+          const double* cbase = At + (int64_t)c0 * lda;
+          const int ncw = min(8, ncol - c0);
+          auto prefetch_chunk = [&](int r0) {
+            for (int idx = lane; idx < 72; idx += 32) {
+              const int pc = idx / 9, pr = r0 + (idx % 9) * 16;
+              if (pc < ncw && pr < rows) prefetch_l1(cbase + (int64_t)pc * lda + pr);
+            }
+          };
+          prefetch_chunk(0);
           int i0 = 0;
+          for (int ch = 0; ch + 8 <= rows; ch += 128) {
+            prefetch_chunk(ch + 128);
+            const int iend = min(ch + 128, rows);
 #pragma unroll 4
-          for (; i0 + 8 <= rows; i0 += 8) {
-            const double b0 = cok ? ac[i0] : 0.0;
-            const double b1 = cok ? ac[i0 + 4] : 0.0;
-            dmma_r(d0, vq0[i0], b0);
-            dmma_r(d1, vq1[i0], b0);
-            dmma_r(e0, vq0[i0 + 4], b1);
-            dmma_r(e1, vq1[i0 + 4], b1);
+            for (; i0 + 8 <= iend; i0 += 8) {
+              const double b0 = cok ? ac[i0] : 0.0;
+              const double b1 = cok ? ac[i0 + 4] : 0.0;
+              dmma_r(d0, vq0[i0], b0);
+              dmma_r(d1, vq1[i0], b0);
+              dmma_r(e0, vq0[i0 + 4], b1);
+              dmma_r(e1, vq1[i0 + 4], b1);
+            }
           }
           for (; i0 < rows; i0 += 4) {
             const double b0 = (cok && i0 + lk < rows) ? ac[i0] : 0.0;
@@ -296,6 +316,11 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_qr_reg(const QrJob* __restr
             bz[ct][ks] = (ct < nct && ct * 8 + lr < wcb) ? Wz[(ks * 4 + lk) + (ct * 8 + lr) * 16] : 0.0;
         const int nrt = (rows + 7) >> 3;
         for (int rt = warp; rt < nrt; rt += NW) {
+          {   // this warp's tile after next: one 64-byte segment per column
+            const int pi = (rt + 2 * NW) * 8;
+            if (pi < rows)
+              for (int pc = lane; pc < wcb; pc += 32) prefetch_l1(At + pi + (int64_t)(cb + pc) * lda);
+          }
           const int i = rt * 8 + lr;
           const bool iok = i < rows;
           double av[4];
@@ -354,6 +379,154 @@ void launch_qr_reg(const QrJob* d_jobs, int njobs, int max_m, cudaStream_t st) {
   else if (max_m <= 384) launch_one<128, 3, 2>(d_jobs, njobs, max_m, st);
   else if (max_m <= 512) launch_one<256, 2, 1>(d_jobs, njobs, max_m, st);
   else launch_one<256, 3, 1>(d_jobs, njobs, max_m, st);
+}
+
+}  // namespace hm
+
+namespace hm {
+
+// ---------------------------------------------------------------------------
+// X <- Q X, Q = H_0 ... H_{r-1} from a blocked QR with compact-WY T factors
+// (Q_p = I - V_p T_p V_p^T, last panel first), ALL columns of X per pass over
+// a panel: W = V_p^T X, Z = -T_p W, X += V_p Z on the FP64 tensor pipe, the
+// panel staged once in shared memory (k_applyq re-reads the whole V per
+// column of X: measured L2-bandwidth bound, 4.2 ms for 1184 factors of
+// 760 x 128 with 40 columns).  One CTA per (job, 64 columns of X); m <= 1536.
+__global__ void __launch_bounds__(256, 2) k_applyq_dmma(const ApplyQJob* __restrict__ jobs) {
+  constexpr int NT = 256, NW = 8, CB = 64;
+  extern __shared__ double smq[];
+  __shared__ double Ts[kNb * kNb];
+  const ApplyQJob J = jobs[blockIdx.x];
+  const int c = J.cdyn ? *J.cdyn : J.c;
+  const int cb = blockIdx.y * CB;
+  if (cb >= c) return;
+  const int wcb = min(CB, c - cb);
+  const int m = J.m, ldv = J.ldv, ldx = J.ldx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int ldp = ld4mod16(m);
+  double* Vs = smq;
+  double* Wz = smq + (int64_t)ldp * kNb;
+  for (int p = (J.r + kNb - 1) / kNb - 1; p >= 0; p--) {
+    const int j0 = p * kNb, kb = min(kNb, J.r - j0);
+    const int rows = m - j0;
+    // stage the panel: explicit V (unit diagonal, zeros above / beyond rows, kb)
+    {
+      const double* Vp = J.V + j0 + (int64_t)j0 * ldv;
+      // (read-only loads: all 16 of a row are in flight before the first store)
+      for (int li = tid; li < ldp; li += NT) {
+        double v[kNb];
+#pragma unroll
+        for (int q = 0; q < kNb; q++)
+          v[q] = (li < rows && q < kb && li > q) ? __ldg(Vp + li + (int64_t)q * ldv)
+                                                 : ((li == q && q < kb && li < rows) ? 1.0 : 0.0);
+#pragma unroll
+        for (int q = 0; q < kNb; q++) Vs[li + q * ldp] = v[q];
+      }
+      const double* Tp = J.T + 256 * p;
+      const int q = tid & 15, r = tid >> 4;   // T(q, r), upper triangular within kb
+      Ts[tid] = (q <= r && r < kb) ? __ldg(Tp + tid) : 0.0;
+    }
+    __syncthreads();
+    double* Xt = J.X + j0 + (int64_t)cb * ldx;   // rows j0.., columns cb..
+    // a. W = V^T X_blk: warp w owns columns 8 w .. 8 w + 7 of the block
+    {
+      const int c0 = 8 * warp;
+      if (c0 < wcb) {   // warp-uniform
+        const bool cok = c0 + lr < wcb;
+        const double* vq0 = Vs + lk + lr * ldp;
+        const double* vq1 = vq0 + 8 * ldp;
+        const double* xc = Xt + (int64_t)(cok ? c0 + lr : c0) * ldx + lk;
+        double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0}, e0[2] = {0.0, 0.0}, e1[2] = {0.0, 0.0};
+        int i0 = 0;
+#pragma unroll 4
+        for (; i0 + 8 <= rows; i0 += 8) {
+          const double b0 = cok ? xc[i0] : 0.0;
+          const double b1 = cok ? xc[i0 + 4] : 0.0;
+          dmma_r(d0, vq0[i0], b0);
+          dmma_r(d1, vq1[i0], b0);
+          dmma_r(e0, vq0[i0 + 4], b1);
+          dmma_r(e1, vq1[i0 + 4], b1);
+        }
+        for (; i0 < rows; i0 += 4) {
+          const double b0 = (cok && i0 + lk < rows) ? xc[i0] : 0.0;
+          dmma_r(d0, vq0[i0], b0);
+          dmma_r(d1, vq1[i0], b0);
+        }
+        double* w = Wz + c0 * 16;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          w[lr + (2 * lk + h) * 16] = d0[h] + e0[h];
+          w[8 + lr + (2 * lk + h) * 16] = d1[h] + e1[h];
+        }
+      }
+    }
+    __syncthreads();
+    // b. Z(q, j) = -sum_{r >= q} T(q, r) W(r, j), in place
+    if (tid < wcb) {
+      double* w = Wz + tid * 16;
+      double wr[kNb];
+#pragma unroll
+      for (int r = 0; r < kNb; r++) wr[r] = w[r];
+#pragma unroll
+      for (int q = 0; q < kNb; q++) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = q; r < kNb; r++) s = fma(Ts[q + r * kNb], wr[r], s);
+        w[q] = -s;
+      }
+    }
+    __syncthreads();
+    // c. X_blk += V Z: 8-row tiles round-robin over the warps
+    {
+      const int nct = (wcb + 7) >> 3;
+      double bz[NW][4];
+#pragma unroll
+      for (int ct = 0; ct < NW; ct++)
+#pragma unroll
+        for (int ks = 0; ks < 4; ks++)
+          bz[ct][ks] = (ct < nct && ct * 8 + lr < wcb) ? Wz[(ks * 4 + lk) + (ct * 8 + lr) * 16] : 0.0;
+      const int nrt = (rows + 7) >> 3;
+      for (int rt = warp; rt < nrt; rt += NW) {
+        const int i = rt * 8 + lr;
+        const bool iok = i < rows;
+        double av[4];
+#pragma unroll
+        for (int ks = 0; ks < 4; ks++) av[ks] = iok ? Vs[i + (ks * 4 + lk) * ldp] : 0.0;
+        double c2[NW][2];
+#pragma unroll
+        for (int ct = 0; ct < NW; ct++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int jj = ct * 8 + 2 * lk + h;
+            c2[ct][h] = (ct < nct && iok && jj < wcb) ? Xt[i + (int64_t)jj * ldx] : 0.0;
+          }
+#pragma unroll
+        for (int ct = 0; ct < NW; ct++)
+          if (ct < nct) {   // warp-uniform
+#pragma unroll
+            for (int ks = 0; ks < 4; ks++) dmma_r(c2[ct], av[ks], bz[ct][ks]);
+          }
+#pragma unroll
+        for (int ct = 0; ct < NW; ct++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int jj = ct * 8 + 2 * lk + h;
+            if (ct < nct && iok && jj < wcb) Xt[i + (int64_t)jj * ldx] = c2[ct][h];
+          }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// every job: T != nullptr and m <= 1536 (max_m = the largest m); cmax = host bound of the columns
+void launch_applyq_dmma(const ApplyQJob* d_jobs, int njobs, int cmax, int max_m, cudaStream_t st) {
+  if (njobs <= 0 || cmax <= 0) return;
+  count_launch();
+  ensure_smem_attr((const void*)k_applyq_dmma, (int)(((size_t)ld4mod16(1536) * kNb + 16 * 64) * sizeof(double)));
+  const size_t bytes = ((size_t)ld4mod16(max_m) * kNb + 16 * 64) * sizeof(double);
+  k_applyq_dmma<<<dim3(njobs, (cmax + 63) / 64), 256, bytes, st>>>(d_jobs);
 }
 
 }  // namespace hm

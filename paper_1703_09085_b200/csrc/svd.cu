@@ -78,6 +78,26 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
+// HM_SUBWARPS=0: every sequential phase on all warps of the CTA (A/B reference)
+__device__ int g_subwarps = 1;
+
+// Barrier among the first `nthreads` threads of the CTA (whole warps; hardware
+// barrier 1 -- __syncthreads is barrier 0): the sequential phases run on only
+// as many warps as they have independent columns / column pairs for, the other
+// warps skip to the next __syncthreads instead of issuing the loop overhead.
+__device__ __forceinline__ void sub_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ bool sub_sync_or(int nthreads, bool pred) {
+  int r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.s32 q, %2, 0;\n barrier.red.or.pred p, 1, %1, q;\n selp.s32 %0, 1, 0, p;\n}"
+      : "=r"(r)
+      : "r"(nthreads), "r"((int)pred)
+      : "memory");
+  return r != 0;
+}
+
 __device__ double bsum(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   v = wsum(v);
@@ -184,8 +204,9 @@ __device__ __forceinline__ void jacobi_rot(double al, double be, double ga, doub
 // its E elements of both columns in registers for the rotation (c <= E G).
 // Returns the number of sweeps.
 template <int G, int E>
-__device__ int jacobi_sweeps(double* X, int ldx, int c, int rt, double tol2, double delta2) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+__device__ int jacobi_sweeps(double* X, int ldx, int c, int rt, double tol2, double delta2, int NW) {
+  // called by the first NW warps of the CTA only (sub_sync)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int gpw = 32 / G;
   const int gl = lane & (G - 1);
   const int cp = rt + (rt & 1);
@@ -236,9 +257,9 @@ __device__ int jacobi_sweeps(double* X, int ldx, int c, int rt, double tol2, dou
           rot = 1;
         }
       }
-      __syncthreads();
+      sub_sync(NW * 32);
     }
-    if (!__syncthreads_or(rot)) break;
+    if (!sub_sync_or(NW * 32, rot)) break;
   }
   return sweep;
 }
@@ -343,14 +364,20 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   // beta / tau itself; groups of Gq lanes update one column each; the scaling
   // of the reflector x is deferred to the next step (x is read by all groups
   // during its own step).
+  // Only the warps that have a column group to update take part (named
+  // barrier); the others wait at the block barrier below.
+  __shared__ int s_rt;
   int rt = 0;
+  const int nwq = g_subwarps ? min(NW, max(1, (c * Gq + 31) >> 5)) : NW;
+  const int NTq = nwq * 32;
+  if (warp < nwq) {
   int pending = -1;
   double pbeta = 0.0, psc = 0.0, pt = 0.0;
   for (int j = 0; j < c && j < L; j++) {
     if (pending >= 0) {
       double* xp = C + (int64_t)pending * ldc;
       if (pt != 0.0)
-        for (int i = pending + 1 + tid; i < L; i += NT) xp[i] *= psc;
+        for (int i = pending + 1 + tid; i < L; i += NTq) xp[i] *= psc;
       if (tid == 0) xp[pending] = pbeta;
       pending = -1;
     }
@@ -369,17 +396,17 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
       s += __shfl_xor_sync(0xffffffffu, s, o);
     }
     if (!(s > delta2)) break;
-    __syncthreads();   // every warp has read nrm before it is swapped / updated
+    sub_sync(NTq);   // every warp has read nrm before it is swapped / updated
     if (piv != j) {
       double* a = C + (int64_t)j * ldc;
       double* b = C + (int64_t)piv * ldc;
-      for (int i = tid; i < L; i += NT) { const double t = a[i]; a[i] = b[i]; b[i] = t; }
+      for (int i = tid; i < L; i += NTq) { const double t = a[i]; a[i] = b[i]; b[i] = t; }
       if (tid == 0) {
         const double t = nrm[j]; nrm[j] = nrm[piv]; nrm[piv] = t;
         const double t2 = nrm2[j]; nrm2[j] = nrm2[piv]; nrm2[piv] = t2;
         const int pp = perm[j]; perm[j] = perm[piv]; perm[piv] = pp;
       }
-      __syncthreads();
+      sub_sync(NTq);
     }
     const double* x = C + (int64_t)j * ldc;
     const double alpha = x[j];
@@ -392,7 +419,7 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
     }
     if (tid == 0) tau[j] = t;
     const double tsc = t * sc;
-    for (int base = j + 1 + warp * gpwq; base < c; base += NW * gpwq) {
+    for (int base = j + 1 + warp * gpwq; base < c; base += nwq * gpwq) {
       const int col = base + lane / Gq;
       const bool act = col < c;
       double* y = C + (int64_t)(act ? col : j) * ldc;
@@ -416,17 +443,20 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
       __syncwarp();
       if (act && gq == 0) { y[j] = yj - d; nrm[col] = nn; nrm2[col] = nn2; }
     }
-    __syncthreads();
+    sub_sync(NTq);
     pending = j; pbeta = beta; psc = sc; pt = t;
     rt = j + 1;
   }
   if (pending >= 0) {
     double* xp = C + (int64_t)pending * ldc;
     if (pt != 0.0)
-      for (int i = pending + 1 + tid; i < L; i += NT) xp[i] *= psc;
+      for (int i = pending + 1 + tid; i < L; i += NTq) xp[i] *= psc;
     if (tid == 0) xp[pending] = pbeta;
   }
+  if (tid == 0) s_rt = rt;
+  }
   __syncthreads();
+  rt = s_rt;
   PHASE("qrcp");
   // X = R^T (c x rt, ld ldx)
   const int ldx = pad_ld(c);
@@ -443,19 +473,22 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   const double tol = 64.0 * kUs * sqrt((double)c);
   const double tol2 = tol * tol;
   const int cp = rt + (rt & 1);
-  // G lanes per pair: at least c / 8 (register slices), at most what keeps
-  // every pair of a round in flight at once (NT / G >= cp / 2), within 8..32
-  int G = 8;
-  while (G < 32 && 8 * G < c) G <<= 1;
-  while (G < 32 && (NT / (2 * G)) >= (cp >> 1)) G <<= 1;
-  int sweep;
-  if (c > 8 * 32) sweep = jacobi_sweeps_stream(X, ldx, c, rt, tol2, delta2);
-  else if (G == 8) sweep = jacobi_sweeps<8, 8>(X, ldx, c, rt, tol2, delta2);
-  else if (G == 16) sweep = c <= 64 ? jacobi_sweeps<16, 4>(X, ldx, c, rt, tol2, delta2)
-                                    : jacobi_sweeps<16, 8>(X, ldx, c, rt, tol2, delta2);
-  else sweep = c <= 64 ? jacobi_sweeps<32, 2>(X, ldx, c, rt, tol2, delta2)
-                       : (c <= 128 ? jacobi_sweeps<32, 4>(X, ldx, c, rt, tol2, delta2)
-                                   : jacobi_sweeps<32, 8>(X, ldx, c, rt, tol2, delta2));
+  // G lanes per pair: the fewest that hold a column in register slices of 8
+  // (fewer shuffle levels, fewer warps issuing the loop), on the warps that
+  // have a pair of the round (named barrier); c > 256: streamed, all warps
+  const int G = c <= 64 ? 8 : (c <= 128 ? 16 : 32);
+  int sweep = 0;
+  if (c > 8 * 32) {
+    sweep = jacobi_sweeps_stream(X, ldx, c, rt, tol2, delta2);
+  } else {
+    const int nwj = g_subwarps ? min(NW, max(1, ((cp >> 1) * G + 31) >> 5)) : NW;
+    if (warp < nwj) {
+      if (G == 8) sweep = jacobi_sweeps<8, 8>(X, ldx, c, rt, tol2, delta2, nwj);
+      else if (G == 16) sweep = jacobi_sweeps<16, 8>(X, ldx, c, rt, tol2, delta2, nwj);
+      else sweep = jacobi_sweeps<32, 8>(X, ldx, c, rt, tol2, delta2, nwj);
+    }
+    __syncthreads();
+  }
   PHASE("jacobi");
   if (tid == 0 && J.nsweep) *J.nsweep = sweep + 1000 * rt;
   // ---------------------------------------------------------------- 3. rank
@@ -662,6 +695,10 @@ __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* ta
     if (col < cols && gl == 0) nrm2[col] = s2;
   }
   __syncthreads();
+  // the Householder steps run on the warps that have a column group (named barrier)
+  const int nwa = g_subwarps ? min(NW, max(1, (cols * G + 31) >> 5)) : NW;
+  const int NTa = nwa * 32;
+  if (warp < nwa) {
   int pending = -1;
   double pbeta = 0.0, psc = 0.0, pt = 0.0;
   const int steps = cols < rows ? cols : rows;
@@ -669,7 +706,7 @@ __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* ta
     if (pending >= 0) {
       double* xp = A + (int64_t)pending * lda;
       if (pt != 0.0)
-        for (int i = pending + 1 + tid; i < rows; i += NT) xp[i] *= psc;
+        for (int i = pending + 1 + tid; i < rows; i += NTa) xp[i] *= psc;
       if (tid == 0) xp[pending] = pbeta;
     }
     const double* x = A + (int64_t)j * lda;
@@ -682,7 +719,7 @@ __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* ta
     }
     if (tid == 0) tau[j] = t;
     const double tsc = t * sc;
-    for (int base = j + 1 + warp * gpw; base < cols; base += NW * gpw) {
+    for (int base = j + 1 + warp * gpw; base < cols; base += nwa * gpw) {
       const int col = base + lane / G;
       const bool act = col < cols;
       double* y = A + (int64_t)(act ? col : j) * lda;
@@ -704,14 +741,15 @@ __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* ta
       __syncwarp();
       if (act && gl == 0) { y[j] = yj - d; nrm2[col] = nn2; }
     }
-    __syncthreads();
+    sub_sync(NTa);
     pending = j; pbeta = beta; psc = sc; pt = t;
   }
   if (pending >= 0) {
     double* xp = A + (int64_t)pending * lda;
     if (pt != 0.0)
-      for (int i = pending + 1 + tid; i < rows; i += NT) xp[i] *= psc;
+      for (int i = pending + 1 + tid; i < rows; i += NTa) xp[i] *= psc;
     if (tid == 0) xp[pending] = pbeta;
+  }
   }
   __syncthreads();
 }
@@ -892,8 +930,21 @@ __global__ void __launch_bounds__(512) k_trunc_small(const TruncSmallJob* __rest
   PHASE_FLUSH;
 }
 
+// HM_SUBWARPS (diagnostics): copied to the device flag once, before the first launch
+static void subwarps_knob() {
+  static const bool done = [] {
+    if (const char* e = std::getenv("HM_SUBWARPS")) {
+      const int v = std::atoi(e);
+      cudaMemcpyToSymbol(g_subwarps, &v, sizeof(int));
+    }
+    return true;
+  }();
+  (void)done;
+}
+
 void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
   if (njobs <= 0) return;
+  subwarps_knob();
   ensure_smem_attr((const void*)k_trunc_small, 26 * 1024 * 8);
   count_launch();
   // small stacks: one warp per stack (barriers of a 1-warp CTA are nearly
@@ -923,6 +974,7 @@ int svd_smem_capacity() { return 26 * 1024; }
 
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
   if (njobs <= 0) return;
+  subwarps_knob();
   ensure_smem_attr((const void*)k_svd, svd_smem_capacity() * 8);
   if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
   static const int tg = [] { const char* e = std::getenv("HM_SVDG_THREADS"); return e ? std::atoi(e) : 512; }();
