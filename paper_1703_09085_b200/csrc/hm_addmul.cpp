@@ -15,10 +15,13 @@
 // exact stack once (DESIGN.md §3 R2), so the truncated matrices are the
 // oracle's (oracle/product.py S2).
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <numeric>
 #include <unordered_map>
@@ -221,9 +224,22 @@ struct Planner {
   // H-side product over the DFS leaves of block blk of X (yside = false) or Y
   // (yside = true); trans: out += coef H|_blk^T V instead of H|_blk V.
   struct EvalMeta { double cost; int blk, mat; };
-  std::vector<EvalMeta> emeta;   // host-side companions of the level's EvalJobs
+  // Host-side state of one eval batch under construction.  The level batch of
+  // hm_addmul is built by several host threads (run_level_enqueue): each
+  // worker points tl_emit at its own EmitState; everything else uses `em0`.
+  struct EmitState {
+    std::vector<EvalMeta> emeta;   // host-side companions of the batch's EvalJobs
+    std::vector<int2> erng;        // leaf-range table of split jobs (uploaded with the jobs)
+    std::vector<EvalJob> etail;    // chained continuation jobs (identity groups)
+    double fl = 0, by = 0;         // convention work emitted by a worker (folded in by the owner)
+  };
+  EmitState em0;
+  static EmitState*& tl_emit() {
+    static thread_local EmitState* p = nullptr;
+    return p;
+  }
+  EmitState& em() { return tl_emit() ? *tl_emit() : em0; }
   double split_thr = -1;         // > 0: fixed split threshold (hm_test_eval_batched)
-  std::vector<int2> erng;        // leaf-range table of split jobs (uploaded with the jobs)
 
   // H-side product over the DFS leaves of block blk of matrix mats[mi]
   void add_eval(std::vector<EvalJob>& ej, int mi, int blk, int trans, double coef, double* out,
@@ -252,12 +268,12 @@ struct Planner {
     const double smn = pn[e.leaf_end] - pn[e.leaf_begin];
     double fl = videntity ? 0.0 : 2.0 * w * smat;   // expansion: a copy, not arithmetic
     const double by = 8.0 * (smat + smn * w);
-    fl_eval += fl;
-    by_eval += by;
+    if (tl_emit()) { tl_emit()->fl += fl; tl_emit()->by += by; }
+    else { fl_eval += fl; by_eval += by; }
     e.nrng = 0;
     e.rng = nullptr;
     ej.push_back(e);
-    emeta.push_back(EvalMeta{by + fl, blk, mi});
+    em().emeta.push_back(EvalMeta{by + fl, blk, mi});
   }
 
   // Load balance of one eval batch: a job whose cost exceeds thr is cut into
@@ -268,6 +284,8 @@ struct Planner {
   // output entry run over the same leaves in the same order, so the result is
   // bit-identical to the unsplit job.
   void split_evals(std::vector<EvalJob>& ej) {
+    std::vector<EvalMeta>& emeta = em().emeta;
+    std::vector<int2>& erng = em().erng;
     erng.clear();
     double total = 0;
     for (auto& m : emeta) total += m.cost;
@@ -339,36 +357,53 @@ struct Planner {
     emeta.swap(mout);
   }
 
-  // Split (load balance), sort largest-first and launch one k_eval2 batch.
-  void launch_evals(std::vector<EvalJob>& ej, Arena& scratch, double fl, double by) {
-    if (ej.empty()) return;
+  // Split (load balance) and sort largest-first: host work only, on the active
+  // EmitState (a worker thread's or em0).  The range-table offsets and chain
+  // links of the sorted jobs stay relative until submit_evals.
+  std::vector<EvalJob> prepare_evals(std::vector<EvalJob>& ej) {
+    std::vector<EvalJob> sorted;
+    if (ej.empty()) return sorted;
     split_evals(ej);
+    const std::vector<EvalMeta>& emeta = em().emeta;
     std::vector<int> order(ej.size());
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return emeta[a].cost > emeta[b].cost; });
-    const int2* drng = erng.empty() ? nullptr : scratch.upload(erng);
-    EvalJob* dtail = nullptr;
-    if (!etail.empty()) {
-      dtail = static_cast<EvalJob*>(scratch.alloc_bytes(etail.size() * sizeof(EvalJob)));
-      for (auto& t : etail)
-        if (t.next) t.next = dtail + (reinterpret_cast<intptr_t>(t.next) - 1);
-      void* h = c->pinned(etail.size() * sizeof(EvalJob));
-      std::memcpy(h, etail.data(), etail.size() * sizeof(EvalJob));
-      HM_CUDA(cudaMemcpyAsync(dtail, h, etail.size() * sizeof(EvalJob), cudaMemcpyHostToDevice, c->stream));
-    }
-    std::vector<EvalJob> sorted(ej.size());
-    for (size_t i = 0; i < order.size(); i++) {
-      sorted[i] = ej[order[i]];
-      if (sorted[i].nrng > 0) sorted[i].rng = drng + reinterpret_cast<intptr_t>(sorted[i].rng);
-      if (sorted[i].next) sorted[i].next = dtail + (reinterpret_cast<intptr_t>(sorted[i].next) - 1);
-    }
-    emeta.clear();
-    erng.clear();
+    sorted.resize(ej.size());
+    for (size_t i = 0; i < order.size(); i++) sorted[i] = ej[order[i]];
+    em().emeta.clear();
     ej.clear();
-    etail.clear();
+    return sorted;
+  }
+
+  // Upload one prepared batch (jobs, range table, chained jobs of state E) and launch k_eval2.
+  void submit_evals(std::vector<EvalJob>& sorted, EmitState& E, Arena& scratch, double fl, double by) {
+    if (sorted.empty()) return;
+    const int2* drng = E.erng.empty() ? nullptr : scratch.upload(E.erng);
+    EvalJob* dtail = nullptr;
+    if (!E.etail.empty()) {
+      dtail = static_cast<EvalJob*>(scratch.alloc_bytes(E.etail.size() * sizeof(EvalJob)));
+      for (auto& t : E.etail)
+        if (t.next) t.next = dtail + (reinterpret_cast<intptr_t>(t.next) - 1);
+      void* h = c->pinned(E.etail.size() * sizeof(EvalJob));
+      std::memcpy(h, E.etail.data(), E.etail.size() * sizeof(EvalJob));
+      HM_CUDA(cudaMemcpyAsync(dtail, h, E.etail.size() * sizeof(EvalJob), cudaMemcpyHostToDevice, c->stream));
+    }
+    for (EvalJob& j : sorted) {
+      if (j.nrng > 0) j.rng = drng + reinterpret_cast<intptr_t>(j.rng);
+      if (j.next) j.next = dtail + (reinterpret_cast<intptr_t>(j.next) - 1);
+    }
+    E.erng.clear();
+    E.etail.clear();
     ProfScope ps(c, PC_EVAL, fl, by);
     launch_eval2(scratch.upload(sorted), (int)sorted.size(), c->stream);
     HM_CHECK_LAUNCH();
+    sorted.clear();
+  }
+
+  void launch_evals(std::vector<EvalJob>& ej, Arena& scratch, double fl, double by) {
+    if (ej.empty()) return;
+    std::vector<EvalJob> sorted = prepare_evals(ej);
+    submit_evals(sorted, em(), scratch, fl, by);
   }
 
   // Emit the A2 realisation of one evaluated term into stack columns [col, col+w).
@@ -457,8 +492,7 @@ struct Planner {
     return best;
   }
 
-  // chained continuation jobs of the current eval batch (identity groups)
-  std::vector<EvalJob> etail;
+  // chained continuation jobs of the current eval batch (identity groups): em().etail
   void add_eval_chained(std::vector<EvalJob>& ej, int& head, int& last, int mi, int blk, int trans,
                         double coef, double* out, int ldo, int w, const double* V, int ldv, int vtrans) {
     add_eval(ej, mi, blk, trans, coef, out, ldo, w, V, ldv, vtrans, 0);
@@ -467,6 +501,8 @@ struct Planner {
       last = -1;
       return;
     }
+    std::vector<EvalMeta>& emeta = em().emeta;
+    std::vector<EvalJob>& etail = em().etail;
     EvalJob e = ej.back();
     ej.pop_back();
     emeta[head].cost += emeta.back().cost;
@@ -557,19 +593,30 @@ struct Planner {
     if (lt.scratch) lt.scratch->release();
   }
 
-  LevelTail run_level_enqueue(std::vector<Node>& nodes) {
+  // plan_groups of every node of a level: independent of the ranks the previous
+  // level produces, so run_from computes it while that level runs on the device
+  std::vector<Groups> plan_level(const std::vector<Node>& nodes) const {
+    std::vector<Groups> g(nodes.size());
+    for (size_t i = 0; i < nodes.size(); i++) g[i] = plan_groups(nodes[i]);
+    return g;
+  }
+
+  LevelTail run_level_enqueue(std::vector<Node>& nodes, std::vector<Groups>* pre = nullptr) {
     double t0 = now_s();
     LevelTail lt;
     lt.scratch.reset(new Arena(c));
     Arena& scratch = *lt.scratch;
     std::vector<Stack> stacks;
-    std::vector<Groups> groups(nodes.size());
+    std::vector<Groups> groups;
+    if (pre && pre->size() == nodes.size()) groups.swap(*pre);
+    const bool planned = !groups.empty();
+    groups.resize(nodes.size());
     for (int i = 0; i < (int)nodes.size(); i++) {
       Node& nd = nodes[i];
       const int m = csize(nd.t), n = csize(nd.r);
       int kind = 0, l = 0;
       const int kb = nd.base >= 0 ? fps[nd.base].k : 0;
-      groups[i] = plan_groups(nd);
+      if (!planned) groups[i] = plan_groups(nd);
       const int wt = groups[i].width;
       if (!nd.pend.empty() || nd.force_split || nd.zt == ZS) {
         // (iv) split with pending products; (iii) P = 0 into a subdivided
@@ -604,44 +651,15 @@ struct Planner {
     }
     double t1 = now_s();
     t_a += t1 - t0;
-    std::vector<CopyJob> cj;
-    std::vector<EvalJob> ej;
-    {
-      size_t nterms = 0;
-      for (auto& s : stacks) nterms += nodes[s.node].terms.size();
-      cj.reserve(nterms + 2 * stacks.size());
-      ej.reserve(nterms);
-      emeta.reserve(nterms);
-    }
-    int64_t ctiles = 0;
-    double fl_eval0 = fl_eval, by_eval0 = by_eval;
-    // The level's copy and eval jobs are launched in chunks as they are built,
-    // so the device starts on the first chunk while the host builds the rest
-    // (copies and evaluations write disjoint stack columns: any order).
-    static const size_t kChunk = [] { const char* e = std::getenv("HM_JOB_CHUNK"); return e ? (size_t)std::atoll(e) : (size_t)1 << 16; }();
-    auto flush_copy = [&]() {
-      if (cj.empty()) return;
-      double cb = 0;
-      for (auto& j : cj) cb += 16.0 * j.rows * (j.identity ? 1 : j.cols);
-      std::vector<int> tmap((size_t)ctiles);
-      for (size_t j = 0; j < cj.size(); j++) {
-        const int64_t t1 = j + 1 < cj.size() ? cj[j + 1].tile0 : ctiles;
-        std::fill(tmap.begin() + cj[j].tile0, tmap.begin() + t1, (int)j);
-      }
-      ProfScope ps(c, PC_COPY, 0, cb);
-      const CopyJob* dj = scratch.upload(cj);
-      launch_copy_mapped(dj, (int)cj.size(), scratch.upload(tmap), ctiles, c->stream);
-      HM_CHECK_LAUNCH();
-      cj.clear();
-      ctiles = 0;
-    };
-    auto flush_eval = [&]() {
-      if (ej.empty()) return;
-      launch_evals(ej, scratch, fl_eval - fl_eval0, by_eval - by_eval0);
-      fl_eval0 = fl_eval;
-      by_eval0 = by_eval;
-    };
-    for (auto& s : stacks) {
+    // ---- copy and eval jobs of the level (copies and evaluations write disjoint
+    // stack columns: any launch order).  Large levels are cut into parts of
+    // about equal term count that several host threads build, split and sort
+    // (prepare_evals) while this thread uploads and launches the finished
+    // parts in order, so the device starts on part 0 while the rest is built;
+    // small levels are built here in chunks.
+    size_t nterms = 0;
+    for (auto& s : stacks) nterms += nodes[s.node].terms.size();
+    auto emit_stack = [&](Stack& s, std::vector<CopyJob>& cj, int64_t& ctiles, std::vector<EvalJob>& ej) {
       Node& nd = nodes[s.node];
       int col = 0;
       if (s.kind == 2) {
@@ -667,13 +685,115 @@ struct Planner {
         emit_term(nd.terms[ti], s.A, s.m, s.B, s.n, col, cj, ctiles, ej);
         col += nd.terms[ti].w;
       }
-      if (ej.size() >= kChunk) flush_eval();
-      if (cj.size() >= kChunk) flush_copy();
+    };
+    auto submit_copy = [&](std::vector<CopyJob>& cj, int64_t& ctiles) {
+      if (cj.empty()) return;
+      double cb = 0;
+      for (auto& j : cj) cb += 16.0 * j.rows * (j.identity ? 1 : j.cols);
+      std::vector<int> tmap((size_t)ctiles);
+      for (size_t j = 0; j < cj.size(); j++) {
+        const int64_t t1 = j + 1 < cj.size() ? cj[j + 1].tile0 : ctiles;
+        std::fill(tmap.begin() + cj[j].tile0, tmap.begin() + t1, (int)j);
+      }
+      ProfScope ps(c, PC_COPY, 0, cb);
+      const CopyJob* dj = scratch.upload(cj);
+      launch_copy_mapped(dj, (int)cj.size(), scratch.upload(tmap), ctiles, c->stream);
+      HM_CHECK_LAUNCH();
+      cj.clear();
+      ctiles = 0;
+    };
+    static const int host_threads = [] {
+      if (const char* e = std::getenv("HM_HOST_THREADS")) return std::max(1, std::atoi(e));
+      const unsigned hw = std::thread::hardware_concurrency();
+      return (int)std::min(8u, std::max(1u, hw / 2));
+    }();
+    double t2 = t1;
+    if (host_threads > 1 && nterms >= 20000) {
+      struct Part {
+        size_t s0 = 0, s1 = 0;
+        std::vector<CopyJob> cj;
+        int64_t ctiles = 0;
+        std::vector<EvalJob> ej, sorted;
+        EmitState es;
+        std::atomic<int> ready{0};
+      };
+      const int np = host_threads * 6;
+      std::vector<Part> parts(np);
+      {
+        size_t si = 0, acc = 0;
+        for (int p = 0; p < np; p++) {
+          parts[p].s0 = si;
+          const size_t target = nterms * (size_t)(p + 1) / np;
+          while (si < stacks.size() && (acc < target || p == np - 1)) acc += nodes[stacks[si++].node].terms.size() + 1;
+          parts[p].s1 = si;
+        }
+        parts[np - 1].s1 = stacks.size();
+      }
+      std::atomic<int> next{0};
+      std::atomic<bool> failed{false};
+      std::exception_ptr eptr;
+      auto worker = [&]() {
+        for (;;) {
+          const int p = next.fetch_add(1);
+          if (p >= np) break;
+          Part& P = parts[p];
+          try {
+            tl_emit() = &P.es;
+            for (size_t i = P.s0; i < P.s1; i++) emit_stack(stacks[i], P.cj, P.ctiles, P.ej);
+            P.sorted = prepare_evals(P.ej);
+          } catch (...) {
+            failed = true;
+          }
+          tl_emit() = nullptr;
+          P.ready.store(1, std::memory_order_release);
+        }
+      };
+      std::vector<std::thread> pool;
+      for (int t = 0; t < host_threads; t++) pool.emplace_back(worker);
+      for (int p = 0; p < np; p++) {
+        Part& P = parts[p];
+        while (!P.ready.load(std::memory_order_acquire)) std::this_thread::yield();
+        if (failed) continue;
+        try {
+          submit_copy(P.cj, P.ctiles);
+          fl_eval += P.es.fl;
+          by_eval += P.es.by;
+          submit_evals(P.sorted, P.es, scratch, P.es.fl, P.es.by);
+        } catch (...) {   // join the workers before the error leaves this frame
+          failed = true;
+          eptr = std::current_exception();
+        }
+      }
+      for (auto& th : pool) th.join();
+      if (eptr) std::rethrow_exception(eptr);
+      if (failed) throw Error(HM_ESTRUCT, "internal: job emission failed");
+      t2 = now_s();
+      t_b += t2 - t1;
+    } else {
+      std::vector<CopyJob> cj;
+      std::vector<EvalJob> ej;
+      cj.reserve(nterms + 2 * stacks.size());
+      ej.reserve(nterms);
+      em0.emeta.reserve(nterms);
+      int64_t ctiles = 0;
+      double fl_eval0 = fl_eval, by_eval0 = by_eval;
+      static const size_t kChunk = [] { const char* e = std::getenv("HM_JOB_CHUNK"); return e ? (size_t)std::atoll(e) : (size_t)1 << 16; }();
+      auto flush_eval = [&]() {
+        if (ej.empty()) return;
+        launch_evals(ej, scratch, fl_eval - fl_eval0, by_eval - by_eval0);
+        fl_eval0 = fl_eval;
+        by_eval0 = by_eval;
+      };
+      for (auto& s : stacks) {
+        emit_stack(s, cj, ctiles, ej);
+        if (ej.size() >= kChunk) flush_eval();
+        if (cj.size() >= kChunk) submit_copy(cj, ctiles);
+      }
+      submit_copy(cj, ctiles);
+      t2 = now_s();
+      t_b += t2 - t1;
+      flush_eval();
     }
-    flush_copy();
-    double t2 = now_s();
-    t_b += t2 - t1;
-    flush_eval();
     // truncations and dense adds
     std::vector<TruncReq> tr;
     std::vector<int> tr_fp;
@@ -965,11 +1085,13 @@ struct Planner {
     auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
     levels.clear();
     levels.push_back(std::move(roots));
+    std::vector<Groups> pre;
     while (true) {
       auto a = clk::now();
-      LevelTail tail = run_level_enqueue(levels.back());
+      LevelTail tail = run_level_enqueue(levels.back(), &pre);
       auto b = clk::now();
       std::vector<Node> next = split_level(levels.back());   // overlaps the level's device work
+      pre = plan_level(next);
       auto d = clk::now();
       run_level_finish(std::move(tail));
       t_level += sec(a, b);

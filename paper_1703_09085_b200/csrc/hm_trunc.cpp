@@ -151,6 +151,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   // factors into more, shorter chunks (more CTAs on one QR)
   static const int ts_min_l = [] { const char* e = std::getenv("HM_TSQR_ROWS_LAT"); return e ? std::atoi(e) : 1536; }();
   static const int ts_h_l = [] { const char* e = std::getenv("HM_TSQR_H_LAT"); return e ? std::atoi(e) : 768; }();
+  static const int ts_even = [] { const char* e = std::getenv("HM_TSQR_EVEN"); return e ? std::atoi(e) : 1; }();
   const bool lat_batch = nj < 64;
   const int ts_min = lat_batch ? ts_min_l : ts_min_b;
   const int ts_h = lat_batch ? ts_h_l : ts_h_b;
@@ -167,8 +168,15 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       TsPlan P{i, side, r.l, trunc_kcap(r.m, r.n, r.l), {}};
       TsLevel L{side == 0 ? r.A : r.B, rows0, rows0, 0, 1, nullptr, 0, side == 0 ? r.Aout : r.Bout, rows0, nullptr};
       for (;;) {
-        if (L.rows > ts_min) { L.h = ts_h; L.nch = L.rows / ts_h; }
-        else { L.h = L.rows; L.nch = 1; }
+        if (L.rows > ts_min) {
+          if (ts_even) {   // chunks of equal height <= ts_h (every chunk in the register-panel QR's range)
+            L.nch = (L.rows + ts_h - 1) / ts_h;
+            L.h = (L.rows + L.nch - 1) / L.nch;
+          } else {         // chunks of ts_h rows, the last one takes the remainder (< 2 ts_h)
+            L.h = ts_h;
+            L.nch = L.rows / ts_h;
+          }
+        } else { L.h = L.rows; L.nch = 1; }
         L.tau = ar.alloc((size_t)L.nch * r.l);
         L.T = ar.alloc((size_t)L.nch * ((r.l + 15) / 16) * 256);
         P.lv.push_back(L);
