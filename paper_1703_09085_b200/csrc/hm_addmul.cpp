@@ -378,7 +378,7 @@ struct Planner {
   // Upload one prepared batch (jobs, range table, chained jobs of state E) and launch k_eval2.
   void submit_evals(std::vector<EvalJob>& sorted, EmitState& E, Arena& scratch, double fl, double by) {
     if (sorted.empty()) return;
-    const int2* drng = E.erng.empty() ? nullptr : scratch.upload(E.erng);
+    const int2* drng = E.erng.empty() ? nullptr : scratch.upload_t(E.erng);
     EvalJob* dtail = nullptr;
     if (!E.etail.empty()) {
       dtail = static_cast<EvalJob*>(scratch.alloc_bytes(E.etail.size() * sizeof(EvalJob)));
@@ -395,7 +395,7 @@ struct Planner {
     E.erng.clear();
     E.etail.clear();
     ProfScope ps(c, PC_EVAL, fl, by);
-    launch_eval2(scratch.upload(sorted), (int)sorted.size(), c->stream);
+    launch_eval2(scratch.upload_t(sorted), (int)sorted.size(), c->stream);
     HM_CHECK_LAUNCH();
     sorted.clear();
   }
@@ -696,8 +696,8 @@ struct Planner {
         std::fill(tmap.begin() + cj[j].tile0, tmap.begin() + t1, (int)j);
       }
       ProfScope ps(c, PC_COPY, 0, cb);
-      const CopyJob* dj = scratch.upload(cj);
-      launch_copy_mapped(dj, (int)cj.size(), scratch.upload(tmap), ctiles, c->stream);
+      const CopyJob* dj = scratch.upload_t(cj);
+      launch_copy_mapped(dj, (int)cj.size(), scratch.upload_t(tmap), ctiles, c->stream);
       HM_CHECK_LAUNCH();
       cj.clear();
       ctiles = 0;
@@ -833,7 +833,7 @@ struct Planner {
     }
     if (!gj.empty()) {
       ProfScope ps(c, PC_DENSE, fl_dense - fl_dense0, by_dense - by_dense0);
-      launch_gemm_mapped(scratch.upload(gj), (int)gj.size(), scratch.tile_map(gj, gtiles), gtiles, c->stream);
+      launch_gemm_mapped(scratch.upload_t(gj), (int)gj.size(), scratch.tile_map_t(gj, gtiles), gtiles, c->stream);
       HM_CHECK_LAUNCH();
     }
     double t3 = now_s();
@@ -995,7 +995,7 @@ struct Planner {
         }
         {
           ProfScope ps(c, PC_COPY, 0, 0);
-          launch_copy_mapped(scratch.upload(cj), (int)cj.size(), scratch.tile_map(cj, ctiles), ctiles, c->stream);
+          launch_copy_mapped(scratch.upload_t(cj), (int)cj.size(), scratch.tile_map_t(cj, ctiles), ctiles, c->stream);
           HM_CHECK_LAUNCH();
         }
         std::vector<TruncReq> tr;
@@ -1062,7 +1062,7 @@ struct Planner {
       add_copy(cj, ctiles, nB[b], f.ldb, f.B, f.ldb, f.ldb, f.k, 0, 0, 1.0);
     }
     Arena scratch(c);
-    launch_copy_mapped(scratch.upload(cj), (int)cj.size(), scratch.tile_map(cj, ctiles), ctiles, c->stream);
+    launch_copy_mapped(scratch.upload_t(cj), (int)cj.size(), scratch.tile_map_t(cj, ctiles), ctiles, c->stream);
     HM_CHECK_LAUNCH();
     HM_CUDA(cudaStreamSynchronize(c->stream));
     scratch.release();
@@ -1372,7 +1372,7 @@ struct Factorizer {
     else steps_lower(t, mode == 0, T.cl_start[t], st);
     Arena ar(c);
     std::vector<TrsmJob> jb{TrsmJob{V, ldv, ncols, T.cl_start[t], 0, (int)st.size()}};
-    trsm_launch(ar.upload(jb), 1, ar.upload(st), dlt, c->stream);
+    trsm_launch(ar.upload_t(jb), 1, ar.upload_t(st), dlt, c->stream);
     HM_CHECK_LAUNCH();
   }
 
@@ -1382,7 +1382,7 @@ struct Factorizer {
     const int m = T.cl_size[t];
     Arena ar(c);
     std::vector<LeafFactorJob> j{LeafFactorJob{G->pA[d], m, m, t}};
-    launch_leaf_factor(ar.upload(j), 1, chol ? 1 : 0, d_fail, d_minpiv + t, m, c->stream);
+    launch_leaf_factor(ar.upload_t(j), 1, chol ? 1 : 0, d_fail, d_minpiv + t, m, c->stream);
     HM_CHECK_LAUNCH();
   }
 
@@ -1431,9 +1431,9 @@ struct Factorizer {
     }
     n_trsm += (int64_t)jobs.size();
     ProfScope ps(c, PC_TRSM, 0, 0);
-    if (!pre.empty()) launch_copy_mapped(ar.upload(pre), (int)pre.size(), ar.tile_map(pre, pt), pt, c->stream);
-    if (!jobs.empty()) trsm_launch(ar.upload(jobs), (int)jobs.size(), ar.upload(st), dlt, c->stream);
-    if (!post.empty()) launch_copy_mapped(ar.upload(post), (int)post.size(), ar.tile_map(post, qt), qt, c->stream);
+    if (!pre.empty()) launch_copy_mapped(ar.upload_t(pre), (int)pre.size(), ar.tile_map_t(pre, pt), pt, c->stream);
+    if (!jobs.empty()) trsm_launch(ar.upload_t(jobs), (int)jobs.size(), ar.upload_t(st), dlt, c->stream);
+    if (!post.empty()) launch_copy_mapped(ar.upload_t(post), (int)post.size(), ar.tile_map_t(post, qt), qt, c->stream);
     HM_CHECK_LAUNCH();
   }
 

@@ -19,14 +19,15 @@ bool debug_sync() {
 void* Ctx::pinned(size_t bytes) {
   bytes = (bytes + 255) & ~size_t(255);
   if (pin_used + bytes > pin_cap) {
-    // recycle: wait until every copy from the staging buffer has completed
-    HM_CUDA(cudaStreamSynchronize(stream));
+    // recycle: wait until every copy from the staging buffer has completed and
+    // every kernel (auxiliary streams too) has read its in-place descriptors
+    HM_CUDA(cudaDeviceSynchronize());
     pin_used = 0;
     if (bytes > pin_cap) {
       if (pin) cudaFreeHost(pin);
       pin = nullptr;
       size_t cap = std::max(bytes, (size_t)256 << 20);
-      HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pin), cap));
+      HM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pin), cap, cudaHostAllocMapped | cudaHostAllocPortable));
       pin_cap = cap;
     }
   }

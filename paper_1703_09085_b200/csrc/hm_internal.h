@@ -87,6 +87,10 @@ struct Ctx {
   // after the stream has been synchronized (so in-flight copies are complete)
   char* pin = nullptr;
   size_t pin_cap = 0, pin_used = 0;
+  // Arena::upload_t: arrays up to this size are read in place.  Off by default
+  // (measured on B200: no effect on the H-LR, 9.59 vs 9.60 s at n = 81920 -- the
+  // descriptor copies are not on the critical path); HM_ZERO_COPY=1 enables it.
+  size_t zc_max = [] { const char* e = std::getenv("HM_ZERO_COPY"); return (e && e[0] == '1') ? (size_t)32 << 10 : (size_t)0; }();
   void* pinned(size_t bytes);
   void pinned_reset() { pin_used = 0; }
   // grow-only device workspace for the per-level stacks (one user at a time,
@@ -145,6 +149,31 @@ struct Arena {
     std::memcpy(h, v.data(), bytes);
     HM_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     return d;
+  }
+  // Transient job descriptors (read once by the kernels enqueued before the
+  // owner's next stream synchronisation): small arrays are NOT copied to the
+  // device -- the kernels read the pinned, mapped staging memory directly
+  // (UVA), which saves one H2D copy (host call + copy-engine latency on the
+  // stream) per launch on the latency-bound paths.  HM_ZERO_COPY=0: always copy.
+  template <class T>
+  T* upload_t(const std::vector<T>& v) {
+    if (v.empty()) return nullptr;
+    const size_t bytes = v.size() * sizeof(T);
+    if (bytes > ctx->zc_max) return upload(v);
+    void* h = ctx->pinned(bytes);
+    std::memcpy(h, v.data(), bytes);
+    return static_cast<T*>(h);
+  }
+  template <class J>
+  const int* tile_map_t(const std::vector<J>& v, int64_t ntiles) {
+    if (v.empty() || ntiles <= 0) return nullptr;
+    if ((size_t)ntiles * sizeof(int) > ctx->zc_max) return tile_map(v, ntiles);
+    std::vector<int> m((size_t)ntiles);
+    for (size_t j = 0; j < v.size(); j++) {
+      const int64_t t1 = j + 1 < v.size() ? v[j + 1].tile0 : ntiles;
+      for (int64_t t = v[j].tile0; t < t1; t++) m[(size_t)t] = (int)j;
+    }
+    return upload_t(m);
   }
   // job index of every tile of a tiled launch (jobs carry a prefix-summed
   // tile0), uploaded next to the jobs: one load per CTA instead of a binary

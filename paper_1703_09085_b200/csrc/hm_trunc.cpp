@@ -90,7 +90,7 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
     const TruncSmallJob* dj[3];
     bool any = false;
     for (int b = 0; b < 3; b++) {
-      dj[b] = fb[b].empty() ? nullptr : ar.upload(fb[b]);
+      dj[b] = fb[b].empty() ? nullptr : ar.upload_t(fb[b]);
       any = any || dj[b];
     }
     if (any) {
@@ -253,12 +253,12 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     for (int b = 0; b < 3; b++) prep_bucket(qbk[b], b);
     // uploads first (they are ordered on the main stream), then every bucket
     // on its own auxiliary stream: the buckets are independent problems
-    const QrJob* dqs = qs.empty() ? nullptr : ar.upload(qs);
-    const QrJob* dqh = qr_huge.empty() ? nullptr : ar.upload(qr_huge);
+    const QrJob* dqs = qs.empty() ? nullptr : ar.upload_t(qs);
+    const QrJob* dqh = qr_huge.empty() ? nullptr : ar.upload_t(qr_huge);
     const QrJob* dqb[4];
     int used = (dqs ? 1 : 0) + (dqh ? 1 : 0);
     for (int b = 0; b < 4; b++) {
-      dqb[b] = qbk[b].empty() ? nullptr : ar.upload(qbk[b]);
+      dqb[b] = qbk[b].empty() ? nullptr : ar.upload_t(qbk[b]);
       used += dqb[b] ? 1 : 0;
     }
     const bool par = used > 1 && c->multi_stream();
@@ -341,7 +341,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
           qj.push_back(QrJob{U.V + r0, cr, P.l, U.ld, U.tau + (size_t)ch * P.l, chunkT(U, ch, cr, P.l)});
         }
       }
-      launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
+      launch_copy_mapped(ar.upload_t(cj), (int)cj.size(), ar.tile_map_t(cj, tiles), tiles, st);
       launch_qr_set(qj);
     }
     HM_CHECK_LAUNCH();
@@ -385,7 +385,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   c->prof_note(shapes);
   {
     ProfScope ps(c, PC_GEMM_M, fl_m, 0);
-    launch_gemm_mapped(ar.upload(gj), (int)gj.size(), ar.tile_map(gj, tiles), tiles, st);
+    launch_gemm_mapped(ar.upload_t(gj), (int)gj.size(), ar.tile_map_t(gj, tiles), tiles, st);
     HM_CHECK_LAUNCH();
   }
   if (const char* dm = std::getenv("HM_DUMP_M")) {   // diagnostics: first job's M (tall orientation)
@@ -428,7 +428,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     for (int b = 0; b < 4; b++)
       if (!pq[b].empty()) {
         prep_bucket(pq[b], b);
-        launch_bucket(pq[b], ar.upload(pq[b]), b, pqcap[b], st);
+        launch_bucket(pq[b], ar.upload_t(pq[b]), b, pqcap[b], st);
       }
     HM_CHECK_LAUNCH();
   }
@@ -468,7 +468,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     const SvdJob* dsj[4];
     int used = 0;
     for (int b = 0; b < 4; b++) {
-      dsj[b] = sj[b].empty() ? nullptr : ar.upload(sj[b]);
+      dsj[b] = sj[b].empty() ? nullptr : ar.upload_t(sj[b]);
       used += dsj[b] ? 1 : 0;
     }
     const bool par = used > 1 && c->multi_stream();
@@ -542,8 +542,8 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
         if (aq_dmma && j.T && j.m <= 1536) { fast.push_back(j); mm = std::max(mm, j.m); }
         else slow.push_back(j);
       }
-      if (!fast.empty()) launch_applyq_dmma(ar.upload(fast), (int)fast.size(), cmax(fast), mm, st);
-      if (!slow.empty()) launch_applyq(ar.upload(slow), (int)slow.size(), cmax(slow), st);
+      if (!fast.empty()) launch_applyq_dmma(ar.upload_t(fast), (int)fast.size(), cmax(fast), mm, st);
+      if (!slow.empty()) launch_applyq(ar.upload_t(slow), (int)slow.size(), cmax(slow), st);
     };
     launch_applyq_split(aq1);
     if (!ts.empty()) {
@@ -557,7 +557,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       int64_t tiles = 0;
       for (const TsPlan& P : ts)
         add_copy(cj, tiles, P.lv.back().X, P.lv.back().ldx, P.lv[0].X, P.lv[0].ldx, P.l, P.kcap, 0);
-      launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
+      launch_copy_mapped(ar.upload_t(cj), (int)cj.size(), ar.tile_map_t(cj, tiles), tiles, st);
       for (size_t lvl = maxdepth - 1; lvl >= 1; lvl--) {
         std::vector<ApplyQJob> tq;
         cj.clear();
@@ -579,7 +579,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
           }
         }
         launch_applyq_split(tq);
-        launch_copy_mapped(ar.upload(cj), (int)cj.size(), ar.tile_map(cj, tiles), tiles, st);
+        launch_copy_mapped(ar.upload_t(cj), (int)cj.size(), ar.tile_map_t(cj, tiles), tiles, st);
       }
     }
     launch_applyq_split(aq);

@@ -314,8 +314,12 @@ __device__ int jacobi_sweeps_stream(double* X, int ldx, int c, int rt, double to
 //   C = Q R P^T = (Q R U_x) (P U_x)^T,
 // i.e. the permuted (short) side gets the orthonormal P U_x,k and the Q side
 // gets Q (R U_x,k) = Q V_k S_k, formed by one product with the R left in C.
+// spill (k_svd, C + X too large for shared memory but C alone fits): C lives in
+// shared memory for the QRCP, is then moved to `spill` (global memory; R and
+// the reflectors are only read again by the output phase) and X = R^T takes
+// its place (X == the shared-memory address of C on entry).
 __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, int L, int c, double* C, int ldc, double* X,
-                         double* tau, double* nrm, double* sig, int* perm, int* order) {
+                         double* tau, double* nrm, double* sig, int* perm, int* order, double* spill = nullptr) {
   __shared__ double red[32];
   __shared__ int s_rank;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -457,6 +461,15 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   }
   __syncthreads();
   rt = s_rt;
+  if (spill) {
+    // columns < rt whole (reflectors + R), the others only their R rows
+    for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
+      const int i = (int)(e % L), col = (int)(e / L);
+      if (col < rt || i < rt) spill[i + (int64_t)col * ldc] = C[i + (int64_t)col * ldc];
+    }
+    __syncthreads();
+    C = spill;
+  }
   PHASE("qrcp");
   // X = R^T (c x rt, ld ldx)
   const int ldx = pad_ld(c);
@@ -562,6 +575,29 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   // Q side: one group of Gq lanes per output column; the column stays in
   // registers (row gq + u Gq in slot u) while R u is formed and the rt
   // reflectors are applied
+  // spill mode: R and the reflectors come back into the shared memory behind X
+  // when they fit (rt <~ 0.38 c), else they are read from global memory / L2
+  const double* Clo = C;                        // columns < rt (reflectors + R), ld ldc
+  const double* Rhi = C + (int64_t)rt * ldc;    // columns >= rt (rows < rt of R), ld ldh
+  int ldh = ldc;
+  if (spill) {
+    double* S = X + (int64_t)ldx * rt;
+    if ((int64_t)ldx * rt + (int64_t)ldc * rt + (int64_t)rt * (c - rt) <= (int64_t)ldc * c) {
+      double* S2 = S + (int64_t)ldc * rt;
+      for (int64_t e = tid; e < (int64_t)L * rt; e += NT) {
+        const int i = (int)(e % L), col = (int)(e / L);
+        S[i + (int64_t)col * ldc] = C[i + (int64_t)col * ldc];
+      }
+      for (int64_t e = tid; e < (int64_t)rt * (c - rt); e += NT) {
+        const int i = (int)(e % rt), col = (int)(e / rt);
+        S2[i + (int64_t)col * rt] = C[i + (int64_t)(rt + col) * ldc];
+      }
+      __syncthreads();
+      Clo = S;
+      Rhi = S2;
+      ldh = rt;
+    }
+  }
   const bool oreg = L <= kE * Gq;
   for (int base = warp * gpwq; base < k; base += NW * gpwq) {
     const int i = base + lane / Gq;
@@ -577,7 +613,7 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
       if (act)
         for (int jj = 0; jj < c; jj++) {
           const double xv = w[jj] * inv;
-          const double* rc = C + (int64_t)jj * ldc;
+          const double* rc = jj < rt ? Clo + (int64_t)jj * ldc : Rhi + (int64_t)(jj - rt) * ldh;
 #pragma unroll
           for (int u = 0; u < kE; u++) {
             const int r = gq + u * Gq;
@@ -587,7 +623,7 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
       for (int jj = rt - 1; jj >= 0; jj--) {
         const double t = tau[jj];
         if (t == 0.0) continue;
-        const double* v = C + (int64_t)jj * ldc;
+        const double* v = Clo + (int64_t)jj * ldc;
         double d = 0.0, yj = 0.0;
         const int uj = jj / Gq;
 #pragma unroll
@@ -619,14 +655,15 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
         for (int r = gq; r < Qrows; r += Gq) {
           double s = 0.0;
           if (r < rt)
-            for (int jj = r; jj < c; jj++) s = fma(C[r + (int64_t)jj * ldc], w[jj] * inv, s);
+            for (int jj = r; jj < c; jj++)
+              s = fma(jj < rt ? Clo[r + (int64_t)jj * ldc] : Rhi[r + (int64_t)(jj - rt) * ldh], w[jj] * inv, s);
           y[r] = s;
         }
       __syncwarp();
       for (int jj = rt - 1; jj >= 0; jj--) {
         const double t = tau[jj];
         if (t == 0.0) continue;
-        const double* v = C + (int64_t)jj * ldc;
+        const double* v = Clo + (int64_t)jj * ldc;
         double d = 0.0;
         if (act)
           for (int r = jj + 1 + gq; r < L; r += Gq) d = fma(v[r], y[r], d);
@@ -662,9 +699,11 @@ __global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, do
   }
   const int ldc = pad_ld(L);
   const int64_t need = svd_ws(L, c);
-  double* C = (need <= cap) ? sm : J.work;      // L x c (ld ldc), QRCP in place
-  double* X = C + (int64_t)ldc * c;             // c x rt  (R^T, then W)
-  double* tau = X + (int64_t)pad_ld(c) * c;     // c
+  const bool fits = need <= cap;
+  const bool spillm = !fits && J.work && (int64_t)ldc * c + 6 * (int64_t)c <= cap;
+  double* C = (fits || spillm) ? sm : J.work;   // L x c (ld ldc), QRCP in place
+  double* X = spillm ? sm : C + (int64_t)ldc * c;   // c x rt  (R^T, then W)
+  double* tau = spillm ? sm + (int64_t)ldc * c : X + (int64_t)pad_ld(c) * c;     // c
   double* nrm = tau + c;                        // c
   double* sig = nrm + c;                        // c
   int* perm = reinterpret_cast<int*>(sig + c);  // c
@@ -674,7 +713,7 @@ __global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, do
     const int mi = tr ? j : i, mj = tr ? i : j;   // entry (mi, mj) of M
     C[i + (int64_t)j * ldc] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
   }
-  svd_core(J, eps, drop_rel, tr, L, c, C, ldc, X, tau, nrm, sig, perm, order);
+  svd_core(J, eps, drop_rel, tr, L, c, C, ldc, X, tau, nrm, sig, perm, order, spillm ? J.work : nullptr);
   PHASE_FLUSH;
 }
 
@@ -971,11 +1010,12 @@ void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int 
 }
 
 int svd_smem_capacity() { return 26 * 1024; }
+static constexpr int kSpillCap = 28 * 1024;   // doubles of shared memory of the spill mode (224 KB)
 
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st) {
   if (njobs <= 0) return;
   subwarps_knob();
-  ensure_smem_attr((const void*)k_svd, svd_smem_capacity() * 8);
+  ensure_smem_attr((const void*)k_svd, kSpillCap * 8);
   if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
   static const int tg = [] { const char* e = std::getenv("HM_SVDG_THREADS"); return e ? std::atoi(e) : 512; }();
   int threads = (cap == 0 || cap > 8 * 1024 || njobs < 296) ? 512 : 256;
@@ -984,6 +1024,11 @@ void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream
   static const int tlat = [] { const char* e = std::getenv("HM_SVD_LAT"); return e ? std::atoi(e) : 0; }();
   if (tlat > 0 && njobs < 296) threads = tlat;
   count_launch();
+  // global-workspace bucket: the matrices whose C alone fits get the spill mode
+  // (QRCP and Jacobi in shared memory, C parked in the workspace in between);
+  // one CTA per SM either way (registers)
+  static const int spill = [] { const char* e = std::getenv("HM_SVD_SPILL"); return e ? std::atoi(e) : 1; }();
+  if (cap == 0 && spill) cap = kSpillCap;
   k_svd<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, drop_rel_host(), cap);
 }
 

@@ -153,6 +153,8 @@ def test_trunc_kernel_reg_qr(hm, ctx):
         shapes.append((400 + 30 * i, 90 + 5 * i, 33 + 8 * i, i % 2))          # classes 3-4 one-sided
         shapes.append((1600 + 400 * i, 300 + 20 * i, 20 + 6 * i, 1))          # TSQR: chunk stacks of 2-7 l rows
     shapes += [(768, 767, 133, 0), (385, 384, 100, 1), (257, 256, 31, 2), (129, 128, 47, 0), (513, 512, 64, 1)]
+    # M = R_A R_B^T of 112 .. 167 columns: the SVD's spill mode (svd.cu), then the global workspace
+    shapes += [(300, 290, 113, 0), (320, 310, 150, 1), (500, 450, 160, 0), (400, 380, 167, 0), (420, 400, 166, 1)]
     stacks, svals = [], []
     for m, n, q, junk in shapes:
         s = 10.0 ** (-0.21 * np.arange(q))
