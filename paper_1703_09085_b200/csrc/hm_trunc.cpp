@@ -400,9 +400,9 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   }
   // --- SVD jobs; matrices too large for shared memory are first reduced by an
   // unpivoted blocked QR (Mt = Q1 R1) and the SVD kernel works on R1 (c x c).
-  std::vector<SvdJob> sj[4];
+  std::vector<SvdJob> sj[5];   // 3 shared-memory buckets, global workspace, spill mode
   int caps[4] = {3 * 1024, 8 * 1024, 26 * 1024, 0};
-  double fl_svd = 0, fl_b[4] = {0, 0, 0, 0};
+  double fl_svd = 0, fl_b[5] = {0, 0, 0, 0, 0};
   const char* dump = std::getenv("HM_DUMP_JOBS");
   int* d_sw = dump ? static_cast<int*>(ar.alloc_bytes(sizeof(int) * (nj + 1))) : nullptr;
   std::vector<int> bucket_of(nj);
@@ -457,30 +457,33 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     int b = 3;
     for (int k = 0; k < 3; k++)
       if (cap == caps[k]) { b = k; break; }
+    if (b == 3 && svd_spill_fits(Ls, cc)) b = 4;
     fl_b[b] += 22.0 * (double)cc * cc * cc;
     bucket_of[i] = b;
-    if (b == 3) s.work = ar.alloc((size_t)need);
+    if (b >= 3) s.work = ar.alloc((size_t)need);
     sj[b].push_back(s);
   }
   c->prof_note(shapes);
   {
     ProfScope ps(c, PC_SVD, fl_svd, 0);
-    const SvdJob* dsj[4];
+    const SvdJob* dsj[5];
     int used = 0;
-    for (int b = 0; b < 4; b++) {
+    for (int b = 0; b < 5; b++) {
       dsj[b] = sj[b].empty() ? nullptr : ar.upload_t(sj[b]);
       used += dsj[b] ? 1 : 0;
     }
     const bool par = used > 1 && c->multi_stream();
-    for (int b = 3; b >= 0; b--) {   // the largest problems first
+    for (int b = 4; b >= 0; b--) {   // the largest problems first; spill mode shares the global bucket's stream
       if (!dsj[b]) continue;
-      cudaStream_t sb = par ? c->fork(1 + b) : st;
-      ProfScope pb(c, PC_SVD_B0 + b, fl_b[b], (double)sj[b].size(), sb);
-      launch_svd(dsj[b], (int)sj[b].size(), eps, caps[b], sb);
+      const int sb_i = b == 4 ? 3 : b;
+      cudaStream_t sb = par ? c->fork(1 + sb_i) : st;
+      ProfScope pb(c, PC_SVD_B0 + sb_i, fl_b[b], (double)sj[b].size(), sb);
+      if (b == 4) launch_svd_spill(dsj[b], (int)sj[b].size(), eps, sb);
+      else launch_svd(dsj[b], (int)sj[b].size(), eps, caps[b], sb);
     }
     if (par)
       for (int b = 0; b < 4; b++)
-        if (dsj[b]) c->join(1 + b);
+        if (dsj[b] || (b == 3 && dsj[4])) c->join(1 + b);
     HM_CHECK_LAUNCH();
   }
   if (dump) {

@@ -193,6 +193,9 @@ void launch_qr_reg(const QrJob* d_jobs, int njobs, int max_m, cudaStream_t st);
 void launch_applyq_dmma(const ApplyQJob* d_jobs, int njobs, int cmax, int max_m, cudaStream_t st);
 void launch_applyq(const ApplyQJob* d_jobs, int njobs, int cmax, cudaStream_t st);
 void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream_t st);
+// k_svd spill mode (C in shared memory for the QRCP, parked in SvdJob::work, X in its place)
+bool svd_spill_fits(int p, int q);
+void launch_svd_spill(const SvdJob* d_jobs, int njobs, double eps, cudaStream_t st);
 void launch_copy(const CopyJob* d_jobs, int njobs, int64_t ntiles, cudaStream_t st);
 void launch_copy_mapped(const CopyJob* d_jobs, int njobs, const int* d_tmap, int64_t ntiles, cudaStream_t st);
 void launch_eval2(const EvalJob* d_jobs, int njobs, cudaStream_t st);   // eval.cu (shared-memory tiles)

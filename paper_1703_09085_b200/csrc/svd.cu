@@ -205,6 +205,7 @@ __device__ __forceinline__ void jacobi_rot(double al, double be, double ga, doub
 // Returns the number of sweeps.
 template <int G, int E>
 __device__ int jacobi_sweeps(double* X, int ldx, int c, int rt, double tol2, double delta2, int NW) {
+  const double tol = sqrt(tol2);
   // called by the first NW warps of the CTA only (sub_sync)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int gpw = 32 / G;
@@ -254,7 +255,9 @@ __device__ int jacobi_sweeps(double* X, int ldx, int c, int rt, double tol2, dou
               x[u * G] = cs * xr[u] - sn * yr[u];
               y[u * G] = sn * xr[u] + cs * yr[u];
             }
-          rot = 1;
+          // quadratic convergence: a sweep whose largest |x.y| / (|x||y|) is below
+          // sqrt(tol) leaves at most ~tol behind -- no confirming sweep after it
+          if (ga * ga > tol * al * be) rot = 1;
         }
       }
       sub_sync(NW * 32);
@@ -295,7 +298,7 @@ __device__ int jacobi_sweeps_stream(double* X, int ldx, int c, int rt, double to
             x[i] = cs * xv - sn * yv;
             y[i] = sn * xv + cs * yv;
           }
-          rot = 1;
+          if (ga * ga > sqrt(tol2) * al * be) rot = 1;
         }
       }
       __syncthreads();
@@ -1024,12 +1027,24 @@ void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream
   static const int tlat = [] { const char* e = std::getenv("HM_SVD_LAT"); return e ? std::atoi(e) : 0; }();
   if (tlat > 0 && njobs < 296) threads = tlat;
   count_launch();
-  // global-workspace bucket: the matrices whose C alone fits get the spill mode
-  // (QRCP and Jacobi in shared memory, C parked in the workspace in between);
-  // one CTA per SM either way (registers)
-  static const int spill = [] { const char* e = std::getenv("HM_SVD_SPILL"); return e ? std::atoi(e) : 1; }();
-  if (cap == 0 && spill) cap = kSpillCap;
   k_svd<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, drop_rel_host(), cap);
+}
+
+// Spill mode (see svd_core): matrices whose C + X do not fit in shared memory
+// but whose C alone does.  Their own launch: the plain global-workspace
+// bucket keeps the whole L1 (no dynamic shared memory).
+bool svd_spill_fits(int p, int q) {
+  static const int spill = [] { const char* e = std::getenv("HM_SVD_SPILL"); return e ? std::atoi(e) : 1; }();
+  const int L = p > q ? p : q, c = p < q ? p : q;
+  return spill && svd_ws(L, c) > svd_smem_capacity() && (int64_t)pad_ld(L) * c + 6 * (int64_t)c <= kSpillCap;
+}
+
+void launch_svd_spill(const SvdJob* d_jobs, int njobs, double eps, cudaStream_t st) {
+  if (njobs <= 0) return;
+  subwarps_knob();
+  ensure_smem_attr((const void*)k_svd, kSpillCap * 8);
+  count_launch();
+  k_svd<<<njobs, 512, (size_t)kSpillCap * 8, st>>>(d_jobs, eps, drop_rel_host(), kSpillCap);
 }
 
 }  // namespace hm
