@@ -549,14 +549,22 @@ struct Planner {
   }
 
   void sync_ranks(int* d_ranks, const std::vector<int>& fp_ids) {
-    if (fp_ids.empty()) return;
+    if (fp_ids.empty()) {
+      if (c->rank_is_host(d_ranks)) c->rank_used = 0;   // nothing was enqueued on it
+      return;
+    }
     n_sync++;
     std::vector<int> h(fp_ids.size());
     auto a = std::chrono::steady_clock::now();
     HM_CUDA(cudaStreamSynchronize(c->stream));
     c->pinned_reset();   // every staged upload has completed
     t_wait += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
-    HM_CUDA(cudaMemcpy(h.data(), d_ranks, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    if (c->rank_is_host(d_ranks)) {   // written by the kernels into mapped host memory
+      std::memcpy(h.data(), d_ranks, h.size() * sizeof(int));
+      c->rank_used = 0;
+    } else {
+      HM_CUDA(cudaMemcpy(h.data(), d_ranks, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    }
     for (size_t i = 0; i < fp_ids.size(); i++) fps[fp_ids[i]].k = h[i];
   }
 
@@ -799,7 +807,8 @@ struct Planner {
     std::vector<int> tr_fp;
     std::vector<GemmJob> gj;
     int64_t gtiles = 0;
-    int* d_ranks = static_cast<int*>(scratch.alloc_bytes(sizeof(int) * (stacks.size() + 1)));
+    int* d_ranks = c->rank_alloc(stacks.size() + 1);
+    if (!d_ranks) d_ranks = static_cast<int*>(scratch.alloc_bytes(sizeof(int) * (stacks.size() + 1)));
     const double fl_dense0 = fl_dense, by_dense0 = by_dense;
     for (auto& s : stacks) {
       Node& nd = nodes[s.node];
@@ -1000,7 +1009,8 @@ struct Planner {
         }
         std::vector<TruncReq> tr;
         std::vector<int> tr_fp;
-        int* d_ranks = static_cast<int*>(scratch.alloc_bytes(sizeof(int) * (pre.size() + 1)));
+        int* d_ranks = c->rank_alloc(pre.size() + 1);
+        if (!d_ranks) d_ranks = static_cast<int*>(scratch.alloc_bytes(sizeof(int) * (pre.size() + 1)));
         for (size_t w = 0; w < pre.size(); w++) {
           S& s = pre[w];
           const Node& nd = levels[lev][mn[who[w].first]];
@@ -1218,16 +1228,6 @@ struct Factorizer {
   }
   int son0(int t) const { return T.cl_son0[t]; }
 
-  void patch_leaf(int b) {
-    const int pos = leafpos[b];
-    lt[pos].A = G->pA[b];
-    lt[pos].B = G->pB[b];
-    lt[pos].k = T.bl_kind[b] == HM_BLOCK_ADM ? G->rank[b] : 0;
-    void* h = c->pinned(sizeof(LeafDesc));
-    std::memcpy(h, &lt[pos], sizeof(LeafDesc));
-    HM_CUDA(cudaMemcpyAsync(dlt + pos, h, sizeof(LeafDesc), cudaMemcpyHostToDevice, c->stream));
-  }
-
   Node acc_for(int b) const {
     Node nd;
     nd.t = T.bl_row[b];
@@ -1277,6 +1277,12 @@ struct Factorizer {
     }
     P.run_from(std::move(roots));
     for (size_t i = 0; i < red_nodes.size(); i++) red_nodes[i]->red = P.levels[0][nflush + i].red;
+    // the new factors move from the flush's arena into buffers of their own and
+    // the leaf table is patched: ONE copy launch and ONE patch launch per flush
+    // (per-block cudaMemcpyAsync calls left the device idle for ~180 us per flush)
+    std::vector<CopyJob> cj;
+    std::vector<LeafPatch> patches;
+    int64_t ctiles = 0;
     for (int zb : zbs) {
       if (T.bl_kind[zb] != HM_BLOCK_ADM) continue;
       const int f = P.zres(0, zb);
@@ -1286,16 +1292,27 @@ struct Factorizer {
       const size_t bytes = sizeof(double) * ((size_t)(m + n) * k + 1);
       double* buf = static_cast<double*>(c->dmalloc(bytes));
       if (k > 0) {
-        HM_CUDA(cudaMemcpyAsync(buf, fp.A, sizeof(double) * (size_t)m * k, cudaMemcpyDeviceToDevice, c->stream));
-        HM_CUDA(cudaMemcpyAsync(buf + (size_t)m * k, fp.B, sizeof(double) * (size_t)n * k,
-                                cudaMemcpyDeviceToDevice, c->stream));
+        P.add_copy(cj, ctiles, buf, m, fp.A, m, m, k, 0, 0, 1.0);
+        P.add_copy(cj, ctiles, buf + (size_t)m * k, n, fp.B, n, n, k, 0, 0, 1.0);
       }
       if (own[zb].first) c->dfree(own[zb].first, own[zb].second);
       own[zb] = {buf, bytes};
       G->pA[zb] = buf;
       G->pB[zb] = buf + (size_t)m * k;
       G->rank[zb] = k;
-      patch_leaf(zb);
+      const int pos = leafpos[zb];
+      lt[pos].A = G->pA[zb];
+      lt[pos].B = G->pB[zb];
+      lt[pos].k = k;
+      patches.push_back(LeafPatch{pos, lt[pos]});
+    }
+    if (!cj.empty()) {
+      launch_copy_mapped(local.upload(cj), (int)cj.size(), local.tile_map(cj, ctiles), ctiles, c->stream);
+      HM_CHECK_LAUNCH();
+    }
+    if (!patches.empty()) {
+      launch_patch_leaves(dlt, local.upload(patches), (int)patches.size(), c->stream);
+      HM_CHECK_LAUNCH();
     }
     P.fp_arena = nullptr;
     local.release();

@@ -36,6 +36,20 @@ void* Ctx::pinned(size_t bytes) {
   return p;
 }
 
+int* Ctx::rank_alloc(size_t n) {
+  static const bool off = [] { const char* e = std::getenv("HM_RANK_HOST"); return e && e[0] == '0'; }();
+  if (off || n > 4096) return nullptr;
+  if (!rank_host) {
+    rank_cap = (size_t)1 << 16;
+    HM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&rank_host), rank_cap * sizeof(int),
+                          cudaHostAllocMapped | cudaHostAllocPortable));
+  }
+  if (rank_used + n > rank_cap) return nullptr;
+  int* p = rank_host + rank_used;
+  rank_used += n;
+  return p;
+}
+
 void Ctx::cap_free() {
   for (auto& L : cap)
     if (L.data) dfree(L.data, L.ndoubles * sizeof(double));
@@ -56,6 +70,7 @@ Ctx::~Ctx() {
   if (pin) cudaFreeHost(pin);
   if (pool) cudaMemPoolDestroy(pool);
   if (plog) std::fclose(plog);
+  if (rank_host) cudaFreeHost(rank_host);
 }
 
 double* Ctx::stack_ws(size_t ndoubles) {

@@ -93,6 +93,15 @@ struct Ctx {
   size_t zc_max = [] { const char* e = std::getenv("HM_ZERO_COPY"); return (e && e[0] == '1') ? (size_t)32 << 10 : (size_t)0; }();
   void* pinned(size_t bytes);
   void pinned_reset() { pin_used = 0; }
+  // Rank read-back of small TRUNC batches (the latency-bound factorization
+  // steps): the kernels write the ranks straight into mapped pinned host
+  // memory, so the host reads them after the stream synchronisation without a
+  // blocking cudaMemcpy.  One outstanding batch at a time (reset by the reader);
+  // nullptr if the batch is too large (the caller then uses device memory).
+  int* rank_host = nullptr;
+  size_t rank_cap = 0, rank_used = 0;
+  int* rank_alloc(size_t n);
+  bool rank_is_host(const int* p) const { return rank_host && p >= rank_host && p < rank_host + rank_cap; }
   // grow-only device workspace for the per-level stacks (one user at a time,
   // stream ordered): avoids re-mapping tens of GB every level
   double* ws = nullptr;

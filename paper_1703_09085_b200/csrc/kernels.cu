@@ -489,6 +489,19 @@ void launch_leaf_inverse(const LeafFactorJob* d_jobs, int njobs, int* fail, doub
   k_leaf_inverse<<<njobs, 256, (size_t)maxm * (maxm + 1) * 8, st>>>(d_jobs, fail, minpiv);
 }
 
+// table[patch[i].pos] = patch[i].leaf: the leaf descriptors of the blocks one
+// flush has rewritten, in ONE launch (instead of one H2D copy per block)
+__global__ void k_patch_leaves(LeafDesc* __restrict__ table, const LeafPatch* __restrict__ patch, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) table[patch[i].pos] = patch[i].leaf;
+}
+
+void launch_patch_leaves(LeafDesc* table, const LeafPatch* d_patch, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  k_patch_leaves<<<(n + 127) / 128, 128, 0, st>>>(table, d_patch, n);
+}
+
 // dst_i[0:count_i] = 0 for a list of device ranges (zeroing H-matrix blocks)
 __global__ void k_zero_ranges(double* const* __restrict__ ptr, const int64_t* __restrict__ cnt) {
   double* p = ptr[blockIdx.x];

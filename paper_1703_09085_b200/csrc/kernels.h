@@ -106,6 +106,12 @@ struct LeafDesc {
   const double* B;     // adm: n x k
 };
 
+struct LeafPatch {
+  int pos;             // index into a device leaf table
+  LeafDesc leaf;
+};
+void launch_patch_leaves(LeafDesc* table, const LeafPatch* d_patch, int n, cudaStream_t st);
+
 constexpr int kEvalRanges = 8;
 // out += coef * H|_{t x s} V   (trans=0; out rows = #t, V rows = #s) or
 // out += coef * H|_{t x s}^T V (trans=1; out rows = #s, V rows = #t),
