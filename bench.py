@@ -64,19 +64,31 @@ FACTOR_RUNS = [
 ]
 # profile class -> (kernel function, bound, what the class's convention work measures)
 CLASS_FUNCTION = {
-    "qr": ("k_qr_blocked+k_qr (Householder QR of the stacks, incl. TSQR)", "alu"),
+    "qr": ("k_qr_reg+k_qr_blocked+k_qr (Householder QR of the stacks, incl. TSQR)", "alu"),
     "jacobi_svd": ("k_svd (QRCP + one-sided Jacobi)", "alu"),
     "trunc_fused": ("k_trunc_small (fused TRUNC)", "alu"),
     "eval": ("k_eval2 (H x thin dense, addeval)", "hbm"),
-    "apply_q": ("k_applyq (reform A' = Q_A U)", "alu"),
+    "apply_q": ("k_applyq_dmma+k_applyq (reform A' = Q_A U)", "alu"),
     "gemm_M": ("k_gemm2 (M = R_A R_B^T)", "alu"),
     "dense_add": ("k_gemm2 (dense flush N += A B^T)", "alu"),
     "copy": ("k_copy (stack gathers)", "hbm"),
     "pre_qr_M": ("k_qr_blocked (pre-QR of large M)", "alu"),
 }
-NCU_NAME = {"qr": "k_qr_blocked", "jacobi_svd": "k_svd", "trunc_fused": "k_trunc_small", "eval": "k_eval2",
-            "apply_q": "k_applyq", "gemm_M": "k_gemm2", "dense_add": "k_gemm2", "copy": "k_copy",
-            "pre_qr_M": "k_qr_blocked"}
+NCU_NAME = {"qr": "k_qr_reg+k_qr_blocked+k_qr", "jacobi_svd": "k_svd", "trunc_fused": "k_trunc_small",
+            "eval": "k_eval2", "apply_q": "k_applyq_dmma+k_applyq", "gemm_M": "k_gemm2", "dense_add": "k_gemm2",
+            "copy": "k_copy", "pre_qr_M": "k_qr_reg+k_qr_blocked"}
+
+
+def ncu_function(tj, names):
+    """dram bytes per launch over the kernel functions `a+b+...` of one class
+    (profiles/*_traffic.json, scripts/ncu_traffic.py)."""
+    launches = byts = 0.0
+    for n in names.split("+"):
+        f = tj.get(n)
+        if f:
+            launches += f["launches"]
+            byts += f.get("dram_bytes", f["dram_bytes_per_launch"] * f["launches"])
+    return {"dram_bytes_per_launch": byts / launches} if launches else {}
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA/DMMA: SMs x FMA/clk x 2 x max clock
 CPU_SAMPLE_LEVEL = 5   # oracle sample: icosphere L5 (n = 20480) with config 4's leaf / eta / eps
 
@@ -288,7 +300,7 @@ def roofline_report(prof, dgemm_tf, peaks, traffic_file):
             achieved = p["flops"] / sec / 1e12
             peak, unit = dgemm_tf or NOMINAL_FP64_TFLOPS, "TFLOP/s"
             frac_nom = achieved / NOMINAL_FP64_TFLOPS
-        nc = tj.get(NCU_NAME.get(k, ""), {})
+        nc = ncu_function(tj, NCU_NAME.get(k, ""))
         algo_per_launch = p["bytes"] / p["launches"] if p["bytes"] else None
         rows.append({"class": k, "kernel": fn, "bound": bound, "ms": round(p["ms"], 3),
                      "share": round(p["ms"] / total_ms, 4) if total_ms else None, "launches": p["launches"],

@@ -376,7 +376,9 @@ struct Planner {
   }
 
   // Upload one prepared batch (jobs, range table, chained jobs of state E) and launch k_eval2.
-  void submit_evals(std::vector<EvalJob>& sorted, EmitState& E, Arena& scratch, double fl, double by) {
+  // aux >= 0: the kernel runs on auxiliary stream `aux` (forked after the uploads;
+  // the caller joins it), so consecutive batches overlap their tails
+  void submit_evals(std::vector<EvalJob>& sorted, EmitState& E, Arena& scratch, double fl, double by, int aux = -1) {
     if (sorted.empty()) return;
     const int2* drng = E.erng.empty() ? nullptr : scratch.upload_t(E.erng);
     EvalJob* dtail = nullptr;
@@ -394,8 +396,10 @@ struct Planner {
     }
     E.erng.clear();
     E.etail.clear();
-    ProfScope ps(c, PC_EVAL, fl, by);
-    launch_eval2(scratch.upload_t(sorted), (int)sorted.size(), c->stream);
+    const EvalJob* dj = scratch.upload_t(sorted);
+    cudaStream_t st = aux >= 0 ? c->fork(aux) : c->stream;
+    ProfScope ps(c, PC_EVAL, fl, by, st);
+    launch_eval2(dj, (int)sorted.size(), st);
     HM_CHECK_LAUNCH();
     sorted.clear();
   }
@@ -694,7 +698,7 @@ struct Planner {
         col += nd.terms[ti].w;
       }
     };
-    auto submit_copy = [&](std::vector<CopyJob>& cj, int64_t& ctiles) {
+    auto submit_copy = [&](std::vector<CopyJob>& cj, int64_t& ctiles, int aux = -1) {
       if (cj.empty()) return;
       double cb = 0;
       for (auto& j : cj) cb += 16.0 * j.rows * (j.identity ? 1 : j.cols);
@@ -703,9 +707,11 @@ struct Planner {
         const int64_t t1 = j + 1 < cj.size() ? cj[j + 1].tile0 : ctiles;
         std::fill(tmap.begin() + cj[j].tile0, tmap.begin() + t1, (int)j);
       }
-      ProfScope ps(c, PC_COPY, 0, cb);
       const CopyJob* dj = scratch.upload_t(cj);
-      launch_copy_mapped(dj, (int)cj.size(), scratch.upload_t(tmap), ctiles, c->stream);
+      const int* dm = scratch.upload_t(tmap);
+      cudaStream_t st = aux >= 0 ? c->fork(aux) : c->stream;
+      ProfScope ps(c, PC_COPY, 0, cb, st);
+      launch_copy_mapped(dj, (int)cj.size(), dm, ctiles, st);
       HM_CHECK_LAUNCH();
       cj.clear();
       ctiles = 0;
@@ -725,7 +731,11 @@ struct Planner {
         EmitState es;
         std::atomic<int> ready{0};
       };
-      const int np = host_threads * 6;
+      // parts of >= 16 K terms (a launch's tail is its largest job), at most 6 per
+      // thread; their kernels go round-robin to 4 auxiliary streams, so the
+      // tail of one part overlaps the head of the next
+      const int np = (int)std::max<size_t>(2, std::min<size_t>((size_t)host_threads * 6, nterms / 16384));
+      const bool par_streams = c->multi_stream();
       std::vector<Part> parts(np);
       {
         size_t si = 0, acc = 0;
@@ -763,16 +773,19 @@ struct Planner {
         while (!P.ready.load(std::memory_order_acquire)) std::this_thread::yield();
         if (failed) continue;
         try {
-          submit_copy(P.cj, P.ctiles);
+          const int aux = par_streams ? p % 4 : -1;
+          submit_copy(P.cj, P.ctiles, aux);
           fl_eval += P.es.fl;
           by_eval += P.es.by;
-          submit_evals(P.sorted, P.es, scratch, P.es.fl, P.es.by);
+          submit_evals(P.sorted, P.es, scratch, P.es.fl, P.es.by, aux);
         } catch (...) {   // join the workers before the error leaves this frame
           failed = true;
           eptr = std::current_exception();
         }
       }
       for (auto& th : pool) th.join();
+      if (par_streams)
+        for (int k = 0; k < 4; k++) c->join(k);
       if (eptr) std::rethrow_exception(eptr);
       if (failed) throw Error(HM_ESTRUCT, "internal: job emission failed");
       t2 = now_s();

@@ -15,7 +15,8 @@ timeout 1200 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram_
 echo "launch list exit $?"
 python scripts/ncu_traffic.py $OUT/${TAG}_launches.csv $OUT/${TAG}_traffic.json > $OUT/${TAG}_traffic.txt 2>&1
 head -25 $OUT/${TAG}_traffic.txt
-for spec in "_ZN2hm12k_qr_blockedILi256ELi2ELi4ELb0EE:qr768:1" "_ZN2hm12k_qr_blockedILi512ELi1ELi4ELb0EE:qr1536:1" \
+for spec in "_ZN2hm8k_qr_regILi256ELi3ELi1EEE:qr_reg768:1" "_ZN2hm8k_qr_regILi128ELi3ELi2EEE:qr_reg384:1" \
+            "_ZN2hm12k_qr_blockedILi512ELi1ELi4ELb0EE:qr1536:1" "_ZN2hm13k_applyq_dmma:applyq_dmma:2" \
             "_ZN2hm5k_svd:svd:3" "_ZN2hm13k_trunc_small:trunc_small:3" "_ZN2hm7k_eval2:eval2:3"; do
   IFS=: read -r rx name skip <<< "$spec"
   timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on \

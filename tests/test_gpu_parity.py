@@ -220,6 +220,35 @@ def test_addmul_parity(hm, ctx, L, leaf, eps, alpha):
         assert np.linalg.norm(Zg - ref) <= 1e-12 * np.linalg.norm(ref)
 
 
+def test_addmul_and_lr_bit_reproducible(hm, ctx, monkeypatch):
+    """No atomics, disjoint outputs per CTA (the lock-free update claim,
+    P:L1333-1336): repeated runs of the product (the level built by several
+    host threads: n = 5120 has levels above the 20 000-term threshold) and of
+    the H-LR give bit-identical ranks, factors and dense leaves."""
+    from hm_inputs import sphere_points
+    x, w = sphere_points(4)
+    G = ctx.build(x, w, 32, 2.0, 1e-4)
+    outs = []
+    for _ in range(2):
+        X, Y, Z = G.clone(), G.clone(), G.clone()
+        hm.addmul(1.0, X, Y, Z, 1e-4)
+        outs.append(Z.export())
+        for M in (X, Y, Z):
+            M.free()
+    assert np.array_equal(outs[0]["bl_rank"], outs[1]["bl_rank"])
+    assert np.array_equal(outs[0]["factors"], outs[1]["factors"])
+    assert np.array_equal(outs[0]["dense"], outs[1]["dense"])
+    outs = []
+    for _ in range(2):
+        F = G.clone()
+        hm.lr(F, 1e-4)
+        outs.append(F.export())
+        F.free()
+    assert np.array_equal(outs[0]["bl_rank"], outs[1]["bl_rank"])
+    assert np.array_equal(outs[0]["factors"], outs[1]["factors"])
+    assert np.array_equal(outs[0]["dense"], outs[1]["dense"])
+
+
 def test_addmul_distinct_operands(hm, ctx):
     """X != Y != Z (ragged random geometry, odd n)."""
     x, w = random_points(333, 4)
