@@ -15,12 +15,12 @@ timeout 1200 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram_
 echo "launch list exit $?"
 python scripts/ncu_traffic.py $OUT/${TAG}_launches.csv $OUT/${TAG}_traffic.json > $OUT/${TAG}_traffic.txt 2>&1
 head -25 $OUT/${TAG}_traffic.txt
-for spec in "_ZN2hm8k_qr_regILi256ELi3ELi1EEE:qr_reg768:1" "_ZN2hm8k_qr_regILi128ELi3ELi2EEE:qr_reg384:1" \
-            "_ZN2hm12k_qr_blockedILi512ELi1ELi4ELb0EE:qr1536:1" "_ZN2hm13k_applyq_dmma:applyq_dmma:2" \
-            "_ZN2hm5k_svd:svd:3" "_ZN2hm13k_trunc_small:trunc_small:3" "_ZN2hm7k_eval2:eval2:3"; do
-  IFS=: read -r rx name skip <<< "$spec"
+python scripts/ncu_pick.py $OUT/${TAG}_launches.csv > $OUT/${TAG}_specs.txt
+cat $OUT/${TAG}_specs.txt
+while IFS=: read -r rx name skip; do
+  [ -z "$rx" ] && continue
   timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on \
       --kernel-name-base mangled -k "regex:$rx" --launch-skip $skip -c 1 -o $OUT/${TAG}_${name} \
       python scripts/ncu_step.py load /tmp/cfgL.npz > $OUT/${TAG}_${name}.log 2>&1
   echo "full $name exit $?"
-done
+done < $OUT/${TAG}_specs.txt
