@@ -20,7 +20,7 @@ roofline of the top kernel functions; the standard (S0) product next to the
 accumulated one when available; the CPU oracle on all host cores.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 4|1] [--no-cpu-baseline] [--no-factor] [--no-flush]
+                    [--config 4|1] [--no-cpu-baseline] [--no-factor] [--no-flush] [--no-s0]
 
 `--impl reference` times the CPU oracle (oracle/, the reference arm of this
 tier) on a bounded sample of the same workload; it is test infrastructure,
@@ -521,6 +521,34 @@ def run_ours(args, cfg):
         except Exception as e:   # reported, never fatal for the main line
             flush = {"error": repr(e)}
 
+    # ---- standard (immediate-update, S0) product next to the accumulated one:
+    # the paper's central comparison (Fig. 9) --
+    # device seconds and truncation counts of ONE hm_addmul_std on the same
+    # operands (untimed for `value`; reported, never fatal)
+    s0 = None
+    if rank == 0 and not args.no_s0:
+        try:
+            Z0 = G.clone()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            hm.addmul_std(1.0, X, Y, Z0, cfg["eps"])
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            s0st = ctx.last_stats()
+            Z0.free()
+            s0_s = e0.elapsed_time(e1) / 1e3
+            s0 = {"s0_seconds": s0_s, "s2_seconds": ms_step / 1e3, "s0_over_s2": s0_s / (ms_step / 1e3),
+                  "s0_truncations": s0st["truncations"], "s2_truncations": st["truncations"],
+                  "s0_trunc_cols": s0st["trunc_cols"], "s2_trunc_cols": st["trunc_cols"],
+                  "s0_convention_gflop": (s0st["flops_trunc"] + s0st["flops_eval"] + s0st["flops_dense"]) / 1e9,
+                  "note": "hm_addmul_std (standard algorithm, one truncation per update) vs hm_addmul "
+                          "(accumulated updates) on the same operands; paper: factor 2-3 (P:L1672-1675)"}
+            log(f"S0 product {s0_s:.2f}s, {s0st['truncations']} truncations")
+        except Exception as e:
+            s0 = {"error": repr(e)}
+
     # ---- H-LR / H-Cholesky setup seconds (BASELINE configs[1], [2], [4] and the
     # metric's n = 81920 H-LR, "config 4'"), device time with CUDA events
     factor = {}
@@ -579,6 +607,7 @@ def run_ours(args, cfg):
             "roofline": roof,
             "hlr_hchol_setup": factor,
             "standalone_flush": flush,
+            "s0_vs_s2": s0,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -610,6 +639,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-factor", action="store_true", help="skip the H-LR / H-Cholesky setup timings")
     ap.add_argument("--no-flush", action="store_true", help="skip the standalone batched-flush timing")
+    ap.add_argument("--no-s0", action="store_true", help="skip the standard (S0) product comparison")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # replicas only (the path does not shard): spawn one rank per GPU

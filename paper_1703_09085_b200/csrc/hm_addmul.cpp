@@ -1302,14 +1302,13 @@ struct Factorizer {
       if (f < 0) throw Error(HM_ESTRUCT, "internal: flush produced no result");
       const FP& fp = P.fps[f];
       const int m = fp.lda, n = fp.ldb, k = fp.k;
-      const size_t bytes = sizeof(double) * ((size_t)(m + n) * k + 1);
-      double* buf = static_cast<double*>(c->dmalloc(bytes));
+      // bump allocation from the planner's heap arena (64 MB chunks, released
+      // with the factorization): no cudaMallocAsync / cudaFreeAsync per block
+      double* buf = P.heap.alloc((size_t)(m + n) * k + 1);
       if (k > 0) {
         P.add_copy(cj, ctiles, buf, m, fp.A, m, m, k, 0, 0, 1.0);
         P.add_copy(cj, ctiles, buf + (size_t)m * k, n, fp.B, n, n, k, 0, 0, 1.0);
       }
-      if (own[zb].first) c->dfree(own[zb].first, own[zb].second);
-      own[zb] = {buf, bytes};
       G->pA[zb] = buf;
       G->pB[zb] = buf + (size_t)m * k;
       G->rank[zb] = k;
@@ -1400,7 +1399,7 @@ struct Factorizer {
     std::vector<TrsmStep> st;
     if (mode == 1) steps_rt(t, T.cl_start[t], st);
     else steps_lower(t, mode == 0, T.cl_start[t], st);
-    Arena ar(c);
+    Arena ar(c, true);
     std::vector<TrsmJob> jb{TrsmJob{V, ldv, ncols, T.cl_start[t], 0, (int)st.size()}};
     trsm_launch(ar.upload_t(jb), 1, ar.upload_t(st), dlt, c->stream);
     HM_CHECK_LAUNCH();
@@ -1410,7 +1409,7 @@ struct Factorizer {
     n_leaf++;
     const int d = blk(t, t);
     const int m = T.cl_size[t];
-    Arena ar(c);
+    Arena ar(c, true);
     std::vector<LeafFactorJob> j{LeafFactorJob{G->pA[d], m, m, t}};
     launch_leaf_factor(ar.upload_t(j), 1, chol ? 1 : 0, d_fail, d_minpiv + t, m, c->stream);
     HM_CHECK_LAUNCH();
@@ -1426,7 +1425,7 @@ struct Factorizer {
 
   void trsm_set(int t, const std::vector<std::pair<int, int>>& targets) {   // (block, mode)
     if (targets.empty()) return;
-    Arena ar(c);
+    Arena ar(c, true);
     std::vector<TrsmStep> st;
     int rng[3][2] = {{-1, -1}, {-1, -1}, {-1, -1}};
     for (auto& tg : targets) {

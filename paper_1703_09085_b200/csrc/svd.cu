@@ -22,6 +22,7 @@
 //      Q [V_k S_k; 0] (one product with the R kept in C, then the stored
 //      reflectors).
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <math.h>
 #include <stdint.h>
 #include <cstdio>
@@ -71,6 +72,11 @@ __device__ int g_ph_n;
 // fused TRUNC: no stack QR when m, n <= this (0 = always QR the thin side;
 // measured: skipping it does not shorten the H-LR critical path)
 static constexpr int kNoQrRows = 0;
+
+// Address-space hint: the pointer is known to address shared memory, so the
+// compiler emits LDS / STS instead of generic LD / ST (ncu: the generic
+// accesses of svd_core were its long-scoreboard stalls).
+#define HM_ASSUME_SHARED(p) __builtin_assume(__isShared(p))
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -203,8 +209,9 @@ __device__ __forceinline__ void jacobi_rot(double al, double be, double ga, doub
 // X (c x rt, ld ldx).  One group of G lanes per column pair; each lane keeps
 // its E elements of both columns in registers for the rotation (c <= E G).
 // Returns the number of sweeps.
-template <int G, int E>
+template <int G, int E, bool kSm>
 __device__ int jacobi_sweeps(double* X, int ldx, int c, int rt, double tol2, double delta2, int NW) {
+  if (kSm) HM_ASSUME_SHARED(X);
   const double tol = sqrt(tol2);
   // called by the first NW warps of the CTA only (sub_sync)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -321,8 +328,20 @@ __device__ int jacobi_sweeps_stream(double* X, int ldx, int c, int rt, double to
 // shared memory for the QRCP, is then moved to `spill` (global memory; R and
 // the reflectors are only read again by the output phase) and X = R^T takes
 // its place (X == the shared-memory address of C on entry).
+// kMode 0: C / X / the small arrays anywhere (global workspace); 1: all in
+// shared memory; 2: spill mode (shared memory, C parked in `spill` after the QRCP).
+template <int kMode>
 __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, int L, int c, double* C, int ldc, double* X,
                          double* tau, double* nrm, double* sig, int* perm, int* order, double* spill = nullptr) {
+  if (kMode >= 1) {
+    HM_ASSUME_SHARED(C);
+    HM_ASSUME_SHARED(X);
+    HM_ASSUME_SHARED(tau);
+    HM_ASSUME_SHARED(nrm);
+    HM_ASSUME_SHARED(sig);
+    HM_ASSUME_SHARED(perm);
+    HM_ASSUME_SHARED(order);
+  }
   __shared__ double red[32];
   __shared__ int s_rank;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -375,6 +394,7 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   // barrier); the others wait at the block barrier below.
   __shared__ int s_rt;
   int rt = 0;
+  const bool qregs = L <= kE * Gq;   // rows per lane of a column group fit the register slices
   const int nwq = g_subwarps ? min(NW, max(1, (c * Gq + 31) >> 5)) : NW;
   const int NTq = nwq * 32;
   if (warp < nwq) {
@@ -431,13 +451,47 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
       const bool act = col < c;
       double* y = C + (int64_t)(act ? col : j) * ldc;
       double d = 0.0;
+      double nn = 0.0, nn2 = 0.0;
+      if (qregs) {
+        // <= kE rows per lane: the lane's slices of x and y stay in registers
+        // between the dot product and the update (same operation order as the
+        // streamed loops below: bit-identical)
+        double xr[kE], yr[kE];
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int i = j + 1 + gq + u * Gq;
+          const bool ok = act && i < L;
+          xr[u] = ok ? x[i] : 0.0;
+          yr[u] = ok ? y[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kE; u++) d = fma(xr[u], yr[u], d);
+        d = gsum(d, Gq);
+        const double yj = act ? y[j] : 0.0;
+        d = t != 0.0 ? fma(tsc, d, t * yj) : 0.0;   // tau (y_j + v.y), v = sc x below j
+        const double ds = d * sc;
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int i = j + 1 + gq + u * Gq;
+          if (act && i < L) {
+            const double yi = fma(-ds, xr[u], yr[u]);
+            y[i] = yi;
+            nn = fma(yi, yi, nn);
+            if (u > 0 || gq > 0) nn2 = fma(yi, yi, nn2);
+          }
+        }
+        nn = gsum(nn, Gq);
+        nn2 = gsum(nn2, Gq);
+        __syncwarp();
+        if (act && gq == 0) { y[j] = yj - d; nrm[col] = nn; nrm2[col] = nn2; }
+        continue;
+      }
       if (act && t != 0.0)
         for (int i = j + 1 + gq; i < L; i += Gq) d = fma(x[i], y[i], d);
       d = gsum(d, Gq);
       const double yj = act ? y[j] : 0.0;
       d = t != 0.0 ? fma(tsc, d, t * yj) : 0.0;   // tau (y_j + v.y), v = sc x below j
       const double ds = d * sc;
-      double nn = 0.0, nn2 = 0.0;
       if (act)
         for (int i = j + 1 + gq; i < L; i += Gq) {
           const double yi = fma(-ds, x[i], y[i]);
@@ -464,21 +518,22 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   }
   __syncthreads();
   rt = s_rt;
-  if (spill) {
+  const double* Cg = C;   // R and the reflectors from here on (spill mode: in global memory)
+  if (kMode == 2) {
     // columns < rt whole (reflectors + R), the others only their R rows
     for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
       const int i = (int)(e % L), col = (int)(e / L);
       if (col < rt || i < rt) spill[i + (int64_t)col * ldc] = C[i + (int64_t)col * ldc];
     }
     __syncthreads();
-    C = spill;
+    Cg = spill;
   }
   PHASE("qrcp");
   // X = R^T (c x rt, ld ldx)
   const int ldx = pad_ld(c);
   for (int64_t e = tid; e < (int64_t)c * rt; e += NT) {
     const int col = (int)(e % c), i = (int)(e / c);
-    X[col + (int64_t)i * ldx] = (col >= i) ? C[i + (int64_t)col * ldc] : 0.0;
+    X[col + (int64_t)i * ldx] = (col >= i) ? Cg[i + (int64_t)col * ldc] : 0.0;
   }
   __syncthreads();
   // ---------------------------------------------------------------- 2. Jacobi
@@ -499,9 +554,9 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   } else {
     const int nwj = g_subwarps ? min(NW, max(1, ((cp >> 1) * G + 31) >> 5)) : NW;
     if (warp < nwj) {
-      if (G == 8) sweep = jacobi_sweeps<8, 8>(X, ldx, c, rt, tol2, delta2, nwj);
-      else if (G == 16) sweep = jacobi_sweeps<16, 8>(X, ldx, c, rt, tol2, delta2, nwj);
-      else sweep = jacobi_sweeps<32, 8>(X, ldx, c, rt, tol2, delta2, nwj);
+      if (G == 8) sweep = jacobi_sweeps<8, 8, (kMode >= 1)>(X, ldx, c, rt, tol2, delta2, nwj);
+      else if (G == 16) sweep = jacobi_sweeps<16, 8, (kMode >= 1)>(X, ldx, c, rt, tol2, delta2, nwj);
+      else sweep = jacobi_sweeps<32, 8, (kMode >= 1)>(X, ldx, c, rt, tol2, delta2, nwj);
     }
     __syncthreads();
   }
@@ -580,20 +635,20 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   // reflectors are applied
   // spill mode: R and the reflectors come back into the shared memory behind X
   // when they fit (rt <~ 0.38 c), else they are read from global memory / L2
-  const double* Clo = C;                        // columns < rt (reflectors + R), ld ldc
-  const double* Rhi = C + (int64_t)rt * ldc;    // columns >= rt (rows < rt of R), ld ldh
+  const double* Clo = Cg;                       // columns < rt (reflectors + R), ld ldc
+  const double* Rhi = Cg + (int64_t)rt * ldc;   // columns >= rt (rows < rt of R), ld ldh
   int ldh = ldc;
-  if (spill) {
+  if (kMode == 2) {
     double* S = X + (int64_t)ldx * rt;
     if ((int64_t)ldx * rt + (int64_t)ldc * rt + (int64_t)rt * (c - rt) <= (int64_t)ldc * c) {
       double* S2 = S + (int64_t)ldc * rt;
       for (int64_t e = tid; e < (int64_t)L * rt; e += NT) {
         const int i = (int)(e % L), col = (int)(e / L);
-        S[i + (int64_t)col * ldc] = C[i + (int64_t)col * ldc];
+        S[i + (int64_t)col * ldc] = Cg[i + (int64_t)col * ldc];
       }
       for (int64_t e = tid; e < (int64_t)rt * (c - rt); e += NT) {
         const int i = (int)(e % rt), col = (int)(e / rt);
-        S2[i + (int64_t)col * rt] = C[i + (int64_t)(rt + col) * ldc];
+        S2[i + (int64_t)col * rt] = Cg[i + (int64_t)(rt + col) * ldc];
       }
       __syncthreads();
       Clo = S;
@@ -704,19 +759,30 @@ __global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, do
   const int64_t need = svd_ws(L, c);
   const bool fits = need <= cap;
   const bool spillm = !fits && J.work && (int64_t)ldc * c + 6 * (int64_t)c <= cap;
-  double* C = (fits || spillm) ? sm : J.work;   // L x c (ld ldc), QRCP in place
-  double* X = spillm ? sm : C + (int64_t)ldc * c;   // c x rt  (R^T, then W)
-  double* tau = spillm ? sm + (int64_t)ldc * c : X + (int64_t)pad_ld(c) * c;     // c
-  double* nrm = tau + c;                        // c
-  double* sig = nrm + c;                        // c
-  int* perm = reinterpret_cast<int*>(sig + c);  // c
-  int* order = perm + c;                        // c
-  for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
-    const int i = (int)(e % L), j = (int)(e / L);
-    const int mi = tr ? j : i, mj = tr ? i : j;   // entry (mi, mj) of M
-    C[i + (int64_t)j * ldc] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
+  // The pointers of the shared-memory modes are derived from `sm` directly (not
+  // through a select with J.work): svd_core is inlined per mode and its
+  // accesses compile to LDS / STS instead of generic LD / ST.
+  auto run = [&](auto mode, double* C, double* X, double* small) {
+    double* tau = small;                          // c
+    double* nrm = tau + c;                        // c
+    double* sig = nrm + c;                        // c
+    int* perm = reinterpret_cast<int*>(sig + c);  // c
+    int* order = perm + c;                        // c
+    for (int64_t e = tid; e < (int64_t)L * c; e += NT) {
+      const int i = (int)(e % L), j = (int)(e / L);
+      const int mi = tr ? j : i, mj = tr ? i : j;   // entry (mi, mj) of M
+      C[i + (int64_t)j * ldc] = (J.maskM && mi > mj) ? 0.0 : J.M[mi + (int64_t)mj * J.ldm];
+    }
+    svd_core<decltype(mode)::value>(J, eps, drop_rel, tr, L, c, C, ldc, X, tau, nrm, sig, perm, order, J.work);
+  };
+  if (fits) {          // C (L x c, ld ldc), X (c x rt: R^T, then W), small arrays: all in shared memory
+    run(std::integral_constant<int, 1>{}, sm, sm + (int64_t)ldc * c, sm + (int64_t)ldc * c + (int64_t)pad_ld(c) * c);
+  } else if (spillm) { // X takes C's place after the QRCP
+    run(std::integral_constant<int, 2>{}, sm, sm, sm + (int64_t)ldc * c);
+  } else {             // global workspace
+    double* W = J.work;
+    run(std::integral_constant<int, 0>{}, W, W + (int64_t)ldc * c, W + (int64_t)ldc * c + (int64_t)pad_ld(c) * c);
   }
-  svd_core(J, eps, drop_rel, tr, L, c, C, ldc, X, tau, nrm, sig, perm, order, spillm ? J.work : nullptr);
   PHASE_FLUSH;
 }
 
@@ -726,6 +792,9 @@ __global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, do
 // groups of G lanes update one column each, and the scaling of the reflector
 // is deferred to the next step (all groups read it during its own step).
 __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* tau, double* nrm2) {
+  HM_ASSUME_SHARED(A);
+  HM_ASSUME_SHARED(tau);
+  HM_ASSUME_SHARED(nrm2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
   const int G = col_group(rows), gl = lane & (G - 1), gpw = 32 / G;
   for (int base = warp * gpw; base < cols; base += NW * gpw) {
@@ -738,6 +807,7 @@ __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* ta
   }
   __syncthreads();
   // the Householder steps run on the warps that have a column group (named barrier)
+  const bool hregs = rows <= kE * G;
   const int nwa = g_subwarps ? min(NW, max(1, (cols * G + 31) >> 5)) : NW;
   const int NTa = nwa * 32;
   if (warp < nwa) {
@@ -766,13 +836,42 @@ __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* ta
       const bool act = col < cols;
       double* y = A + (int64_t)(act ? col : j) * lda;
       double d = 0.0;
+      double nn2 = 0.0;
+      if (hregs) {   // register slices of x and y (see svd_core's QRCP update; bit-identical)
+        double xr[kE], yr[kE];
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int i = j + 1 + gl + u * G;
+          const bool ok = act && i < rows;
+          xr[u] = ok ? x[i] : 0.0;
+          yr[u] = ok ? y[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kE; u++) d = fma(xr[u], yr[u], d);
+        d = gsum(d, G);
+        const double yj = act ? y[j] : 0.0;
+        d = t != 0.0 ? fma(tsc, d, t * yj) : 0.0;
+        const double ds = d * sc;
+#pragma unroll
+        for (int u = 0; u < kE; u++) {
+          const int i = j + 1 + gl + u * G;
+          if (act && i < rows) {
+            const double yi = fma(-ds, xr[u], yr[u]);
+            y[i] = yi;
+            if (u > 0 || gl > 0) nn2 = fma(yi, yi, nn2);
+          }
+        }
+        nn2 = gsum(nn2, G);
+        __syncwarp();
+        if (act && gl == 0) { y[j] = yj - d; nrm2[col] = nn2; }
+        continue;
+      }
       if (act && t != 0.0)
         for (int i = j + 1 + gl; i < rows; i += G) d = fma(x[i], y[i], d);
       d = gsum(d, G);
       const double yj = act ? y[j] : 0.0;
       d = t != 0.0 ? fma(tsc, d, t * yj) : 0.0;
       const double ds = d * sc;
-      double nn2 = 0.0;
       if (act)
         for (int i = j + 1 + gl; i < rows; i += G) {
           const double yi = fma(-ds, x[i], y[i]);
@@ -801,6 +900,8 @@ __device__ void house_qr_smem(double* A, int rows, int lda, int cols, double* ta
 // registers (row gl + u G in slot u) while the r reflectors are applied.
 __device__ void apply_q_smem(const double* Vr, int ldv, const double* tau, int rows, int r, double* X, int ldx,
                              int k) {
+  HM_ASSUME_SHARED(Vr);
+  HM_ASSUME_SHARED(tau);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
   const int G = col_group(rows), gl = lane & (G - 1), gpw = 32 / G;
   const bool inreg = rows <= kE * G;
@@ -963,7 +1064,7 @@ __global__ void __launch_bounds__(512) k_trunc_small(const TruncSmallJob* __rest
   S.Bout = tall ? J.Bout : J.Aout;
   S.ldb = tall ? n : m;
   S.nb = S.ldb;
-  svd_core(S, eps, drop_rel, false, L, c, C, ldc, X, tau, nrm, sig, perm, order);
+  svd_core<1>(S, eps, drop_rel, false, L, c, C, ldc, X, tau, nrm, sig, perm, order);
   __syncthreads();
   const int k = *J.rank;
   if (qa) apply_q_smem(sA, lda, tA, m, l, J.Aout, m, k);

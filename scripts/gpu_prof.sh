@@ -23,4 +23,10 @@ while IFS=: read -r rx name skip; do
       --kernel-name-base mangled -k "regex:$rx" --launch-skip $skip -c 1 -o $OUT/${TAG}_${name} \
       python scripts/ncu_step.py load /tmp/cfgL.npz > $OUT/${TAG}_${name}.log 2>&1
   echo "full $name exit $?"
+  # gpurun_out is limited to 64 MiB: keep the CSV exports, not the reports
+  if [ -f $OUT/${TAG}_${name}.ncu-rep ]; then
+    ncu -i $OUT/${TAG}_${name}.ncu-rep --page details --csv > $OUT/${TAG}_k_${name}_full_details.csv 2>/dev/null
+    python scripts/ncu_src.py $OUT/${TAG}_${name}.ncu-rep 25 > $OUT/${TAG}_k_${name}_source_summary.txt 2>/dev/null
+    rm -f $OUT/${TAG}_${name}.ncu-rep
+  fi
 done < $OUT/${TAG}_specs.txt
