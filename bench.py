@@ -521,34 +521,7 @@ def run_ours(args, cfg):
         except Exception as e:   # reported, never fatal for the main line
             flush = {"error": repr(e)}
 
-    # ---- standard (immediate-update, S0) product next to the accumulated one:
-    # the paper's central comparison (Fig. 9) --
-    # device seconds and truncation counts of ONE hm_addmul_std on the same
-    # operands (untimed for `value`; reported, never fatal)
     s0 = None
-    if rank == 0 and not args.no_s0:
-        try:
-            Z0 = G.clone()
-            torch.cuda.synchronize(dev)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            hm.addmul_std(1.0, X, Y, Z0, cfg["eps"])
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-            s0st = ctx.last_stats()
-            Z0.free()
-            s0_s = e0.elapsed_time(e1) / 1e3
-            s0 = {"s0_seconds": s0_s, "s2_seconds": ms_step / 1e3, "s0_over_s2": s0_s / (ms_step / 1e3),
-                  "s0_truncations": s0st["truncations"], "s2_truncations": st["truncations"],
-                  "s0_trunc_cols": s0st["trunc_cols"], "s2_trunc_cols": st["trunc_cols"],
-                  "s0_convention_gflop": (s0st["flops_trunc"] + s0st["flops_eval"] + s0st["flops_dense"]) / 1e9,
-                  "note": "hm_addmul_std (standard algorithm, one truncation per update) vs hm_addmul "
-                          "(accumulated updates) on the same operands; paper: factor 2-3 (P:L1672-1675)"}
-            log(f"S0 product {s0_s:.2f}s, {s0st['truncations']} truncations")
-        except Exception as e:
-            s0 = {"error": repr(e)}
-
     # ---- H-LR / H-Cholesky setup seconds (BASELINE configs[1], [2], [4] and the
     # metric's n = 81920 H-LR, "config 4'"), device time with CUDA events
     factor = {}
@@ -582,6 +555,41 @@ def run_ours(args, cfg):
                            "truncations": fst["truncations"], "trunc_cols": fst["trunc_cols"],
                            "convention_gflop": fgf, "gflops": fgf / min(times), "min_pivot": fst["min_pivot"],
                            "build_s": tb}
+
+    # ---- standard (immediate-update, S0) product next to the accumulated one:
+    # the paper's central comparison (Fig. 9).  The
+    # device S0 evaluates every term up front into one pool, which does not
+    # fit one GPU at config 4 (n = 81920), so both products run on the
+    # n = 20480 member of the same family (leaf, eta, eps of config 4) -- last
+    # on the device, reported, never fatal.
+    if rank == 0 and not args.no_s0:
+        try:
+            xs, wsf = sphere_points(5 if cfg["level"] >= 6 else cfg["level"])
+            Gs = ctx.build(xs, wsf, cfg["leaf"], cfg["eta"], cfg["eps"])
+            Xs, Ys = Gs.clone(), Gs.clone()
+            res = {}
+            for name, fn in (("s2", hm.addmul), ("s0", hm.addmul_std), ("s2", hm.addmul), ("s0", hm.addmul_std)):
+                Zs = Gs.clone()
+                torch.cuda.synchronize(dev)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn(1.0, Xs, Ys, Zs, cfg["eps"])
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                sst = ctx.last_stats()
+                Zs.free()
+                res[name] = (e0.elapsed_time(e1) / 1e3, sst["truncations"], sst["trunc_cols"])
+            Xs.free(), Ys.free(), Gs.free()
+            s0 = {"n": len(wsf), "leaf": cfg["leaf"], "eps": cfg["eps"],
+                  "s0_seconds": res["s0"][0], "s2_seconds": res["s2"][0], "s0_over_s2": res["s0"][0] / res["s2"][0],
+                  "s0_truncations": res["s0"][1], "s2_truncations": res["s2"][1],
+                  "s0_trunc_cols": res["s0"][2], "s2_trunc_cols": res["s2"][2],
+                  "note": "hm_addmul_std (standard algorithm, one truncation per update) vs hm_addmul "
+                          "(accumulated updates), second run of each; paper: factor 2-3 (P:L1672-1675)"}
+            log(f"S0 {res['s0'][0]:.2f}s / S2 {res['s2'][0]:.2f}s at n={len(wsf)}")
+        except Exception as e:
+            s0 = {"error": repr(e)}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -89,7 +89,10 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_qr_reg(const QrJob* __restr
     // ---- 2. Householder steps, one barrier per column
 #pragma unroll
     for (int j = 0; j < kNb; j++) {
-      if (j < kb) {   // uniform
+      {   // straight-line code for all 16 steps: the columns >= kb of a short last
+          // panel are zero (tau = 0, no effect), and a column without entries
+          // below the diagonal gets sc = 0 -- no (uniform) branches, whose
+          // convergence barriers were 24 % of the sampled stalls (ncu r2z)
         // slot q (>= j): x . y_q over the rows below the diagonal (x = column j)
         double part[kNb];
 #pragma unroll
@@ -153,23 +156,23 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_qr_reg(const QrJob* __restr
         double d[kNb];
 #pragma unroll
         for (int q = j + 1; q < kNb; q++) d[q] = __shfl_sync(0xffffffffu, dq, q);
-        if (tid == 0) { J.tau[k0 + j] = t; stau[j] = t; }
-        if (t != 0.0) {
+        if (tid == 0) {
+          stau[j] = t;
+          if (j < kb) J.tau[k0 + j] = t;
+        }
+        // t = 0 (nothing below the diagonal): sc = 0, d = 0 -- the updates are no-ops
 #pragma unroll
-          for (int u = 0; u < kRPT; u++) {
-            const bool below = u > 0 || tid > j;
-            if (below) {
-              const double vi = a[u][j] * sc;
-              a[u][j] = vi;
+        for (int u = 0; u < kRPT; u++) {
+          const bool below = u > 0 || tid > j;
+          const double vi = below ? a[u][j] * sc : 0.0;
+          if (below) a[u][j] = vi;
 #pragma unroll
-              for (int q = j + 1; q < kNb; q++) a[u][q] = fma(-d[q], vi, a[u][q]);
-            }
-          }
-          if (tid == j) {
-            a[0][j] = beta;
+          for (int q = j + 1; q < kNb; q++) a[u][q] = fma(-d[q], vi, a[u][q]);
+        }
+        if (tid == j) {
+          a[0][j] = beta;
 #pragma unroll
-            for (int q = j + 1; q < kNb; q++) a[0][q] -= d[q];
-          }
+          for (int q = j + 1; q < kNb; q++) a[0][q] -= d[q];
         }
       }
     }

@@ -554,9 +554,16 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   } else {
     const int nwj = g_subwarps ? min(NW, max(1, ((cp >> 1) * G + 31) >> 5)) : NW;
     if (warp < nwj) {
-      if (G == 8) sweep = jacobi_sweeps<8, 8, (kMode >= 1)>(X, ldx, c, rt, tol2, delta2, nwj);
-      else if (G == 16) sweep = jacobi_sweeps<16, 8, (kMode >= 1)>(X, ldx, c, rt, tol2, delta2, nwj);
-      else sweep = jacobi_sweeps<32, 8, (kMode >= 1)>(X, ldx, c, rt, tol2, delta2, nwj);
+      // register slices per lane: ceil(c / G), instantiated for 4 / 6 / 8
+      // (predicated-off slices still cost their issue slots)
+      constexpr bool sm = kMode >= 1;
+      if (G == 8) sweep = c <= 32 ? jacobi_sweeps<8, 4, sm>(X, ldx, c, rt, tol2, delta2, nwj)
+                                  : (c <= 48 ? jacobi_sweeps<8, 6, sm>(X, ldx, c, rt, tol2, delta2, nwj)
+                                             : jacobi_sweeps<8, 8, sm>(X, ldx, c, rt, tol2, delta2, nwj));
+      else if (G == 16) sweep = c <= 96 ? jacobi_sweeps<16, 6, sm>(X, ldx, c, rt, tol2, delta2, nwj)
+                                        : jacobi_sweeps<16, 8, sm>(X, ldx, c, rt, tol2, delta2, nwj);
+      else sweep = c <= 192 ? jacobi_sweeps<32, 6, sm>(X, ldx, c, rt, tol2, delta2, nwj)
+                            : jacobi_sweeps<32, 8, sm>(X, ldx, c, rt, tol2, delta2, nwj);
     }
     __syncthreads();
   }
