@@ -47,6 +47,7 @@ static double drop_rel_host() {
 __device__ long long g_ph_cyc[32];
 __device__ const char* g_ph_name[32];
 __device__ int g_ph_n;
+__device__ int g_ph_info[5];   // L, c, rt, sweeps, G of CTA 0's svd_core
 #define PHASE(name)                                                                        \
   do {                                                                                     \
     __syncthreads();                                                                       \
@@ -60,6 +61,7 @@ __device__ int g_ph_n;
 #define PHASE_FLUSH                                                                        \
   do {                                                                                     \
     if (blockIdx.x == 0 && threadIdx.x == 0) {                                             \
+      printf("[phase] L=%d c=%d rt=%d sweeps=%d G=%d\n", g_ph_info[0], g_ph_info[1], g_ph_info[2], g_ph_info[3], g_ph_info[4]); \
       for (int i_ = 0; i_ < g_ph_n; i_++) printf("[phase] %-10s %8lld cycles\n", g_ph_name[i_], g_ph_cyc[i_]); \
       g_ph_n = 0;                                                                          \
     }                                                                                      \
@@ -331,7 +333,7 @@ __device__ int jacobi_sweeps_stream(double* X, int ldx, int c, int rt, double to
 // kMode 0: C / X / the small arrays anywhere (global workspace); 1: all in
 // shared memory; 2: spill mode (shared memory, C parked in `spill` after the QRCP).
 template <int kMode>
-__device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, int L, int c, double* C, int ldc, double* X,
+__device__ int svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, int L, int c, double* C, int ldc, double* X,
                          double* tau, double* nrm, double* sig, int* perm, int* order, double* spill = nullptr) {
   if (kMode >= 1) {
     HM_ASSUME_SHARED(C);
@@ -746,8 +748,9 @@ __device__ void svd_core(const SvdJob& J, double eps, double drop_rel, bool tr, 
   }
   PHASE("output");
 #ifdef HM_PHASE_TIMING
-  if (blockIdx.x == 0 && tid == 0) printf("[phase] L=%d c=%d rt=%d sweeps=%d G=%d\n", L, c, rt, sweep, G);
+  if (blockIdx.x == 0 && tid == 0) { g_ph_info[0] = L; g_ph_info[1] = c; g_ph_info[2] = rt; g_ph_info[3] = sweep; g_ph_info[4] = G; }
 #endif
+  return k;   // the rank (every thread has it from shared memory)
 }
 
 __global__ void __launch_bounds__(512) k_svd(const SvdJob* __restrict__ jobs, double eps, double drop_rel, int cap) {
@@ -923,6 +926,9 @@ __device__ void apply_q_smem(const double* Vr, int ldv, const double* tau, int r
         const int i = gl + u * G;
         xr[u] = (act && i < rows) ? x[i] : 0.0;
       }
+#ifdef HM_PHASE_TIMING
+      const long long aq_t0 = clock64();
+#endif
       for (int j = r - 1; j >= 0; j--) {
         const double t = tau[j];
         if (t == 0.0) continue;
@@ -945,6 +951,9 @@ __device__ void apply_q_smem(const double* Vr, int ldv, const double* tau, int r
           else if (i == j) xr[u] -= d;
         }
       }
+#ifdef HM_PHASE_TIMING
+      if (blockIdx.x == 0 && threadIdx.x == 0 && g_ph_n < 32) { g_ph_cyc[g_ph_n] = clock64() - aq_t0; g_ph_name[g_ph_n++] = "aq_loop_w0"; }
+#endif
       if (act)
 #pragma unroll
         for (int u = 0; u < kE; u++) {
@@ -1071,9 +1080,10 @@ __global__ void __launch_bounds__(512) k_trunc_small(const TruncSmallJob* __rest
   S.Bout = tall ? J.Bout : J.Aout;
   S.ldb = tall ? n : m;
   S.nb = S.ldb;
-  svd_core<1>(S, eps, drop_rel, false, L, c, C, ldc, X, tau, nrm, sig, perm, order);
+  // (the rank comes back in a register instead of a global-memory re-read)
+  const int k = svd_core<1>(S, eps, drop_rel, false, L, c, C, ldc, X, tau, nrm, sig, perm, order);
   __syncthreads();
-  const int k = *J.rank;
+  PHASE("svd_core");   // (this function's own clock: the whole svd_core since "gemm_M")
   if (qa) apply_q_smem(sA, lda, tA, m, l, J.Aout, m, k);
   if (qb) apply_q_smem(sB, ldb, tB, n, l, J.Bout, n, k);
   PHASE("apply_q");
