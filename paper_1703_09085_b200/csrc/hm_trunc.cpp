@@ -145,11 +145,11 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   // chunk remains.  Same factorisation A = Q R (Q = blockdiag(Q_chunks) Q_stack,
   // R = the last level's R), but the single-CTA row sweep over thousands of
   // rows becomes nch independent CTAs.
-  static const int ts_min_b = [] { const char* e = std::getenv("HM_TSQR_ROWS"); return e ? std::atoi(e) : 1536; }();
+  static const int ts_min_b = [] { const char* e = std::getenv("HM_TSQR_ROWS"); return e ? std::atoi(e) : 768; }();
   static const int ts_h_b = [] { const char* e = std::getenv("HM_TSQR_H"); return e ? std::atoi(e) : 768; }();
   // small batches (latency-bound, e.g. the H-LR critical path) may cut tall
   // factors into more, shorter chunks (more CTAs on one QR)
-  static const int ts_min_l = [] { const char* e = std::getenv("HM_TSQR_ROWS_LAT"); return e ? std::atoi(e) : 1536; }();
+  static const int ts_min_l = [] { const char* e = std::getenv("HM_TSQR_ROWS_LAT"); return e ? std::atoi(e) : 768; }();
   static const int ts_h_l = [] { const char* e = std::getenv("HM_TSQR_H_LAT"); return e ? std::atoi(e) : 768; }();
   static const int ts_even = [] { const char* e = std::getenv("HM_TSQR_EVEN"); return e ? std::atoi(e) : 1; }();
   const bool lat_batch = nj < 64;
