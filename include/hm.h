@@ -155,6 +155,11 @@ hm_status hm_ctx_create(int device, void* cuda_stream, const hm_allocator* alloc
 hm_status hm_ctx_destroy(hm_ctx ctx);
 const char* hm_last_error(hm_ctx ctx);
 hm_status hm_sync(hm_ctx ctx);
+/* Synchronises the stream and gives back the context's grow-only workspaces
+ * (level stacks, LIFO pool, captured flush batches) and the memory its private
+ * pool has cached; live hm_mat handles are untouched.  The next operation
+ * re-grows what it needs.  hm_build / hm_build_nrm call it first. */
+hm_status hm_trim(hm_ctx ctx);
 const char* hm_version(void);
 
 /*

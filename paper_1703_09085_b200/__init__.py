@@ -94,6 +94,10 @@ class Context:
     def sync(self):
         self.check(lib().hm_sync(self.h))
 
+    def trim(self):
+        """Give back the context's workspaces and cached pool memory (hm_trim)."""
+        self.check(lib().hm_trim(self.h))
+
     # ---- construction
     def build(self, points, areas, leaf_size, eta, eps, kernel=0, normals=None):
         """kernel 0: single layer G, 1: (G+G^T)/2, 2: double layer K + I/2 (needs normals)."""

@@ -72,7 +72,7 @@ class Prof(C.Structure):
 
 
 EXPORTS = [
-    "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_build", "hm_build_nrm",
+    "hm_version", "hm_ctx_create", "hm_ctx_destroy", "hm_last_error", "hm_sync", "hm_trim", "hm_build", "hm_build_nrm",
     "hm_import", "hm_export", "hm_export_sizes", "hm_export_into", "hm_clone", "hm_free", "hm_addmul", "hm_addmul_std",
     "hm_lr", "hm_chol", "hm_inv",
     "hm_matvec_thin", "hm_solve_thin", "hm_precond_error", "hm_stats", "hm_profile_enable", "hm_profile_reset", "hm_profile_get",
@@ -94,6 +94,7 @@ def load(path: str = LIB_PATH):
         "hm_ctx_destroy": (C.c_int, [vp]),
         "hm_last_error": (C.c_char_p, [vp]),
         "hm_sync": (C.c_int, [vp]),
+        "hm_trim": (C.c_int, [vp]),
         "hm_build": (C.c_int, [vp, P_f64, P_f64, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,
                                C.POINTER(vp), P_i64]),
         "hm_build_nrm": (C.c_int, [vp, P_f64, P_f64, P_f64, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,

@@ -221,6 +221,14 @@ hm_status hm_sync(hm_ctx ctx) {
   return guard(ctx, [&] { HM_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
 }
 
+hm_status hm_trim(hm_ctx ctx) {
+  if (!ctx) return HM_EINVAL;
+  return guard(ctx, [&] {
+    set_device(ctx->c);
+    ctx->c.trim();
+  });
+}
+
 hm_status hm_import(hm_ctx ctx, const hm_host_desc* d, hm_mat* out) {
   if (!ctx || !d || !out) return HM_EINVAL;
   return guard(ctx, [&] {
@@ -428,6 +436,9 @@ hm_status hm_build_nrm(hm_ctx ctx, const double* pts_host, const double* area_ho
     if (kernel != HM_KERNEL_SLP && kernel != HM_KERNEL_SLP_SYM && kernel != HM_KERNEL_DLP)
       throw Error(HM_EINVAL, "hm_build: unknown kernel");
     if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_build: eps must be >= 0");
+    // the build's temporaries are the largest allocations of a session: the
+    // workspaces earlier operations left behind are given back first
+    ctx->c.trim(false);
     Mat* M = build_matrix(&ctx->c, pts_host, area_host, nrm_host, n, kernel, leaf_size, eta, eps, perm_host);
     auto* H = new hm_mat_s;
     H->m = std::move(*M);

@@ -50,6 +50,20 @@ int* Ctx::rank_alloc(size_t n) {
   return p;
 }
 
+void Ctx::trim(bool captures) {
+  HM_CUDA(cudaStreamSynchronize(stream));
+  if (captures) cap_free();
+  if (ws) dfree(ws, ws_cap * sizeof(double));
+  ws = nullptr;
+  ws_cap = 0;
+  if (sp) dfree(sp, sp_cap);
+  sp = nullptr;
+  sp_cap = 0;
+  sp_top = 0;
+  HM_CUDA(cudaStreamSynchronize(stream));
+  if (pool) cudaMemPoolTrimTo(pool, 0);
+}
+
 void Ctx::cap_free() {
   for (auto& L : cap)
     if (L.data) dfree(L.data, L.ndoubles * sizeof(double));

@@ -107,6 +107,10 @@ struct Ctx {
   double* ws = nullptr;
   size_t ws_cap = 0;
   double* stack_ws(size_t ndoubles);
+  // Give back the grow-only workspaces (level stacks, LIFO pool, captured
+  // flush data) and the private pool's cached memory (hm_trim; also at the
+  // start of hm_build, whose temporaries are the largest allocations).
+  void trim(bool captures = true);
   // grow-only LIFO pool for arenas in stack mode (factor outputs of one
   // operation); overflow falls back to cudaMallocAsync chunks and the pool is
   // resized to the high-water mark at the next operation start
