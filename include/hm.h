@@ -158,7 +158,8 @@ hm_status hm_sync(hm_ctx ctx);
 /* Synchronises the stream and gives back the context's grow-only workspaces
  * (level stacks, LIFO pool, captured flush batches) and the memory its private
  * pool has cached; live hm_mat handles are untouched.  The next operation
- * re-grows what it needs.  hm_build / hm_build_nrm call it first. */
+ * re-grows what it needs.  hm_build / hm_build_nrm call it and retry once
+ * when they run out of device memory. */
 hm_status hm_trim(hm_ctx ctx);
 const char* hm_version(void);
 

@@ -436,10 +436,18 @@ hm_status hm_build_nrm(hm_ctx ctx, const double* pts_host, const double* area_ho
     if (kernel != HM_KERNEL_SLP && kernel != HM_KERNEL_SLP_SYM && kernel != HM_KERNEL_DLP)
       throw Error(HM_EINVAL, "hm_build: unknown kernel");
     if (!(eps >= 0.0)) throw Error(HM_EINVAL, "hm_build: eps must be >= 0");
-    // the build's temporaries are the largest allocations of a session: the
-    // workspaces earlier operations left behind are given back first
-    ctx->c.trim(false);
-    Mat* M = build_matrix(&ctx->c, pts_host, area_host, nrm_host, n, kernel, leaf_size, eta, eps, perm_host);
+    // the build's temporaries are the largest allocations of a session: if it
+    // runs out of memory, the workspaces earlier operations left behind are
+    // given back (hm_trim) and it is tried once more
+    Mat* M = nullptr;
+    try {
+      M = build_matrix(&ctx->c, pts_host, area_host, nrm_host, n, kernel, leaf_size, eta, eps, perm_host);
+    } catch (const Error& e) {
+      if (e.code != HM_ENOMEM) throw;
+      cudaGetLastError();
+      ctx->c.trim(false);
+      M = build_matrix(&ctx->c, pts_host, area_host, nrm_host, n, kernel, leaf_size, eta, eps, perm_host);
+    }
     auto* H = new hm_mat_s;
     H->m = std::move(*M);
     delete M;
