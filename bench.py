@@ -532,6 +532,8 @@ def run_ours(args, cfg):
             if cfg["level"] < 6 and L > 5:
                 continue
             xf, wf = sphere_points(L)
+            if L >= 7:
+                ctx.trim()   # the n = 327680 build needs the workspaces the earlier legs left behind
             tb = time.time()
             G0 = ctx.build(xf, wf, leaf, 2.0, eps, kernel=kern)
             tb = time.time() - tb
