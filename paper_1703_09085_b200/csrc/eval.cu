@@ -95,6 +95,57 @@ __device__ __forceinline__ void acc_zero(double (&acc)[WarpTiling<MT, NCT>::RTW 
   for (int t = 0; t < WarpTiling<MT, NCT>::RTW * WarpTiling<MT, NCT>::CTW; t++) acc[t][0] = acc[t][1] = 0.0;
 }
 
+// The old values of the warp's output fragments, loaded BEFORE the tile is
+// computed (the read-modify-write of store_acc was k_eval2's long-scoreboard
+// stall: the load latency now overlaps the staging and the DMMA work).
+template <int NCT>
+__device__ __forceinline__ void load_out(const EvalJob& J, int orow, int ocol, int i0, int mc, int j0, int wc,
+                                         double (&old)[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2]) {
+  using WT = WarpTiling<8, NCT>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < WT::RTW * WT::CTW; t++) old[t][0] = old[t][1] = 0.0;
+  if (warp >= WT::RG * WT::CG) return;
+  const int rg = warp % WT::RG, cg = warp / WT::RG;
+#pragma unroll
+  for (int r = 0; r < WT::RTW; r++) {
+    const int i = (rg * WT::RTW + r) * 8 + (lane >> 2);
+    if (i >= mc) continue;
+    const double* o = J.out + (orow + i0 + i);
+#pragma unroll
+    for (int c = 0; c < WT::CTW; c++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int j = (cg * WT::CTW + c) * 8 + 2 * (lane & 3) + h;
+        if (j < wc) old[r * WT::CTW + c][h] = o[(int64_t)(ocol + j0 + j) * J.ldo];
+      }
+  }
+}
+
+// out[orow + i0 + i, ocol + j0 + j] = old + coef * D(i, j) for i < mc, j < wc
+template <int NCT>
+__device__ __forceinline__ void store_acc_old(const EvalJob& J, int orow, int ocol, int i0, int mc, int j0, int wc,
+                                              const double (&acc)[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2],
+                                              const double (&old)[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2]) {
+  using WT = WarpTiling<8, NCT>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp >= WT::RG * WT::CG) return;
+  const int rg = warp % WT::RG, cg = warp / WT::RG;
+#pragma unroll
+  for (int r = 0; r < WT::RTW; r++) {
+    const int i = (rg * WT::RTW + r) * 8 + (lane >> 2);
+    if (i >= mc) continue;
+    double* o = J.out + (orow + i0 + i);
+#pragma unroll
+    for (int c = 0; c < WT::CTW; c++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int j = (cg * WT::CTW + c) * 8 + 2 * (lane & 3) + h;
+        if (j < wc) o[(int64_t)(ocol + j0 + j) * J.ldo] = fma(J.coef, acc[r * WT::CTW + c][h], old[r * WT::CTW + c][h]);
+      }
+  }
+}
+
 // out[orow + i0 + i, ocol + j0 + j] += coef * D(i, j) for i < mc, j < wc
 template <int NCT>
 __device__ __forceinline__ void store_acc(const EvalJob& J, int orow, int ocol, int i0, int mc, int j0, int wc,
@@ -157,7 +208,9 @@ __device__ void dense_tiles(const EvalJob& J, const LeafDesc& L, int orow, int v
   for (int i0 = 0; i0 < mo; i0 += kT) {
     const int mc = min(kT, mo - i0);
     double acc[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
+    double old[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
     acc_zero<8, NCT>(acc);
+    load_out<NCT>(J, orow, 0, i0, mc, j0, wc, old);
     for (int p0 = 0; p0 < ko; p0 += kT) {
       const int pc = min(kT, ko - p0), pcp = (pc + 3) & ~3;
       int ars, acs, brs, bcs;
@@ -187,7 +240,7 @@ __device__ void dense_tiles(const EvalJob& J, const LeafDesc& L, int orow, int v
       tile_dmma<8, NCT>(S, ars, acs, Vs, brs, bcs, (pc + 3) & ~3, acc);
       __syncthreads();
     }
-    store_acc<NCT>(J, orow, 0, i0, mc, j0, wc, acc);
+    store_acc_old<NCT>(J, orow, 0, i0, mc, j0, wc, acc, old);
   }
 }
 
@@ -209,6 +262,8 @@ __device__ void apply_f1_t(const EvalJob& J, const double* F1, int ld1, int mo, 
   const int kcp = (kc + 3) & ~3;
   for (int i0 = 0; i0 < mo; i0 += kT) {
     const int mc = min(kT, mo - i0);
+    double old[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
+    load_out<NCT>(J, orow, ocol, i0, mc, j0, wc, old);
     for (int e = tid; e < kT * kcp; e += kNT) {   // S[i + q * 68] = F1(i0 + i, q0 + q)
       const int i = e & (kT - 1), q = e >> 6;
       if (i >= mc) continue;
@@ -220,7 +275,7 @@ __device__ void apply_f1_t(const EvalJob& J, const double* F1, int ld1, int mo, 
     double acc[WarpTiling<8, NCT>::RTW * WarpTiling<8, NCT>::CTW][2];
     acc_zero<8, NCT>(acc);
     tile_dmma<8, NCT>(S, 1, kLd, Ts, kLdJ, 1, (kc + 3) & ~3, acc);
-    store_acc<NCT>(J, orow, ocol, i0, mc, j0, wc, acc);
+    store_acc_old<NCT>(J, orow, ocol, i0, mc, j0, wc, acc, old);
     __syncthreads();
   }
 }
