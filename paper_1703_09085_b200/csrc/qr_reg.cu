@@ -318,25 +318,32 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_qr_reg(const QrJob* __restr
           for (int ks = 0; ks < 4; ks++)
             bz[ct][ks] = (ct < nct && ct * 8 + lr < wcb) ? Wz[(ks * 4 + lk) + (ct * 8 + lr) * 16] : 0.0;
         const int nrt = (rows + 7) >> 3;
-        for (int rt = warp; rt < nrt; rt += NW) {
-          {   // this warp's tile after next: one 64-byte segment per column
-            const int pi = (rt + 2 * NW) * 8;
-            if (pi < rows)
-              for (int pc = lane; pc < wcb; pc += 32) prefetch_l1(At + pi + (int64_t)(cb + pc) * lda);
-          }
+        // software pipeline: the C fragments of the warp's NEXT row tile are
+        // loaded before the DMMAs of the current one (the loads' L2 latency was
+        // exposed once per tile)
+        auto load_c = [&](int rt, auto& cc) {
           const int i = rt * 8 + lr;
-          const bool iok = i < rows;
-          double av[4];
-#pragma unroll
-          for (int ks = 0; ks < 4; ks++) av[ks] = iok ? Vs[i + (ks * 4 + lk) * ldp] : 0.0;
-          double c2[NW][2];
+          const bool iok = rt < nrt && i < rows;
 #pragma unroll
           for (int ct = 0; ct < NW; ct++)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
               const int jj = ct * 8 + 2 * lk + h;
-              c2[ct][h] = (ct < nct && iok && jj < wcb) ? At[i + (int64_t)(cb + jj) * lda] : 0.0;
+              cc[ct][h] = (ct < nct && iok && jj < wcb) ? At[i + (int64_t)(cb + jj) * lda] : 0.0;
             }
+        };
+        // (128-thread variants only: with 8 warps the 2 x 16 fragment registers spill)
+        constexpr bool kPipe = NW <= 4;
+        double c2[NW][2], c2n[kPipe ? NW : 1][2];
+        if (kPipe) load_c(warp, c2);
+        for (int rt = warp; rt < nrt; rt += NW) {
+          const int i = rt * 8 + lr;
+          const bool iok = i < rows;
+          double av[4];
+#pragma unroll
+          for (int ks = 0; ks < 4; ks++) av[ks] = iok ? Vs[i + (ks * 4 + lk) * ldp] : 0.0;
+          if constexpr (kPipe) load_c(rt + NW, c2n);
+          else load_c(rt, c2);
 #pragma unroll
           for (int ct = 0; ct < NW; ct++)
             if (ct < nct) {   // warp-uniform
@@ -349,6 +356,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_qr_reg(const QrJob* __restr
             for (int h = 0; h < 2; h++) {
               const int jj = ct * 8 + 2 * lk + h;
               if (ct < nct && iok && jj < wcb) At[i + (int64_t)(cb + jj) * lda] = c2[ct][h];
+              if constexpr (kPipe) c2[ct][h] = c2n[ct][h];
             }
         }
       }
