@@ -61,24 +61,31 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
       std::fclose(f);
     }
   }
-  std::vector<TruncSmallJob> fb[3];
-  const int fcap[3] = {4 * 1024, 10 * 1024, 26 * 1024};
+  // (13 K doubles = 104 KB: the largest working set of which two CTAs share an SM)
+  constexpr int kFB = 4;
+  std::vector<TruncSmallJob> fb[kFB];
+  const int fcap[kFB] = {4 * 1024, 10 * 1024, 13 * 1024, 26 * 1024};
   std::vector<TruncReq> rest;
   static const bool no_fused = std::getenv("HM_NO_FUSED") != nullptr;
   double fl = 0, by = 0;
   for (const TruncReq& r : reqs) {
     const int need = trunc_small_need(r.m, r.n, r.l);
     int b = -1;
-    for (int k = 0; k < 3; k++)
+    for (int k = 0; k < kFB; k++)
       if (need <= fcap[k]) { b = k; break; }
     if (b < 0 || no_fused) { rest.push_back(r); continue; }
     fb[b].push_back(TruncSmallJob{r.A, r.B, r.m, r.n, r.l, r.Aout, r.Bout, r.d_rank, r.d_sigma});
     fl += trunc_flops(r.m, r.n, r.l, 0.0);   // convention flops (reform term k unknown here)
     by += trunc_bytes(r.m, r.n, r.l, 0.0);
   }
+  // few stacks (latency-bound steps): the 13 K and 26 K buckets share one launch
+  if (!fb[2].empty() && fb[2].size() + fb[3].size() < 296) {
+    fb[3].insert(fb[3].end(), fb[2].begin(), fb[2].end());
+    fb[2].clear();
+  }
   if (c->plog) {
     int mx = 0, ml = 0, nf = 0;
-    for (int b = 0; b < 3; b++)
+    for (int b = 0; b < kFB; b++)
       for (auto& j : fb[b]) { mx = std::max(mx, std::max(j.m, j.n)); ml = std::max(ml, j.l); nf++; }
     c->prof_note("fused jobs " + std::to_string(nf) + " maxmn " + std::to_string(mx) + " maxl " + std::to_string(ml) +
                  " staged " + std::to_string(rest.size()));
@@ -87,9 +94,9 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
   // independent: the fused kernels run on an auxiliary stream next to it
   bool forked = false;
   {
-    const TruncSmallJob* dj[3];
+    const TruncSmallJob* dj[kFB];
     bool any = false;
-    for (int b = 0; b < 3; b++) {
+    for (int b = 0; b < kFB; b++) {
       dj[b] = fb[b].empty() ? nullptr : ar.upload_t(fb[b]);
       any = any || dj[b];
     }
@@ -97,7 +104,7 @@ void trunc_batched(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, double 
       forked = !rest.empty() && c->multi_stream();
       cudaStream_t sf = forked ? c->fork(0) : c->stream;
       ProfScope ps(c, PC_FUSED, fl, by, sf);
-      for (int b = 0; b < 3; b++)
+      for (int b = 0; b < kFB; b++)
         if (dj[b]) launch_trunc_small(dj[b], (int)fb[b].size(), eps, fcap[b], sf);
       HM_CHECK_LAUNCH();
     }
@@ -401,6 +408,7 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
   // --- SVD jobs; matrices too large for shared memory are first reduced by an
   // unpivoted blocked QR (Mt = Q1 R1) and the SVD kernel works on R1 (c x c).
   std::vector<SvdJob> sj[5];   // 3 shared-memory buckets, global workspace, spill mode
+  std::vector<SvdJob> sj13;    // the part of the 26 K bucket that fits 13 K doubles
   int caps[4] = {3 * 1024, 8 * 1024, 26 * 1024, 0};
   double fl_svd = 0, fl_b[5] = {0, 0, 0, 0, 0};
   const char* dump = std::getenv("HM_DUMP_JOBS");
@@ -461,7 +469,8 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
     fl_b[b] += 22.0 * (double)cc * cc * cc;
     bucket_of[i] = b;
     if (b >= 3) s.work = ar.alloc((size_t)need);
-    sj[b].push_back(s);
+    if (b == 2 && need <= 13 * 1024) sj13.push_back(s);   // two CTAs per SM (104 KB)
+    else sj[b].push_back(s);
   }
   c->prof_note(shapes);
   {
@@ -472,6 +481,15 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       dsj[b] = sj[b].empty() ? nullptr : ar.upload_t(sj[b]);
       used += dsj[b] ? 1 : 0;
     }
+    // few matrices (latency-bound steps): one launch, so that they run concurrently
+    if (!sj13.empty() && sj13.size() + sj[2].size() < 296) {
+      sj[2].insert(sj[2].end(), sj13.begin(), sj13.end());
+      sj13.clear();
+      dsj[2] = ar.upload_t(sj[2]);
+    }
+    const SvdJob* d13 = sj13.empty() ? nullptr : ar.upload_t(sj13);   // (uploads before any fork)
+    used = d13 ? 1 : 0;
+    for (int b = 0; b < 5; b++) used += dsj[b] ? 1 : 0;
     const bool par = used > 1 && c->multi_stream();
     for (int b = 4; b >= 0; b--) {   // the largest problems first; spill mode shares the global bucket's stream
       if (!dsj[b]) continue;
@@ -481,9 +499,14 @@ static void trunc_general(Ctx* c, Arena& ar, const std::vector<TruncReq>& reqs, 
       if (b == 4) launch_svd_spill(dsj[b], (int)sj[b].size(), eps, sb);
       else launch_svd(dsj[b], (int)sj[b].size(), eps, caps[b], sb);
     }
+    if (d13) {
+      cudaStream_t sb = par ? c->fork(1 + 2) : st;
+      ProfScope pb(c, PC_SVD_B0 + 2, 0, (double)sj13.size(), sb);
+      launch_svd(d13, (int)sj13.size(), eps, 13 * 1024, sb);
+    }
     if (par)
       for (int b = 0; b < 4; b++)
-        if (dsj[b] || (b == 3 && dsj[4])) c->join(1 + b);
+        if (dsj[b] || (b == 3 && dsj[4]) || (b == 2 && !sj13.empty())) c->join(1 + b);
     HM_CHECK_LAUNCH();
   }
   if (dump) {

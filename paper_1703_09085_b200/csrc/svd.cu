@@ -1125,7 +1125,7 @@ void launch_trunc_small(const TruncSmallJob* d_jobs, int njobs, double eps, int 
   }();
   (void)tl_init;
   const int bk = cap <= 4 * 1024 ? 0 : (cap <= 10 * 1024 ? 1 : 2);
-  int threads = njobs < 296 ? tlat[bk] : (cap > 10 * 1024 ? t26 : 256);
+  int threads = njobs < 296 ? tlat[bk] : (cap > 13 * 1024 ? t26 : 256);
   if (tsmall > 0 && njobs >= 296 && cap <= 4 * 1024) threads = tsmall;
   k_trunc_small<<<njobs, threads, (size_t)cap * 8, st>>>(d_jobs, eps, drop_rel_host());
 }
@@ -1139,7 +1139,7 @@ void launch_svd(const SvdJob* d_jobs, int njobs, double eps, int cap, cudaStream
   ensure_smem_attr((const void*)k_svd, kSpillCap * 8);
   if (cap > svd_smem_capacity()) cap = svd_smem_capacity();
   static const int tg = [] { const char* e = std::getenv("HM_SVDG_THREADS"); return e ? std::atoi(e) : 512; }();
-  int threads = (cap == 0 || cap > 8 * 1024 || njobs < 296) ? 512 : 256;
+  int threads = (cap == 0 || cap > 13 * 1024 || njobs < 296) ? 512 : 256;
   if (cap == 0) threads = tg;   // global workspace: no shared-memory limit on CTAs per SM
   // latency mode (few matrices): threads per CTA, HM_SVD_LAT (0 = the default above)
   static const int tlat = [] { const char* e = std::getenv("HM_SVD_LAT"); return e ? std::atoi(e) : 0; }();
